@@ -1,0 +1,259 @@
+/*
+ * cszi.h — C ABI of libcszi.so, the B200-native (sm_100a) cuSZ-i hot path.
+ *
+ * The reference package (ebcomp, pure Python + numba) has no native FFI; its
+ * drop-in boundary is the Python API  ebcomp.compress / ebcomp.decompress
+ * (pkg/src/ebcomp/pipeline.py:66-78, :166).  Each entry point below replaces
+ * one stage of that path and cites the reference function whose semantics it
+ * reproduces bit-for-bit.  The Python host layer (paper_2312_05492_b200/) is
+ * the only caller; see INTEGRATION.md for the ctypes binding.
+ *
+ * Conventions
+ *  - extern "C", no exceptions cross the ABI; every function returns an int
+ *    status (CSZI_OK or a negative CSZI_E_* code; the E_* codes map 1:1 onto
+ *    the ebcomp.errors classes, CSZI_E_CUDA is a CUDA runtime failure).
+ *  - All device pointers are caller-owned (torch tensors on the host side);
+ *    scratch comes from a caller-provided workspace sized by the matching
+ *    *_workspace_size() query.  Sizes and indices are 64-bit everywhere.
+ *  - Every call is stream-ordered on the caller's cudaStream_t (passed as
+ *    void*) and returns without synchronising; results that are data
+ *    dependent (bit counts, outlier counts, payload length, tuned config,
+ *    error flags) are written into a device-resident cszi_ctl record that
+ *    the caller copies back once at the end.
+ *  - Grids are 1..3-D float32, C order, slowest axis first (grid.py:19-38).
+ *    Internally a rank-r grid is padded to 3-D with leading extent-1 axes.
+ */
+#ifndef CSZI_H
+#define CSZI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.py:8-95) ------------------------------------- */
+#define CSZI_OK 0
+#define CSZI_E_NONFINITE (-1)        /* NonFiniteValue      grid.py:60-62     */
+#define CSZI_E_INCONSISTENT (-2)     /* Inconsistent        predictor.py:150  */
+#define CSZI_E_LENGTH_OVERFLOW (-3)  /* LengthOverflow      huffman.py:97     */
+#define CSZI_E_EMPTY_HISTOGRAM (-4)  /* EmptyHistogram      huffman.py:82     */
+#define CSZI_E_TRUNCATED (-5)        /* TruncatedStream     huffman.py:200    */
+#define CSZI_E_CORRUPT (-6)          /* Corrupt             pass2.py:80       */
+#define CSZI_E_MALFORMED (-7)        /* MalformedSection    archive.py:195    */
+#define CSZI_E_UNKNOWN_SYMBOL (-8)   /* UnknownSymbol       huffman.py:176    */
+#define CSZI_E_OUT_OF_RANGE (-9)     /* OutOfRange          huffman.py:71     */
+#define CSZI_E_LENGTH_MISMATCH (-10) /* LengthMismatch      archive.py:155    */
+#define CSZI_E_OUTLIER_INDEX (-11)   /* outlier index >= n (numpy IndexError) */
+#define CSZI_E_INVALID_ARG (-20)
+#define CSZI_E_UNSUPPORTED (-21)
+#define CSZI_E_CAPACITY (-22) /* a caller buffer is smaller than the data */
+#define CSZI_E_CUDA (-30)
+
+/* Bits of cszi_ctl.flags (device-detected conditions; host raises in the
+ * reference's check order). */
+#define CSZI_F_NONFINITE (1u << 0)
+#define CSZI_F_EB_NONPOSITIVE (1u << 1)
+#define CSZI_F_LENGTH_OVERFLOW (1u << 2)
+#define CSZI_F_EMPTY_HISTOGRAM (1u << 3)
+#define CSZI_F_TRUNCATED (1u << 4)
+#define CSZI_F_P2_CORRUPT (1u << 5)
+#define CSZI_F_P2_LENGTH (1u << 6)
+#define CSZI_F_OUTLIER_COUNT (1u << 7)
+#define CSZI_F_OUTLIER_ORDER (1u << 8)
+#define CSZI_F_OUTLIER_INDEX (1u << 9)
+#define CSZI_F_CAPACITY (1u << 10)
+#define CSZI_F_UNKNOWN_SYMBOL (1u << 11)
+
+#define CSZI_MAX_LEVELS 16
+
+/* Padded-3D geometry of one grid plus its predictor layout
+ * (predictor.py:79-105 ChunkLayout, pipeline.py:159-163 _layout_for). */
+typedef struct cszi_geom {
+  int32_t rank;        /* 1..3 (original rank)                            */
+  int32_t pad_;
+  int64_t ext[3];      /* padded extents, slowest first                   */
+  int64_t stride;      /* anchor stride S (power of two)                  */
+  int64_t tile[3];     /* super-chunk tile per padded axis (1 if padded)  */
+} cszi_geom;
+
+/* Host-provided compression parameters (pipeline.py:66-101). */
+typedef struct cszi_params {
+  int32_t mode_rel;        /* 1 = "rel", 0 = "abs"                         */
+  int32_t radius;          /* quant_radius R (>= 2)                        */
+  double eb;               /* eb as given                                  */
+  int32_t have_alpha;      /* alpha known on the host (override or rel)    */
+  int32_t have_variants;   /* variants override                            */
+  int32_t have_order;      /* dim_order override                           */
+  int32_t pad_;
+  double alpha;            /* used when have_alpha                          */
+  double alpha_pow[CSZI_MAX_LEVELS]; /* alpha ** (level-1), level = 1..    */
+  int32_t variant[3];      /* padded-axis variants (override)               */
+  int32_t order[3];        /* padded-axis dim order (override), rank items  */
+  int32_t exact;           /* 1: force the true-division quantizer          */
+  int32_t pad2_;
+} cszi_params;
+
+/* Device-resident control record: written by kernels, copied back once.  */
+typedef struct cszi_ctl {
+  /* range reduction (grid.py:104-108, grid.py:60-62) */
+  uint32_t vmin_key;       /* order-preserving float keys (atomicMin/Max)  */
+  uint32_t vmax_key;
+  uint64_t first_nonfinite; /* UINT64_MAX when every value is finite        */
+  /* tuned configuration (tuning.py:93-129) */
+  double vmin, vmax, rng;
+  double eb_abs, alpha;
+  double level_eb[CSZI_MAX_LEVELS]; /* coarse -> fine                       */
+  double inv_e2[CSZI_MAX_LEVELS];   /* 1 / (2 * level_eb)                  */
+  double err_sum[3][2];
+  int64_t sample_count[3];
+  int32_t variant[3];      /* padded-axis variants                          */
+  int32_t order[3];        /* padded-axis pass order (rank items used)      */
+  int32_t nlev;
+  int32_t radius;
+  /* entropy stage */
+  uint64_t bits;           /* Huffman bitstream length in bits              */
+  uint64_t n_outliers;
+  uint64_t raw_len;        /* sections concatenated (pre pass-2)            */
+  uint64_t payload_len;    /* stored payload (post pass-2)                  */
+  uint64_t decoded_symbols;
+  uint32_t flags;          /* CSZI_F_* */
+  uint32_t max_len;        /* longest code length                           */
+  uint64_t scratch[8];
+} cszi_ctl;
+
+/* ---- whole-path entry points ------------------------------------------ */
+
+/* Capacities for data-dependent outputs.  If a run overflows one of them,
+ * CSZI_F_CAPACITY is set and the caller retries with larger values (the
+ * worst case is bits_cap = 4*n bytes, outlier_cap = n). */
+typedef struct cszi_caps {
+  uint64_t bits_cap;     /* bytes for the Huffman bitstream              */
+  uint64_t outlier_cap;  /* outlier records                               */
+} cszi_caps;
+
+/* Workspace bytes for cszi_compress on a grid of this geometry. */
+uint64_t cszi_compress_workspace_size(const cszi_geom *g, int32_t radius, const cszi_caps *caps);
+
+/* Device payload capacity (bytes) for cszi_compress. */
+uint64_t cszi_payload_capacity(const cszi_geom *g, int32_t radius, const cszi_caps *caps);
+
+/*
+ * compress — pipeline.py:66-156 for predictor="interp", pass-2 codec 0.
+ * x: device float32[n].  range_done != 0: ctl already holds the range and
+ * finite scan of x (cszi_range ran at Grid construction) — only the output
+ * fields are reset.  Writes the stored payload (pass-2 encoded when
+ * pass2 != 0, else the raw section concatenation) to `payload`, and the
+ * tuned config, section lengths (ctl->bits, n_outliers, raw_len,
+ * payload_len) and CSZI_F_* flags to ctl.
+ */
+int cszi_compress(const float *x, const cszi_geom *g, const cszi_params *p,
+                  const cszi_caps *caps, int32_t pass2, int32_t range_done, uint8_t *payload,
+                  void *workspace, uint64_t ws_bytes, cszi_ctl *ctl, void *stream);
+
+/* Workspace bytes for cszi_decompress. */
+uint64_t cszi_decompress_workspace_size(const cszi_geom *g, int32_t radius,
+                                        const uint64_t sec_len[4], uint64_t payload_len);
+
+/*
+ * decompress — pipeline.py:166-204 (predictor="interp").
+ * payload: device bytes of the stored payload; sec_len: the four
+ * pre-pass-2 section lengths from the header; level_eb: eb_abs /
+ * alpha ** (level-1) coarse -> fine (computed by the host as plan_levels
+ * does); variant/order: padded-axis ids.  table_mode != 0 forces the exact
+ * transfer-table Huffman decode (used when ctl->scratch[1] reports that the
+ * speculative decode did not converge).  Writes y (float32[n]).
+ */
+int cszi_decompress(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
+                    const uint64_t sec_len[4], const cszi_geom *g, int32_t radius,
+                    const double *level_eb, int32_t nlev, const int32_t variant[3],
+                    const int32_t order[3], int32_t table_mode, float *y, void *workspace,
+                    uint64_t ws_bytes, cszi_ctl *ctl, void *stream);
+
+/* ---- stage entry points (fine-grained API of the reference) ------------ */
+
+/* ctl := initial state (range keys reset, counters and flags zero). */
+int cszi_ctl_init(cszi_ctl *ctl, void *stream);
+
+/* value_range + finite scan (grid.py:60-62, :104-108) into ctl. */
+int cszi_range(const float *x, uint64_t n, cszi_ctl *ctl, void *stream);
+
+/* profile_samples + select_config + plan_levels (tuning.py:42-129,
+ * predictor.py:122-136) on a ctl holding the range of x. */
+int cszi_tune(const float *x, const cszi_geom *g, const cszi_params *p, cszi_ctl *ctl,
+              void *stream);
+
+/* compress_predict (predictor.py:395-420) on a tuned ctl:
+ * sym uint16[n] = q + R (0 for outliers, R at anchors), hist uint64[2R]
+ * (outliers and anchors counted as symbol R).  exact != 0 forces the
+ * true-division quantizer (validation of the reciprocal fast path). */
+int cszi_predict(const float *x, const cszi_geom *g, int32_t radius, int32_t exact,
+                 uint16_t *sym, uint64_t *hist, cszi_ctl *ctl, void *stream);
+
+/* Inverse interpolation (predictor.py:423-465) from uint16 symbols
+ * (0xFFFF marks an outlier whose value is found in out_idx/out_val). */
+int cszi_reconstruct(const uint16_t *sym, const float *anchors, const uint64_t *out_idx,
+                     const float *out_val, uint64_t n_out, const cszi_geom *g, int32_t radius,
+                     const double *level_eb, int32_t nlev, const int32_t variant[3],
+                     const int32_t order[3], float *y, void *stream);
+
+/* gather_anchors (predictor.py:250-256): lattice row-major float32 values. */
+int cszi_gather_anchors(const float *x, const cszi_geom *g, float *out, void *stream);
+
+/* build_histogram (huffman.py:60-74): int32 codes -> uint64[2R];
+ * out-of-range codes set bit 31 of ctl->flags. */
+int cszi_histogram_i32(const int32_t *codes, uint64_t n, int32_t radius, uint64_t *counts,
+                       cszi_ctl *ctl, void *stream);
+
+/* _code_lengths + canonical words (huffman.py:77-160):
+ * counts uint64[nbins] -> lengths uint8[nbins], words uint32[nbins]. */
+int cszi_codebook(const uint64_t *counts, uint32_t nbins, uint8_t *lengths, uint32_t *words,
+                  cszi_ctl *ctl, void *stream);
+
+/* Codebook.from_lengths (huffman.py:128-160): canonical words and, when
+ * dec_tables != NULL, the decoder tables (cszi_dec_tables_size bytes). */
+uint64_t cszi_dec_tables_size(uint32_t nbins);
+int cszi_canonical(const uint8_t *lengths, uint32_t nbins, uint32_t *words, void *dec_tables,
+                   cszi_ctl *ctl, void *stream);
+
+/* huffman_encode (huffman.py:167-182): int32 codes -> MSB-first stream in
+ * out (cap bytes, 4-byte aligned); ctl->bits <- exact bit count. */
+uint64_t cszi_huff_encode_workspace_size(uint64_t n);
+int cszi_huff_encode_i32(const int32_t *codes, uint64_t n, int32_t radius,
+                         const uint8_t *lengths, const uint32_t *words, uint8_t *out,
+                         uint64_t cap, void *workspace, cszi_ctl *ctl, void *stream);
+
+/* huffman_decode (huffman.py:185-202): exactly n int32 codes from nbytes
+ * of stream; CSZI_F_TRUNCATED in ctl->flags on failure. */
+uint64_t cszi_huff_decode_workspace_size(uint64_t nbytes, int32_t table_mode);
+int cszi_huff_decode_i32(const uint8_t *stream_bytes, uint64_t nbytes, uint64_t n,
+                         int32_t radius, const void *dec_tables, int32_t *codes,
+                         int32_t table_mode, int32_t lmax, void *workspace, cszi_ctl *ctl,
+                         void *stream);
+
+/* pass2_encode codec 0 (pass2.py:50-67): ctl->payload_len <- output size;
+ * out capacity >= n + n/128 + 1.  n_dev: device pointer to the byte count
+ * (n is its upper bound). */
+uint64_t cszi_pass2_encode_workspace_size(uint64_t n);
+int cszi_pass2_encode(const uint8_t *in, const uint64_t *n_dev, uint64_t n, uint8_t *out,
+                      void *workspace, cszi_ctl *ctl, void *stream);
+
+/* pass2_decode codec 0 (pass2.py:70-86): ctl->raw_len <- decoded size
+ * (always); with expand != 0 also writes out (cap bytes).  Literal overrun
+ * sets CSZI_F_P2_CORRUPT; cap overflow sets CSZI_F_CAPACITY. */
+uint64_t cszi_pass2_decode_workspace_size(uint64_t n);
+int cszi_pass2_decode(const uint8_t *in, uint64_t n, uint8_t *out, uint64_t cap,
+                      int32_t expand, void *workspace, cszi_ctl *ctl, void *stream);
+
+/* Library build identification. */
+const char *cszi_version(void);
+
+/* sizeof(cszi_geom), sizeof(cszi_params), sizeof(cszi_caps), sizeof(cszi_ctl)
+ * — lets a binding verify its struct mirrors at load time. */
+void cszi_abi_sizes(uint64_t out[4]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CSZI_H */

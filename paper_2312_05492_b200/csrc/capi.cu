@@ -1,0 +1,462 @@
+// extern "C" entry points of libcszi.so (see include/cszi.h) and the
+// stream-ordered orchestration of the compress / decompress paths
+// (pipeline.py:66-204).  No exceptions cross the ABI; no host sync inside.
+#include <cstring>
+
+#include "common.cuh"
+
+namespace cszi {
+int launch_ctl_init(cszi_ctl *ctl, cudaStream_t st);
+int launch_range(const float *x, uint64_t n, cszi_ctl *ctl, cudaStream_t st);
+int launch_tune(const float *x, const cszi_geom *g, const cszi_params *p, cszi_ctl *ctl,
+                cudaStream_t st);
+int launch_predict(const float *x, const cszi_geom *g, int32_t radius, const cszi_ctl *ctl,
+                   uint16_t *sym, u64 *hist, bool exact, cudaStream_t st);
+int launch_reconstruct(const uint16_t *sym, const float *anchors, const u64 *oidx,
+                       const float *oval, u64 nout, const u64 *nout_dev, const cszi_geom *g,
+                       int32_t radius,
+                       const double *leb, int nlev, const int32_t variant[3],
+                       const int32_t order[3], float *y, cudaStream_t st);
+int launch_gather_anchors(const float *x, const cszi_geom *g, float *out, cudaStream_t st);
+int launch_hist_i32(const int32_t *codes, u64 n, int R, u64 *hist, cszi_ctl *ctl,
+                    cudaStream_t st);
+int launch_codebook(const u64 *hist, int nbins, uint8_t *lengths, uint32_t *words,
+                    cszi_ctl *ctl, cudaStream_t st);
+size_t dec_tables_bytes(int nbins);
+int launch_canonical(const uint8_t *lengths, int nbins, uint32_t *words, void *dec_tables,
+                     cszi_ctl *ctl, cudaStream_t st);
+u64 enc_scratch_bytes(u64 n);
+int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *lengths,
+                  const uint32_t *words, uint32_t *out, u64 cap_bytes, const float *xval,
+                  u64 *o_idx, float *o_val, u64 o_cap, void *scratch, cszi_ctl *ctl,
+                  cudaStream_t st);
+u64 dec_scratch_bytes(u64 nbytes, int table_mode);
+int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *dec_tables,
+                  void *out, int out_kind, void *scratch, cszi_ctl *ctl, cudaStream_t st,
+                  int table_mode, int lmax);
+u64 p2enc_scratch_bytes(u64 n);
+int launch_pass2_encode(const uint8_t *in, const u64 *Np, u64 cap_n, uint8_t *out,
+                        void *scratch, cszi_ctl *ctl, cudaStream_t st);
+u64 p2dec_scratch_bytes(u64 n);
+int launch_pass2_decode(const uint8_t *in, u64 n, uint8_t *out, u64 cap, void *scratch,
+                        cszi_ctl *ctl, cudaStream_t st, int expand);
+
+// ---------------------------------------------------------------------------
+// small device helpers of the pipeline
+// ---------------------------------------------------------------------------
+// Reset the output fields of ctl, keeping the range of a prior cszi_range.
+__global__ void k_ctl_reset_outputs(cszi_ctl *ctl) {
+  ctl->bits = 0;
+  ctl->n_outliers = 0;
+  ctl->raw_len = 0;
+  ctl->payload_len = 0;
+  ctl->decoded_symbols = 0;
+  ctl->flags = 0;
+  ctl->max_len = 0;
+  for (int i = 0; i < 8; ++i) ctl->scratch[i] = 0;
+}
+
+// Sections after the anchors and codebook: bitstream bytes, then the
+// outlier section (archive.py:184-189: u64 count + packed (u64, f32)).
+__global__ void k_assemble(uint8_t *raw, u64 head, const uint8_t *bits, const u64 *oidx,
+                           const float *oval, u64 raw_cap, u64 bits_cap, u64 o_cap,
+                           cszi_ctl *ctl, int is_payload) {
+  const u64 nbits = ctl->bits;
+  const u64 k = ctl->n_outliers;
+  const u64 nbytes = (nbits + 7) / 8;
+  const u64 total = head + nbytes + 8 + 12 * k;
+  if (total > raw_cap || nbytes > bits_cap || k > o_cap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&ctl->flags, (uint32_t)CSZI_F_CAPACITY);
+    return;
+  }
+  const u64 tid = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+  const u64 nthr = (u64)gridDim.x * blockDim.x;
+  // bitstream: 16-byte chunks where possible
+  uint8_t *dst = raw + head;
+  for (u64 i = tid; i < nbytes; i += nthr) dst[i] = bits[i];
+  uint8_t *os = raw + head + nbytes;
+  if (tid < 8) os[tid] = (uint8_t)(k >> (8 * tid));
+  for (u64 r = tid; r < k; r += nthr) {
+    uint8_t *q = os + 8 + 12 * r;
+    const u64 ix = oidx[r];
+    const uint32_t vb = __float_as_uint(oval[r]);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) q[b] = (uint8_t)(ix >> (8 * b));
+#pragma unroll
+    for (int b = 0; b < 4; ++b) q[8 + b] = (uint8_t)(vb >> (8 * b));
+  }
+  if (tid == 0) {
+    ctl->raw_len = total;
+    if (is_payload) ctl->payload_len = total;
+  }
+}
+
+// Decompress: parse + validate the outlier section (archive.py:192-206) and
+// mark outlier points with the 0xFFFF sentinel in the symbol array.
+__global__ void k_outliers_parse(const uint8_t *sec, u64 sec_len, u64 n, u64 *oidx, float *oval,
+                                 uint16_t *sym, cszi_ctl *ctl) {
+  if (sec_len < 8) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&ctl->flags, (uint32_t)CSZI_F_OUTLIER_COUNT);
+    return;
+  }
+  u64 k = 0;
+  for (int b = 0; b < 8; ++b) k |= (u64)sec[b] << (8 * b);
+  if (k > (sec_len - 8) / 12 || 8 + 12 * k != sec_len) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&ctl->flags, (uint32_t)CSZI_F_OUTLIER_COUNT);
+    return;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctl->n_outliers = k;
+  for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < k;
+       r += (u64)gridDim.x * blockDim.x) {
+    const uint8_t *q = sec + 8 + 12 * r;
+    u64 ix = 0;
+    uint32_t vb = 0;
+    for (int b = 0; b < 8; ++b) ix |= (u64)q[b] << (8 * b);
+    for (int b = 0; b < 4; ++b) vb |= (uint32_t)q[8 + b] << (8 * b);
+    oidx[r] = ix;
+    oval[r] = __uint_as_float(vb);
+    if (r > 0) {
+      const uint8_t *pq = q - 12;
+      u64 pi = 0;
+      for (int b = 0; b < 8; ++b) pi |= (u64)pq[b] << (8 * b);
+      if (!(ix > pi)) atomicOr(&ctl->flags, (uint32_t)CSZI_F_OUTLIER_ORDER);
+    }
+    if (ix >= n) atomicOr(&ctl->flags, (uint32_t)CSZI_F_OUTLIER_INDEX);
+  }
+}
+__global__ void k_outliers_mark(const u64 *oidx, const cszi_ctl *ctl, u64 n, uint16_t *sym) {
+  if (ctl->flags & (CSZI_F_OUTLIER_COUNT | CSZI_F_OUTLIER_ORDER | CSZI_F_OUTLIER_INDEX)) return;
+  const u64 k = ctl->n_outliers;
+  for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < k;
+       r += (u64)gridDim.x * blockDim.x) {
+    const u64 ix = oidx[r];
+    if (ix < n) sym[ix] = 0xFFFFu;
+  }
+}
+
+__global__ void k_check_raw_len(const cszi_ctl *ctl_ro, cszi_ctl *ctl, u64 expect) {
+  if (ctl_ro->raw_len != expect) ctl->flags |= CSZI_F_P2_LENGTH;
+}
+
+// ---------------------------------------------------------------------------
+// workspace layout
+// ---------------------------------------------------------------------------
+static inline u64 al(u64 b) { return (b + 255) & ~(u64)255; }
+
+struct Carver {
+  unsigned char *p;
+  u64 used;
+  unsigned char *take(u64 b) {
+    unsigned char *r = p ? p + used : nullptr;
+    used += al(b);
+    return r;
+  }
+};
+
+static u64 grid_n(const cszi_geom *g) { return (u64)g->ext[0] * g->ext[1] * g->ext[2]; }
+static u64 anchors_count(const cszi_geom *g) {
+  u64 c = 1;
+  for (int a = 0; a < 3; ++a) {
+    const int64_t e = g->ext[a], S = g->stride;
+    c *= (u64)((e - 1) / S + 1 + (((e - 1) % S) ? 1 : 0));
+  }
+  return c;
+}
+static u64 raw_capacity(const cszi_geom *g, int32_t R, const cszi_caps *caps) {
+  return 4 * anchors_count(g) + 2 * (u64)R + caps->bits_cap + 8 + 12 * caps->outlier_cap;
+}
+
+struct CompressWS {
+  uint16_t *sym;
+  u64 *hist;
+  uint32_t *words;
+  uint32_t *bits;
+  u64 *oidx;
+  float *oval;
+  uint8_t *raw;
+  void *enc_scratch;
+  void *p2_scratch;
+};
+
+static u64 layout_compress(const cszi_geom *g, int32_t R, const cszi_caps *caps, void *base,
+                           CompressWS *W) {
+  const u64 n = grid_n(g);
+  Carver c{reinterpret_cast<unsigned char *>(base), 0};
+  CompressWS w;
+  w.sym = reinterpret_cast<uint16_t *>(c.take(2 * n + 32));
+  w.hist = reinterpret_cast<u64 *>(c.take(8 * 2 * (u64)R));
+  w.words = reinterpret_cast<uint32_t *>(c.take(4 * 2 * (u64)R));
+  w.bits = reinterpret_cast<uint32_t *>(c.take(caps->bits_cap + 16));
+  w.oidx = reinterpret_cast<u64 *>(c.take(8 * caps->outlier_cap + 8));
+  w.oval = reinterpret_cast<float *>(c.take(4 * caps->outlier_cap + 4));
+  w.raw = reinterpret_cast<uint8_t *>(c.take(raw_capacity(g, R, caps) + 16));
+  w.enc_scratch = c.take(enc_scratch_bytes(n));
+  w.p2_scratch = c.take(p2enc_scratch_bytes(raw_capacity(g, R, caps)));
+  if (W) *W = w;
+  return c.used;
+}
+
+struct DecompressWS {
+  uint8_t *raw;
+  void *p2_scratch;
+  void *dec_tables;
+  uint16_t *sym;
+  u64 *oidx;
+  float *oval;
+  void *dec_scratch;
+};
+
+static u64 layout_decompress(const cszi_geom *g, int32_t R, const u64 sec[4], u64 payload_len,
+                             int table_mode, void *base, DecompressWS *W) {
+  const u64 n = grid_n(g);
+  const u64 raw = sec[0] + sec[1] + sec[2] + sec[3];
+  const u64 kmax = sec[3] >= 8 ? (sec[3] - 8) / 12 + 1 : 1;
+  Carver c{reinterpret_cast<unsigned char *>(base), 0};
+  DecompressWS w;
+  w.raw = c.take(raw + 64);
+  w.p2_scratch = c.take(p2dec_scratch_bytes(payload_len));
+  w.dec_tables = c.take(dec_tables_bytes(2 * R));
+  w.sym = reinterpret_cast<uint16_t *>(c.take(2 * n + 32));
+  w.oidx = reinterpret_cast<u64 *>(c.take(8 * kmax));
+  w.oval = reinterpret_cast<float *>(c.take(4 * kmax));
+  w.dec_scratch = c.take(dec_scratch_bytes(sec[2], table_mode));
+  if (W) *W = w;
+  return c.used;
+}
+
+static int grid_for(u64 work) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  u64 b = (work + 255) / 256;
+  if (b > (u64)sms * 8) b = (u64)sms * 8;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+#define CK(x)                   \
+  do {                          \
+    const int rc_ = (x);        \
+    if (rc_ != CSZI_OK) return rc_; \
+  } while (0)
+
+static int check_geom(const cszi_geom *g, int32_t R) {
+  if (!g || g->rank < 1 || g->rank > 3) return CSZI_E_INVALID_ARG;
+  if (g->stride < 2 || (g->stride & (g->stride - 1))) return CSZI_E_INVALID_ARG;
+  for (int a = 0; a < 3; ++a)
+    if (g->ext[a] < 1 || g->tile[a] < 1) return CSZI_E_INVALID_ARG;
+  if (R < 2) return CSZI_E_INVALID_ARG;
+  if (2 * (int64_t)R > 16384) return CSZI_E_UNSUPPORTED;  // uint16 symbols + codebook kernel
+  return CSZI_OK;
+}
+
+}  // namespace cszi
+
+using namespace cszi;
+
+extern "C" {
+
+const char *cszi_version(void) {
+  return "libcszi 0.1 sm_100a (fp64 RN, no FMA contraction; decoupled look-back)";
+}
+
+uint64_t cszi_compress_workspace_size(const cszi_geom *g, int32_t radius, const cszi_caps *caps) {
+  return layout_compress(g, radius, caps, nullptr, nullptr) + 256;
+}
+
+uint64_t cszi_payload_capacity(const cszi_geom *g, int32_t radius, const cszi_caps *caps) {
+  const u64 raw = raw_capacity(g, radius, caps);
+  return raw + raw / 128 + 64;
+}
+
+int cszi_compress(const float *x, const cszi_geom *g, const cszi_params *p,
+                  const cszi_caps *caps, int32_t pass2, int32_t range_done, uint8_t *payload,
+                  void *workspace, uint64_t ws_bytes, cszi_ctl *ctl, void *stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int32_t R = p->radius;
+  CK(check_geom(g, R));
+  CompressWS W;
+  const u64 need = layout_compress(g, R, caps, workspace, &W);
+  if (ws_bytes < need) return CSZI_E_CAPACITY;
+  const u64 n = grid_n(g);
+  const u64 nbins = 2 * (u64)R;
+  const u64 na = anchors_count(g);
+  const u64 raw_cap = raw_capacity(g, R, caps);
+  if (!range_done) {
+    CK(launch_ctl_init(ctl, st));
+    CK(launch_range(x, n, ctl, st));
+  } else {
+    k_ctl_reset_outputs<<<1, 1, 0, st>>>(ctl);
+  }
+  CK(launch_tune(x, g, p, ctl, st));
+  cudaMemsetAsync(W.hist, 0, 8 * nbins, st);
+  CK(launch_predict(x, g, R, ctl, W.sym, W.hist, p->exact != 0, st));
+  uint8_t *raw = pass2 ? W.raw : payload;
+  CK(launch_gather_anchors(x, g, reinterpret_cast<float *>(raw), st));
+  uint8_t *lengths = raw + 4 * na;  // the codebook section is the length table
+  CK(launch_codebook(W.hist, (int)nbins, lengths, W.words, ctl, st));
+  CK(launch_encode(0, W.sym, n, R, lengths, W.words, W.bits, caps->bits_cap, x, W.oidx, W.oval,
+                   caps->outlier_cap, W.enc_scratch, ctl, st));
+  const u64 head = 4 * na + nbins;
+  k_assemble<<<grid_for(n / 16), 256, 0, st>>>(raw, head, reinterpret_cast<uint8_t *>(W.bits),
+                                                W.oidx, W.oval, raw_cap, caps->bits_cap,
+                                                caps->outlier_cap, ctl, pass2 ? 0 : 1);
+  if (pass2) CK(launch_pass2_encode(raw, reinterpret_cast<const u64 *>(&ctl->raw_len), raw_cap, payload, W.p2_scratch, ctl, st));
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
+uint64_t cszi_decompress_workspace_size(const cszi_geom *g, int32_t radius,
+                                        const uint64_t sec_len[4], uint64_t payload_len) {
+  return layout_decompress(g, radius, reinterpret_cast<const u64 *>(sec_len), payload_len, 1,
+                           nullptr, nullptr) + 256;
+}
+
+int cszi_decompress(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
+                    const uint64_t sec_len[4], const cszi_geom *g, int32_t radius,
+                    const double *level_eb, int32_t nlev, const int32_t variant[3],
+                    const int32_t order[3], int32_t table_mode, float *y, void *workspace,
+                    uint64_t ws_bytes, cszi_ctl *ctl, void *stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CK(check_geom(g, radius));
+  DecompressWS W;
+  const u64 need = layout_decompress(g, radius, reinterpret_cast<const u64 *>(sec_len),
+                                     payload_len, 1, workspace, &W);
+  if (ws_bytes < need) return CSZI_E_CAPACITY;
+  const u64 n = grid_n(g);
+  const u64 nbins = 2 * (u64)radius;
+  const u64 raw_len = sec_len[0] + sec_len[1] + sec_len[2] + sec_len[3];
+  CK(launch_ctl_init(ctl, st));
+  const uint8_t *raw = payload;
+  if (pass2) {
+    CK(launch_pass2_decode(payload, payload_len, W.raw, raw_len, W.p2_scratch, ctl, st, 1));
+    k_check_raw_len<<<1, 1, 0, st>>>(ctl, ctl, raw_len);
+    raw = W.raw;
+  }
+  if (sec_len[1] != nbins) return CSZI_E_MALFORMED;
+  const uint8_t *anchors = raw;
+  const uint8_t *lengths = raw + sec_len[0];
+  const uint8_t *bits = lengths + sec_len[1];
+  const uint8_t *outl = bits + sec_len[2];
+  CK(launch_canonical(lengths, (int)nbins, nullptr, W.dec_tables, ctl, st));
+  CK(launch_decode(bits, sec_len[2], n, radius, W.dec_tables, W.sym, 0, W.dec_scratch, ctl, st,
+                   table_mode, 32));
+  const u64 kmax = sec_len[3] >= 8 ? (sec_len[3] - 8) / 12 : 0;
+  k_outliers_parse<<<grid_for(kmax), 256, 0, st>>>(outl, sec_len[3], n, W.oidx, W.oval, W.sym,
+                                                   ctl);
+  k_outliers_mark<<<grid_for(kmax), 256, 0, st>>>(W.oidx, ctl, n, W.sym);
+  // the anchor section is 4-byte aligned inside the decoded payload
+  const float *anc = reinterpret_cast<const float *>(anchors);
+  // the outlier count is device-resident (ctl->n_outliers, set by the parse)
+  CK(launch_reconstruct(W.sym, anc, W.oidx, W.oval, kmax,
+                        reinterpret_cast<const u64 *>(&ctl->n_outliers), g, radius, level_eb,
+                        nlev, variant, order, y, st));
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
+int cszi_ctl_init(cszi_ctl *ctl, void *stream) {
+  return launch_ctl_init(ctl, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int cszi_range(const float *x, uint64_t n, cszi_ctl *ctl, void *stream) {
+  return launch_range(x, n, ctl, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int cszi_tune(const float *x, const cszi_geom *g, const cszi_params *p, cszi_ctl *ctl,
+              void *stream) {
+  CK(check_geom(g, p->radius));
+  return launch_tune(x, g, p, ctl, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int cszi_predict(const float *x, const cszi_geom *g, int32_t radius, int32_t exact,
+                 uint16_t *sym, uint64_t *hist, cszi_ctl *ctl, void *stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CK(check_geom(g, radius));
+  cudaMemsetAsync(hist, 0, 8 * 2 * (size_t)radius, st);
+  return launch_predict(x, g, radius, ctl, sym, reinterpret_cast<u64 *>(hist), exact != 0, st);
+}
+
+int cszi_reconstruct(const uint16_t *sym, const float *anchors, const uint64_t *out_idx,
+                     const float *out_val, uint64_t n_out, const cszi_geom *g, int32_t radius,
+                     const double *level_eb, int32_t nlev, const int32_t variant[3],
+                     const int32_t order[3], float *y, void *stream) {
+  CK(check_geom(g, radius));
+  return launch_reconstruct(sym, anchors, reinterpret_cast<const u64 *>(out_idx), out_val, n_out,
+                            nullptr, g, radius, level_eb, nlev, variant, order, y,
+                            reinterpret_cast<cudaStream_t>(stream));
+}
+
+int cszi_gather_anchors(const float *x, const cszi_geom *g, float *out, void *stream) {
+  return launch_gather_anchors(x, g, out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int cszi_histogram_i32(const int32_t *codes, uint64_t n, int32_t radius, uint64_t *counts,
+                       cszi_ctl *ctl, void *stream) {
+  if (radius < 1) return CSZI_E_INVALID_ARG;
+  return launch_hist_i32(codes, n, radius, reinterpret_cast<u64 *>(counts), ctl,
+                         reinterpret_cast<cudaStream_t>(stream));
+}
+
+int cszi_codebook(const uint64_t *counts, uint32_t nbins, uint8_t *lengths, uint32_t *words,
+                  cszi_ctl *ctl, void *stream) {
+  return launch_codebook(reinterpret_cast<const u64 *>(counts), (int)nbins, lengths, words, ctl,
+                         reinterpret_cast<cudaStream_t>(stream));
+}
+
+uint64_t cszi_dec_tables_size(uint32_t nbins) { return dec_tables_bytes((int)nbins); }
+
+int cszi_canonical(const uint8_t *lengths, uint32_t nbins, uint32_t *words, void *dec_tables,
+                   cszi_ctl *ctl, void *stream) {
+  return launch_canonical(lengths, (int)nbins, words, dec_tables, ctl,
+                          reinterpret_cast<cudaStream_t>(stream));
+}
+
+uint64_t cszi_huff_encode_workspace_size(uint64_t n) { return enc_scratch_bytes(n) + 256; }
+
+int cszi_huff_encode_i32(const int32_t *codes, uint64_t n, int32_t radius,
+                         const uint8_t *lengths, const uint32_t *words, uint8_t *out,
+                         uint64_t cap, void *workspace, cszi_ctl *ctl, void *stream) {
+  if (reinterpret_cast<uintptr_t>(out) & 3) return CSZI_E_INVALID_ARG;
+  return launch_encode(1, codes, n, radius, lengths, words, reinterpret_cast<uint32_t *>(out),
+                       cap, nullptr, nullptr, nullptr, 0, workspace, ctl,
+                       reinterpret_cast<cudaStream_t>(stream));
+}
+
+uint64_t cszi_huff_decode_workspace_size(uint64_t nbytes, int32_t table_mode) {
+  return dec_scratch_bytes(nbytes, table_mode) + 256;
+}
+
+int cszi_huff_decode_i32(const uint8_t *stream_bytes, uint64_t nbytes, uint64_t n,
+                         int32_t radius, const void *dec_tables, int32_t *codes,
+                         int32_t table_mode, int32_t lmax, void *workspace, cszi_ctl *ctl,
+                         void *stream) {
+  return launch_decode(stream_bytes, nbytes, n, radius, dec_tables, codes, 1, workspace, ctl,
+                       reinterpret_cast<cudaStream_t>(stream), table_mode, lmax);
+}
+
+uint64_t cszi_pass2_encode_workspace_size(uint64_t n) { return p2enc_scratch_bytes(n) + 256; }
+
+int cszi_pass2_encode(const uint8_t *in, const uint64_t *n_dev, uint64_t n, uint8_t *out,
+                      void *workspace, cszi_ctl *ctl, void *stream) {
+  return launch_pass2_encode(in, reinterpret_cast<const u64 *>(n_dev), n, out, workspace, ctl,
+                             reinterpret_cast<cudaStream_t>(stream));
+}
+
+uint64_t cszi_pass2_decode_workspace_size(uint64_t n) { return p2dec_scratch_bytes(n) + 256; }
+
+int cszi_pass2_decode(const uint8_t *in, uint64_t n, uint8_t *out, uint64_t cap,
+                      int32_t expand, void *workspace, cszi_ctl *ctl, void *stream) {
+  return launch_pass2_decode(in, n, out, cap, workspace, ctl,
+                             reinterpret_cast<cudaStream_t>(stream), expand);
+}
+
+}  // extern "C"
+
+extern "C" {
+// ABI self-check for bindings: sizes of the shared structs.
+void cszi_abi_sizes(uint64_t out[4]) {
+  out[0] = sizeof(cszi_geom);
+  out[1] = sizeof(cszi_params);
+  out[2] = sizeof(cszi_caps);
+  out[3] = sizeof(cszi_ctl);
+}
+}

@@ -1,0 +1,153 @@
+// Shared device utilities for libcszi (sm_100a): warp/block scans, the
+// decoupled look-back used by every stream-compaction stage (bit offsets,
+// outlier positions, pass-2 segments), exact-rounding fp64 helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "cszi.h"
+
+#define DEV __device__ __forceinline__
+#define CSZI_FULL 0xffffffffu
+
+namespace cszi {
+
+typedef unsigned long long u64;
+
+// ---------------------------------------------------------------------------
+// memory-model helpers (release/acquire at gpu scope)
+// ---------------------------------------------------------------------------
+DEV void st_release(u64 *p, u64 v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+DEV u64 ld_acquire(const u64 *p) {
+  u64 v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+DEV uint32_t ld_volatile_u32(const uint32_t *p) { return *(const volatile uint32_t *)p; }
+
+DEV uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+
+// Order-preserving key of a float (for atomicMin/atomicMax on raw bits).
+__host__ __device__ __forceinline__ uint32_t float_key(float f) {
+#ifdef __CUDA_ARCH__
+  uint32_t b = __float_as_uint(f);
+#else
+  uint32_t b;
+  __builtin_memcpy(&b, &f, 4);
+#endif
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__host__ __device__ __forceinline__ float key_float(uint32_t k) {
+  uint32_t b = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+#ifdef __CUDA_ARCH__
+  return __uint_as_float(b);
+#else
+  float f;
+  __builtin_memcpy(&f, &b, 4);
+  return f;
+#endif
+}
+
+// ---------------------------------------------------------------------------
+// scans
+// ---------------------------------------------------------------------------
+template <typename T>
+DEV T warp_incl_scan(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T t = __shfl_up_sync(CSZI_FULL, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+template <typename T>
+DEV T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(CSZI_FULL, v, o);
+  return v;
+}
+
+// Block-wide exclusive scan; `ws` holds NT/32 elements; returns the
+// exclusive prefix of the calling thread and the block total in `total`.
+template <int NT, typename T>
+DEV T block_excl_scan(T v, T *ws, T &total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T inc = warp_incl_scan(v);
+  if (lane == 31) ws[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    T w = (lane < NT / 32) ? ws[lane] : T(0);
+    T wi = warp_incl_scan(w);
+    if (lane < NT / 32) ws[lane] = wi - w;
+    if (lane == NT / 32 - 1) ws[NT / 32] = wi;
+  }
+  __syncthreads();
+  T excl = ws[warp] + inc - v;
+  total = ws[NT / 32];
+  __syncthreads();
+  return excl;
+}
+
+// ---------------------------------------------------------------------------
+// decoupled look-back (single-pass chained scan across tiles)
+// status word: [63:62] flag (0 invalid, 1 aggregate, 2 inclusive), [61:0] value
+// Must be called by all 32 lanes of ONE warp; tiles must be processed in
+// ticket order (tile t only waits on tiles < t, which started earlier).
+// ---------------------------------------------------------------------------
+constexpr u64 LB_AGG = 1ull << 62;
+constexpr u64 LB_INC = 2ull << 62;
+constexpr u64 LB_VAL = (1ull << 62) - 1;
+
+DEV u64 lookback_exclusive(u64 *status, u64 tile, u64 aggregate) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) st_release(&status[0], LB_INC | aggregate);
+    return 0;
+  }
+  if (lane == 0) st_release(&status[tile], LB_AGG | aggregate);
+  u64 excl = 0;
+  long long top = (long long)tile - 1;
+  for (;;) {
+    const long long idx = top - lane;
+    u64 s = (idx >= 0) ? ld_acquire(&status[idx]) : LB_INC;
+    const uint32_t inc_mask = __ballot_sync(CSZI_FULL, (s >> 62) == 2);
+    const int first_inc = inc_mask ? (__ffs(inc_mask) - 1) : 32;
+    const uint32_t inv_mask = __ballot_sync(CSZI_FULL, (s >> 62) == 0 && lane < first_inc);
+    if (inv_mask) continue;  // a predecessor has not published yet: re-poll
+    u64 v = (lane <= first_inc) ? (s & LB_VAL) : 0;
+    v = warp_sum(v);
+    excl += v;
+    if (inc_mask) break;
+    top -= 32;
+  }
+  if (lane == 0) st_release(&status[tile], LB_INC | (excl + aggregate));
+  return excl;
+}
+
+// ---------------------------------------------------------------------------
+// exact fp64 helpers (numpy float64 semantics, never contracted)
+// ---------------------------------------------------------------------------
+DEV double dadd(double a, double b) { return __dadd_rn(a, b); }
+DEV double dsub(double a, double b) { return __dsub_rn(a, b); }
+DEV double dmul(double a, double b) { return __dmul_rn(a, b); }
+DEV double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// float -> double, exact.  Normal floats via integer ops (the conversion
+// pipe runs at 16/clk/SM on B200 vs 128/clk for integer ops); zero and
+// subnormal inputs take the hardware conversion.
+DEV double f2d(float f) {
+  const uint32_t b = __float_as_uint(f);
+  const uint32_t mag = b & 0x7fffffffu;
+  if (mag - 0x00800000u < 0x7f000000u) {  // normal, finite
+    const uint32_t hi = (b & 0x80000000u) | ((mag >> 3) + 0x38000000u);
+    const uint32_t lo = b << 29;
+    return __hiloint2double((int)hi, (int)lo);
+  }
+  return (double)f;
+}
+
+}  // namespace cszi
