@@ -1,0 +1,464 @@
+#!/usr/bin/env python
+"""bench.py — cuSZ-i (arXiv 2312.05492) compression hot path on B200.
+
+Metric (BASELINE.json): compress/decompress GB/s at REL eb 1e-3, CR & PSNR.
+Workload at N=1: the Nyx-shaped 512x512x512 float32 smooth field
+ at REL eb 1e-3 with the reference defaults (interp
+predictor, pass-2 on, R = 512).  One step = Grid construction on a
+device-resident field (range + finite scan) + compress to a complete
+archive in HBM; `value` is input GB/s of that step.  Decompress GB/s, CR,
+PSNR and the bound check ride along in the same JSON line.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs one process per GPU (torchrun); every rank compresses its own
+512^3 field (weak scaling) and the step time is the max over ranks.
+--impl reference times the reference algorithm's CPU implementation (the
+oracle port in oracle/, C + OpenMP on all host cores) on the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "compress/decompress GB/s at REL eb 1e-3 (1/2/4/8 B200, HBM %), CR & PSNR"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--shape", default="512,512,512")
+    ap.add_argument("--eb", type=float, default=1e-3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+def dist_init(n):
+    import torch
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# workload
+# ---------------------------------------------------------------------------
+def smooth_field_gpu(shape, phase=0.0):
+    """SURVEY.md §8d smooth field, float64 math on the device, cast to float32."""
+    import torch
+
+    nz, ny, nx = shape
+    z = torch.arange(nz, dtype=torch.float64, device="cuda").view(nz, 1, 1)
+    y = torch.arange(ny, dtype=torch.float64, device="cuda").view(1, ny, 1)
+    x = torch.arange(nx, dtype=torch.float64, device="cuda").view(1, 1, nx)
+    two_pi = 2 * math.pi
+    f = torch.sin(two_pi * z * 2.0 / nz + phase) + 0.7 * torch.cos(two_pi * y * 3.0 / ny + phase)
+    f = f + 0.5 * torch.sin(two_pi * x * 1.5 / nx + phase)
+    f = f + 0.3 * torch.sin(two_pi * (z / nz + y / ny + x / nx) + phase)
+    return f.to(torch.float32).contiguous()
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_compress_gbs(data_np, eb, min_seconds=10.0, max_reps=3):
+    """Oracle port (C + OpenMP, all host cores) compress throughput."""
+    from oracle import oracle as O
+
+    O.lib()
+    reps, elapsed = 0, 0.0
+    blob = None
+    while reps < max_reps and (reps == 0 or elapsed < min_seconds):
+        t0 = time.perf_counter()
+        blob = O.compress(data_np, eb, threads=cpu_cores())
+        elapsed += time.perf_counter() - t0
+        reps += 1
+    return data_np.nbytes * reps / elapsed / 1e9, blob, reps
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world, local):
+    import numpy as np
+    import torch
+
+    import paper_2312_05492_b200 as P
+    from paper_2312_05492_b200 import _lib
+    from paper_2312_05492_b200.predictor import default_layout, make_geom
+
+    shape = tuple(int(s) for s in args.shape.split(","))
+    n = math.prod(shape)
+    nbytes = 4 * n
+    eb = args.eb
+    lib = _lib.load()
+    dims = P.Dims(shape)
+    x = smooth_field_gpu(shape, phase=0.0)
+    torch.cuda.synchronize()
+
+    def step_compress():
+        g = P.Grid(dims, x)
+        return P.compress_device(g, eb)
+
+    # warm-up (also the correctness probe of this run)
+    for _ in range(max(args.warmup, 1)):
+        arch = step_compress()
+        yg = P.decompress_device(arch)
+    torch.cuda.synchronize()
+    blob_len = len(arch)
+    eb_abs = P.archive.unpack_header(arch.header, blob_len).eb_abs
+    y = yg.tensor
+    diff = (x.double() - y.double()).abs()
+    max_err = float(diff.max().item())
+    mse = float((diff * diff).mean().item())
+    rng = float(x.max().item()) - float(x.min().item())
+    psnr = 10.0 * math.log10(rng * rng / mse) if mse > 0 else float("inf")
+    bound_ok = max_err <= eb_abs
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = Clocks(torch.cuda.current_device())
+    # ---- compress (device-resident) ----
+    launches0 = lib.cszi_launch_count()
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0.record()
+    for _ in range(args.steps):
+        arch = step_compress()
+    ev1.record()
+    torch.cuda.synchronize()
+    barrier(world)
+    launches = lib.cszi_launch_count() - launches0
+    c_ms = ev0.elapsed_time(ev1) / args.steps
+    # ---- decompress (device-resident) ----
+    barrier(world)
+    torch.cuda.synchronize()
+    ev0.record()
+    for _ in range(args.steps):
+        yg = P.decompress_device(arch)
+    ev1.record()
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop()
+    d_ms = ev0.elapsed_time(ev1) / args.steps
+    c_ms = max_over_ranks(c_ms, world)
+    d_ms = max_over_ranks(d_ms, world)
+
+    # ---- dominant kernel: fused predict/quantize/histogram, timed alone ----
+    geom = make_geom(shape, default_layout(len(shape)))
+    R = 512
+    g = P.Grid(dims, x)
+    P.compress_device(g, eb)  # leaves the tuned config in g's ctl
+    sym = torch.empty(n + 16, dtype=torch.int16, device="cuda")
+    hist = torch.empty(2 * R, dtype=torch.int64, device="cuda")
+    st = _lib.stream_ptr()
+    import ctypes
+
+    for _ in range(3):
+        lib.cszi_predict(_lib.ptr(x), ctypes.byref(geom), R, 0, _lib.ptr(sym), _lib.ptr(hist),
+                         g._ctl.ptr, st)
+    torch.cuda.synchronize()
+    ev0.record()
+    kreps = max(args.steps, 5)
+    for _ in range(kreps):
+        lib.cszi_predict(_lib.ptr(x), ctypes.byref(geom), R, 0, _lib.ptr(sym), _lib.ptr(hist),
+                         g._ctl.ptr, st)
+    ev1.record()
+    torch.cuda.synchronize()
+    k_ms = ev0.elapsed_time(ev1) / kreps
+    peak, peak_kind = peaks()
+    k_bytes = 4 * n + 2 * n  # read f32 field, write uint16 codes
+    achieved = k_bytes / (k_ms * 1e-3) / 1e9
+    traffic = None
+    tfile = os.path.join(HERE, "profiles", "predict_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            with open(tfile) as f:
+                tj = json.load(f)
+            if tuple(tj.get("shape", [])) == shape:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    result = {
+        "metric": METRIC,
+        "value": round(world * nbytes / (c_ms * 1e-3) / 1e9, 3),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(c_ms, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {
+            "workload": f"Nyx-shaped {shape[0]}x{shape[1]}x{shape[2]} float32 smooth field "
+                        f"(SURVEY §8d), REL eb {eb:g}, defaults (interp, pass2, R=512); step = "
+                        "Grid(device tensor) [range+finite scan] + compress to a full archive "
+                        "in HBM",
+            "shape": list(shape),
+            "eb": eb,
+            "mode": "rel",
+            "per_gpu_input_bytes": nbytes,
+            "l2": "input 537 MB > 126 MB L2 per step; no flush needed",
+            "parallelism": f"replicas x{world} (one field per GPU)",
+        },
+        "decompress_gbs": round(world * nbytes / (d_ms * 1e-3) / 1e9, 3),
+        "decompress_ms_per_step": round(d_ms, 4),
+        "cr": round(nbytes / blob_len, 4),
+        "psnr": round(psnr, 4),
+        "max_abs_err": max_err,
+        "eb_abs": eb_abs,
+        "bound_ok": bool(bound_ok),
+        "archive_bytes": blob_len,
+        "roofline": {
+            "bound": "hbm",
+            "kernel": "k_predict (fused G-Interp predict+quantize+histogram)",
+            "achieved": round(achieved, 2),
+            "peak": peak,
+            "peak_kind": peak_kind,
+            "unit": "GB/s",
+            "frac": round(achieved / peak, 4),
+            "traffic": traffic,
+            "kernel_ms": round(k_ms, 4),
+            "algorithmic_bytes_per_launch": k_bytes,
+            "share_of_step": round(k_ms / c_ms, 4),
+        },
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+
+    # ---- e2e through the public API with host buffers ----
+    if not args.no_e2e:
+        pinned = torch.empty(shape, dtype=torch.float32, pin_memory=True)
+        pinned.copy_(x)
+        hg = P.Grid(dims, pinned.numpy())
+        blob = P.compress(hg, eb)
+        back = P.decompress(blob)
+        torch.cuda.synchronize()
+        barrier(world)
+        t0 = time.perf_counter()
+        ev0.record()
+        for _ in range(args.steps):
+            blob = P.compress(hg, eb)
+        ev1.record()
+        torch.cuda.synchronize()
+        e_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world)
+        barrier(world)
+        ev0.record()
+        for _ in range(args.steps):
+            back = P.decompress(blob)
+        ev1.record()
+        torch.cuda.synchronize()
+        ed_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world)
+        result["e2e"] = {"value": round(world * nbytes / (e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+                         "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": len(blob),
+                         "ms_per_step": round(e_ms, 3),
+                         "api": "paper_2312_05492_b200.compress(Grid(pinned host numpy), eb)"}
+        result["e2e_decompress"] = {"value": round(world * nbytes / (ed_ms * 1e-3) / 1e9, 3),
+                                    "unit": "GB/s", "h2d_bytes_per_step": len(blob),
+                                    "d2h_bytes_per_step": nbytes, "ms_per_step": round(ed_ms, 3)}
+        result["archive_sha256"] = hashlib.sha256(blob).hexdigest()[:16]
+
+    # ---- CPU baseline: oracle port on the host cores (rank 0, N=1 only) ----
+    if rank == 0 and world == 1 and not args.no_cpu:
+        data_np = x.cpu().numpy()
+        gbs, oblob, reps = oracle_compress_gbs(data_np, eb)
+        result["cpu_baseline"] = {
+            "value": round(gbs, 4), "unit": "GB/s", "cores": cpu_cores(), "kind": "port",
+            "sample": f"full {shape[0]}x{shape[1]}x{shape[2]} field, {reps} compress run(s) of "
+                      "oracle/ (C+OpenMP restatement of ebcomp)",
+        }
+        if not args.no_e2e:
+            result["parity_vs_oracle"] = bool(oblob == blob)
+    return result
+
+
+# ---------------------------------------------------------------------------
+# reference arm (the reference algorithm's CPU implementation: oracle port)
+# ---------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    import numpy as np
+
+    from oracle import oracle as O
+
+    shape = tuple(int(s) for s in args.shape.split(","))
+    n = math.prod(shape)
+    nbytes = 4 * n
+    if rank != 0:
+        return None
+    data = O.smooth_field(shape)
+    O.lib()
+    cores = cpu_cores()
+    blob = None
+    for _ in range(args.warmup):
+        blob = O.compress(data, args.eb, threads=cores)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        blob = O.compress(data, args.eb, threads=cores)
+        times.append(time.perf_counter() - t0)
+    c_s = sum(times) / len(times)
+    t0 = time.perf_counter()
+    back = O.decompress(blob, threads=cores)
+    d_s = time.perf_counter() - t0
+    value = nbytes / c_s / 1e9
+    return {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": round(value, 4),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(c_s * 1e3, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {
+            "workload": f"Nyx-shaped {shape[0]}x{shape[1]}x{shape[2]} float32 smooth field "
+                        f"(SURVEY §8d), REL eb {args.eb:g}, defaults; CPU reference algorithm",
+            "shape": list(shape), "eb": args.eb, "mode": "rel",
+        },
+        "decompress_gbs": round(nbytes / d_s / 1e9, 4),
+        "cr": round(nbytes / len(blob), 4),
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": f"full field, {args.steps} timed compress runs of oracle/ "
+                                   "(C+OpenMP restatement of ebcomp; the Python reference "
+                                   "cannot travel to the GPU box)"},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        res = run_reference(args, rank, world)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+    rank, world, local = dist_init(args.gpus)
+    res = run_ours(args, rank, world, local)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

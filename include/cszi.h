@@ -253,6 +253,9 @@ const char *cszi_version(void);
  * — lets a binding verify its struct mirrors at load time. */
 void cszi_abi_sizes(uint64_t out[4]);
 
+/* Number of kernels this library has launched in this process. */
+uint64_t cszi_launch_count(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -124,6 +124,7 @@ _u32 = ctypes.c_uint32
 _SIGS = {
     "cszi_version": (ctypes.c_char_p, []),
     "cszi_abi_sizes": (None, [_vp]),
+    "cszi_launch_count": (_u64, []),
     "cszi_compress_workspace_size": (_u64, [_vp, _i32, _vp]),
     "cszi_payload_capacity": (_u64, [_vp, _i32, _vp]),
     "cszi_compress": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _u64, _vp, _vp]),

@@ -1,6 +1,7 @@
 // extern "C" entry points of libcszi.so (see include/cszi.h) and the
 // stream-ordered orchestration of the compress / decompress paths
 // (pipeline.py:66-204).  No exceptions cross the ABI; no host sync inside.
+#include <atomic>
 #include <cstring>
 
 #include "common.cuh"
@@ -250,6 +251,9 @@ static int check_geom(const cszi_geom *g, int32_t R) {
   return CSZI_OK;
 }
 
+static std::atomic<unsigned long long> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+
 }  // namespace cszi
 
 using namespace cszi;
@@ -287,6 +291,7 @@ int cszi_compress(const float *x, const cszi_geom *g, const cszi_params *p,
     CK(launch_range(x, n, ctl, st));
   } else {
     k_ctl_reset_outputs<<<1, 1, 0, st>>>(ctl);
+    note_launch();
   }
   CK(launch_tune(x, g, p, ctl, st));
   cudaMemsetAsync(W.hist, 0, 8 * nbins, st);
@@ -301,6 +306,7 @@ int cszi_compress(const float *x, const cszi_geom *g, const cszi_params *p,
   k_assemble<<<grid_for(n / 16), 256, 0, st>>>(raw, head, reinterpret_cast<uint8_t *>(W.bits),
                                                 W.oidx, W.oval, raw_cap, caps->bits_cap,
                                                 caps->outlier_cap, ctl, pass2 ? 0 : 1);
+  note_launch();
   if (pass2) CK(launch_pass2_encode(raw, reinterpret_cast<const u64 *>(&ctl->raw_len), raw_cap, payload, W.p2_scratch, ctl, st));
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
@@ -330,6 +336,7 @@ int cszi_decompress(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
   if (pass2) {
     CK(launch_pass2_decode(payload, payload_len, W.raw, raw_len, W.p2_scratch, ctl, st, 1));
     k_check_raw_len<<<1, 1, 0, st>>>(ctl, ctl, raw_len);
+    note_launch();
     raw = W.raw;
   }
   if (sec_len[1] != nbins) return CSZI_E_MALFORMED;
@@ -343,7 +350,9 @@ int cszi_decompress(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
   const u64 kmax = sec_len[3] >= 8 ? (sec_len[3] - 8) / 12 : 0;
   k_outliers_parse<<<grid_for(kmax), 256, 0, st>>>(outl, sec_len[3], n, W.oidx, W.oval, W.sym,
                                                    ctl);
+  note_launch();
   k_outliers_mark<<<grid_for(kmax), 256, 0, st>>>(W.oidx, ctl, n, W.sym);
+  note_launch();
   // the anchor section is 4-byte aligned inside the decoded payload
   const float *anc = reinterpret_cast<const float *>(anchors);
   // the outlier count is device-resident (ctl->n_outliers, set by the parse)
@@ -453,6 +462,8 @@ int cszi_pass2_decode(const uint8_t *in, uint64_t n, uint8_t *out, uint64_t cap,
 
 extern "C" {
 // ABI self-check for bindings: sizes of the shared structs.
+uint64_t cszi_launch_count(void) { return g_launches.load(); }
+
 void cszi_abi_sizes(uint64_t out[4]) {
   out[0] = sizeof(cszi_geom);
   out[1] = sizeof(cszi_params);

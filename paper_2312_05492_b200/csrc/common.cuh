@@ -15,6 +15,9 @@ namespace cszi {
 
 typedef unsigned long long u64;
 
+// Host-side count of kernels this library launched (cszi_launch_count()).
+void note_launch(int n = 1);
+
 // ---------------------------------------------------------------------------
 // memory-model helpers (release/acquire at gpu scope)
 // ---------------------------------------------------------------------------

@@ -725,6 +725,7 @@ int launch_hist_i32(const int32_t *codes, u64 n, int R, u64 *hist, cszi_ctl *ctl
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks < 1) blocks = 1;
   k_hist_i32<<<(unsigned)blocks, 256, smem, st>>>(codes, n, R, hist, ctl);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
@@ -737,6 +738,7 @@ int launch_codebook(const u64 *hist, int nbins, uint8_t *lengths, uint32_t *word
   const size_t smem = sizeof(u64) * (npow2 + nbins) + sizeof(int32_t) * 3 * nbins + nbins + 16;
   cudaFuncSetAttribute(k_codebook, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_codebook<<<1, CB_NT, smem, st>>>(hist, nbins, lengths, words, ctl);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
@@ -749,6 +751,7 @@ int launch_canonical(const uint8_t *lengths, int nbins, uint32_t *words, void *d
   cudaFuncSetAttribute(k_canonical, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_canonical<<<1, CB_NT, smem, st>>>(lengths, nbins, words,
                                       reinterpret_cast<DecTables *>(dec_tables), ctl);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
@@ -786,11 +789,13 @@ int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *length
     k_encode<0><<<(unsigned)grid, ENC_NT, smem, st>>>(src, n, R, lengths, words, out,
                                                      cap_bytes / 4, xval, o_idx, o_val, o_cap,
                                                      S, ntiles, ctl);
+    note_launch();
   } else {
     cudaFuncSetAttribute(k_encode<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_encode<1><<<(unsigned)grid, ENC_NT, smem, st>>>(src, n, R, lengths, words, out,
                                                      cap_bytes / 4, xval, o_idx, o_val, o_cap,
                                                      S, ntiles, ctl);
+    note_launch();
   }
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
@@ -854,15 +859,19 @@ int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *de
   const unsigned blocks = (unsigned)((M + 255) / 256);
   if (!table_mode) {
     k_dec_spec<<<blocks, 256, 0, st>>>(s, G, sorted, M, spec_exit, spec_cnt, spec_dead);
+    note_launch();
     // iteration 0 verifies every chunk; two more iterations repair chunks
     // whose predecessor did not synchronise.  A chain still moving after
     // that is reported in ctl->scratch[1]; the caller reruns in table mode.
     k_dec_sync<<<blocks, 256, 0, st>>>(s, G, sorted, M, 0, spec_exit, spec_cnt, spec_dead,
                                        nullptr, nullptr, X0, K, D, chg0, nchg + 0);
+    note_launch();
     k_dec_sync<<<blocks, 256, 0, st>>>(s, G, sorted, M, 1, spec_exit, spec_cnt, spec_dead, X0,
                                        chg0, X1, K, D, chg1, nchg + 1);
+    note_launch();
     k_dec_sync<<<blocks, 256, 0, st>>>(s, G, sorted, M, 2, spec_exit, spec_cnt, spec_dead, X1,
                                        chg1, X0, K, D, chg0, nchg + 2);
+    note_launch();
     cudaMemcpyAsync(&ctl->scratch[1], nchg + 2, 4, cudaMemcpyDeviceToDevice, st);
   } else {
     if (lmax < 1 || lmax > 32) lmax = 32;
@@ -874,18 +883,23 @@ int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *de
     const u64 work = M * (u64)lmax;
     k_dec_table<<<(unsigned)((work + 255) / 256), 256, 0, st>>>(s, G, sorted, M, lmax, tab,
                                                                ktab, dtab);
+    note_launch();
     launch_chain_resolve(tab, M, lmax, 0, E, chain_ws, st);
     k_dec_from_tab<<<blocks, 256, 0, st>>>(M, lmax, E, ktab, dtab, X0, K, D);
+    note_launch();
   }
   launch_excl_scan_u32(K, M, off, total, scan_ws, st);
   k_dec_first_dead<<<blocks, 256, 0, st>>>(M, D, first_dead);
+  note_launch();
   k_dec_check<<<1, 1, 0, st>>>(off, K, first_dead, total, n, ctl);
+  note_launch();
   if (out_kind == 0)
     k_dec_write<uint16_t><<<blocks, 256, 0, st>>>(s, G, sorted, M, X0, off, n, R,
                                                   reinterpret_cast<uint16_t *>(out));
   else
     k_dec_write<int32_t><<<blocks, 256, 0, st>>>(s, G, sorted, M, X0, off, n, R,
                                                  reinterpret_cast<int32_t *>(out));
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 

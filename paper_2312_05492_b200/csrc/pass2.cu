@@ -222,8 +222,11 @@ int launch_pass2_encode(const uint8_t *in, const u64 *Np, u64 cap_n, uint8_t *ou
   if (grid > tiles_max) grid = tiles_max;
   if (grid < 1) grid = 1;
   k_p2_segments<<<(unsigned)grid, P2_NT, 0, st>>>(in, Np, S);
+  note_launch();
   k_p2_sizes<<<(unsigned)grid, P2_NT, 0, st>>>(Np, S, ctl);
+  note_launch();
   k_p2_emit<<<(unsigned)grid, P2_NT, 0, st>>>(in, Np, S, out);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
@@ -368,10 +371,12 @@ int launch_pass2_decode(const uint8_t *in, u64 n, uint8_t *out, u64 cap, void *s
   void *chain_ws = carve2(p, chain_scratch_bytes(M, P2D_D));
   void *scan_ws = carve2(p, scan_scratch_bytes(M));
   k_p2d_tables<<<(unsigned)M, 256, 0, st>>>(in, n, tab, ctab);
+  note_launch();
   launch_chain_resolve(tab, M, P2D_D, 0, E, chain_ws, st);
   k_p2d_counts<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(M, E, ctab, cnt, ctl);
+  note_launch();
   launch_excl_scan_u32(cnt, M, off, reinterpret_cast<u64 *>(&ctl->raw_len), scan_ws, st);
-  if (expand) k_p2d_expand<<<(unsigned)M, 256, 0, st>>>(in, n, E, off, out, cap, ctl);
+  if (expand) { k_p2d_expand<<<(unsigned)M, 256, 0, st>>>(in, n, E, off, out, cap, ctl); note_launch(); }
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 

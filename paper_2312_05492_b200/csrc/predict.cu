@@ -472,10 +472,12 @@ static int launch_predict_t(const float *x, const cszi_geom *g, int32_t radius,
     auto k = k_predict<BZ, BY, BX, CSZI_NT, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k<<<(unsigned)nblk, CSZI_NT, smem, st>>>(x, P, ctl, sym, hist, hsm ? 1 : 0);
+    note_launch();
   } else {
     auto k = k_predict<BZ, BY, BX, CSZI_NT, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k<<<(unsigned)nblk, CSZI_NT, smem, st>>>(x, P, ctl, sym, hist, hsm ? 1 : 0);
+    note_launch();
   }
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
@@ -493,6 +495,7 @@ static int launch_recon_t(const uint16_t *sym, const float *anchors, const u64 *
   auto k = k_reconstruct<BZ, BY, BX, CSZI_NT>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<(unsigned)nblk, CSZI_NT, smem, st>>>(sym, anchors, oidx, oval, nout, nout_dev, P, lc, y);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
@@ -553,6 +556,7 @@ int launch_gather_anchors(const float *x, const cszi_geom *g, float *out, cudaSt
   if (blocks > 148 * 32) blocks = 148 * 32;
   if (blocks < 1) blocks = 1;
   k_gather_anchors<<<(unsigned)blocks, threads, 0, st>>>(x, P, na[0], na[1], na[2], out);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 

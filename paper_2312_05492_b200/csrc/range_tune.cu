@@ -259,6 +259,7 @@ __global__ void __launch_bounds__(256) k_tune(const float *__restrict__ x, TuneA
 
 int launch_ctl_init(cszi_ctl *ctl, cudaStream_t st) {
   k_ctl_init<<<1, 32, 0, st>>>(ctl);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
@@ -271,6 +272,7 @@ int launch_range(const float *x, uint64_t n, cszi_ctl *ctl, cudaStream_t st) {
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   k_range<<<(unsigned)blocks, 256, 0, st>>>(x, n, ctl);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
@@ -296,6 +298,7 @@ int launch_tune(const float *x, const cszi_geom *g, const cszi_params *p, cszi_c
     A.order[a] = p->order[a];
   }
   k_tune<<<1, 256, 0, st>>>(x, A, ctl);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 

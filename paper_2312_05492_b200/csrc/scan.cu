@@ -63,6 +63,7 @@ int launch_excl_scan_u32(const uint32_t *in, u64 m, u64 *out, u64 *total, void *
   cudaMemsetAsync(scratch, 0, ntiles * 8 + 16, st);
   k_excl_scan_u32<<<(unsigned)ntiles, SCAN_NT, 0, st>>>(in, m, out, total, status, ticket,
                                                         ntiles);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
@@ -139,15 +140,18 @@ int launch_chain_resolve(const uint8_t *tab, u64 M, int D, int e0, uint8_t *entr
     uint8_t *ge = p;
     p += mg + 64;
     k_chain_up<<<(unsigned)mg, 256, smem, st>>>(ltab[L], lM[L], D, gt);
+    note_launch();
     ++L;
     ltab[L] = gt;
     lent[L] = ge;
     lM[L] = mg;
   }
   k_chain_down<<<1, 256, smem, st>>>(ltab[L], lM[L], D, nullptr, e0, lent[L]);
+  note_launch();
   for (int l = L - 1; l >= 0; --l) {
     const u64 mg = (lM[l] + CH_G - 1) / CH_G;
     k_chain_down<<<(unsigned)mg, 256, smem, st>>>(ltab[l], lM[l], D, lent[l + 1], e0, lent[l]);
+    note_launch();
   }
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }

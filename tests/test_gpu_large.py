@@ -1,0 +1,48 @@
+"""Full-size checks: the bench workload (512^3, rel 1e-3) byte-identical to
+the oracle, plus size-independent properties on other SURVEY §8 configs."""
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_2312_05492_b200 as P
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def test_nyx_512_cube_archive_identical_to_oracle():
+    import torch
+
+    from bench import smooth_field_gpu
+
+    x = smooth_field_gpu((512, 512, 512))
+    data = x.cpu().numpy()
+    g = P.Grid(P.Dims(data.shape), x)
+    arch = P.compress_device(g, 1e-3)
+    blob = arch.to_bytes()
+    ref = O.compress(data, 1e-3)
+    assert hashlib.sha256(blob).hexdigest() == hashlib.sha256(ref).hexdigest()
+    y = P.decompress_device(arch)
+    eb_abs = P.parse_archive(blob).eb_abs
+    err = (x.double() - y.tensor.double()).abs().max().item()
+    assert err <= eb_abs
+    # checksum of the decompressed field against the oracle's
+    assert hashlib.sha256(y.data.tobytes()).digest() == \
+        hashlib.sha256(O.decompress(ref).tobytes()).digest()
+
+
+@pytest.mark.parametrize("shape,eb", [((100, 500, 500), 1e-2), ((256, 384, 384), 1e-5),
+                                      ((449, 449, 235), 1e-3)])
+def test_survey_configs_round_trip(shape, eb):
+    from bench import smooth_field_gpu
+
+    x = smooth_field_gpu(shape)
+    g = P.Grid(P.Dims(shape), x)
+    arch = P.compress_device(g, eb)
+    y = P.decompress_device(arch)
+    eb_abs = P.archive.unpack_header(arch.header, len(arch)).eb_abs
+    assert (x.double() - y.tensor.double()).abs().max().item() <= eb_abs
+    # encode -> decode -> re-encode is idempotent
+    arch2 = P.compress_device(P.Grid(P.Dims(shape), x), eb)
+    assert arch2.to_bytes() == arch.to_bytes()
