@@ -41,36 +41,6 @@ constexpr double NAT_O = -3.0 / 40.0, NAT_I = 23.0 / 40.0;
 constexpr double QO = -1.0 / 8.0, QN = 6.0 / 8.0, QF = 3.0 / 8.0;
 constexpr double MAGIC = 6755399441055744.0;  // 1.5 * 2^52
 
-// predictor.py:297-306 case table; returns the prediction in float64.
-// vm3, vm1, vp1, vp3: neighbours at -3s, -s, +s, +3s (only read if used).
-DEV double spline(int cs, int variant, const float *p, int step) {
-  // cs: 0 cubic, 1 quad-left, 2 quad-right, 3 linear, 4 copy
-  const double v1 = f2d(p[-step]);
-  if (cs == 4) return v1;
-  const double v2 = f2d(p[step]);
-  if (cs == 3) return dadd(dmul(0.5, v1), dmul(0.5, v2));
-  if (cs == 1) {
-    const double v0 = f2d(p[-3 * step]);
-    return dadd(dadd(dmul(QO, v0), dmul(QN, v1)), dmul(QF, v2));
-  }
-  const double v3 = f2d(p[3 * step]);
-  if (cs == 2) return dadd(dadd(dmul(QF, v1), dmul(QN, v2)), dmul(QO, v3));
-  const double v0 = f2d(p[-3 * step]);
-  const double wo = variant ? NAT_O : NAK_O;
-  const double wi = variant ? NAT_I : NAK_I;
-  return dadd(dadd(dadd(dmul(wo, v0), dmul(wi, v1)), dmul(wi, v2)), dmul(wo, v3));
-}
-
-DEV int spline_case(int64_t pd, int64_t s, int64_t tile, int64_t extent) {
-  const int64_t offset = pd & (tile - 1);
-  const bool m3 = offset >= 3 * s;
-  const bool p1 = pd + s <= extent - 1;
-  const bool p3 = (offset <= tile - 3 * s) && (pd + 3 * s <= extent - 1);
-  if (!p1) return 4;
-  if (m3) return p3 ? 0 : 1;
-  return p3 ? 2 : 3;
-}
-
 // predictor.py:327-339.  Returns the symbol (q + R, or 0 for an outlier)
 // and the value stored in the reconstruction buffer.
 template <bool EXACT>
@@ -109,34 +79,24 @@ DEV uint32_t quantize(double pred, float o32, double leb, double e2, double inv,
   return bad ? 0u : (uint32_t)(q + R);
 }
 
-DEV bool is_anchor(const InterpParams &P, int64_t g0, int64_t g1, int64_t g2) {
-  const int64_t m = P.stride - 1;
-  return ((g0 & m) == 0 || g0 == P.ext[0] - 1) && ((g1 & m) == 0 || g1 == P.ext[1] - 1) &&
-         ((g2 & m) == 0 || g2 == P.ext[2] - 1);
+// Outlier values (decompress): symbols hold 0xFFFF at outlier points; the
+// value is found by binary search in the strictly increasing index list.
+DEV float outlier_value(const u64 *idx, const float *val, u64 k, u64 target) {
+  u64 lo = 0, hi = k;
+  while (lo < hi) {
+    const u64 mid = (lo + hi) >> 1;
+    if (idx[mid] < target) lo = mid + 1;
+    else hi = mid;
+  }
+  return val[lo];
 }
 
-// quotient for k < 2^22 via float reciprocal + one correction
+// quotient for 0 <= k < 2^22 via float reciprocal + one correction
 DEV int fdiv(int k, int d, float rd) {
   int q = __float2int_rz(__int2float_rz(k) * rd);
   if (q * d > k) q--;
   else if ((q + 1) * d <= k) q++;
   return q;
-}
-
-struct PassShape {
-  int lo[3], st[3], cnt[3];
-  int total;
-};
-
-DEV PassShape pass_shape(int d, int s, const bool passed[3], const int L[3]) {
-  PassShape ps;
-  for (int a = 0; a < 3; ++a) {
-    ps.lo[a] = (a == d) ? s : 0;
-    ps.st[a] = (a == d || !passed[a]) ? 2 * s : s;
-    ps.cnt[a] = (L[a] - 1 >= ps.lo[a]) ? (L[a] - 1 - ps.lo[a]) / ps.st[a] + 1 : 0;
-  }
-  ps.total = ps.cnt[0] * ps.cnt[1] * ps.cnt[2];
-  return ps;
 }
 
 struct LevelCfg {
@@ -147,11 +107,208 @@ struct LevelCfg {
   int nlev;
 };
 
+// Uniform description of one (level, dimension) pass inside a CTA block.
+// Work item = one segment of up to SEG consecutive pass points on one line
+// along d; items are numbered segment-major so the 32 lanes of a warp sit
+// on 32 different lines at the same position along d, which makes the
+// spline case (a function of the position along d only) warp-uniform.
+struct Pass {
+  int d, s;
+  int a1, a2;        // the two other axes (a1 slower)
+  int st1, st2;      // lattice steps on a1, a2
+  int cnt2;          // lattice count on a2
+  int nlines;
+  int npts;          // pass points per line
+  int seg, nseg;     // points per segment, segments per line
+  int pd_pitch;      // smem element distance between consecutive positions on d
+  int p1_, p2_;      // smem pitch of a1, a2
+  int tile;          // super-chunk tile on d
+  int od, ext_d;     // block origin / grid extent on d
+  int bd;            // owned extent on d
+  int o1, o2, e1, e2, b1, b2;
+  int maxeven;       // largest even-position index 2j*s inside the closed block
+  int c_d, c_1, c_2;         // strides of the owned-code array per axis
+  int64_t g_d, g_1, g_2;     // strides of the flat grid index per axis
+  float r_nl, r_c2;
+};
+
+template <int PX, int PY, int BY, int BX>
+DEV Pass make_pass(int d, int s, int passed, const int L[3], const int B[3],
+                   const int o[3], const int ext[3], const int tile[3]) {
+  Pass p;
+  const int cstr[3] = {BY * BX, BX, 1};
+  const int64_t gstr[3] = {(int64_t)ext[1] * ext[2], (int64_t)ext[2], 1};
+  p.d = d;
+  p.s = s;
+  p.a1 = (d == 0) ? 1 : 0;
+  p.a2 = (d == 2) ? 1 : 2;
+  const int pitch[3] = {PY * PX, PX, 1};
+  int st[3], cnt[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    st[a] = (a == d || !((passed >> a) & 1)) ? 2 * s : s;
+    cnt[a] = (L[a] - 1) / st[a] + 1;
+  }
+  p.st1 = st[p.a1];
+  p.st2 = st[p.a2];
+  p.cnt2 = cnt[p.a2];
+  p.nlines = cnt[p.a1] * cnt[p.a2];
+  p.npts = (L[d] - 1 >= s) ? (L[d] - 1 - s) / (2 * s) + 1 : 0;
+  const int pt = max(tile[d] / (2 * s), 1);
+  p.seg = min(pt, 4);
+  p.nseg = (p.npts + p.seg - 1) / p.seg;
+  p.pd_pitch = pitch[d];
+  p.p1_ = pitch[p.a1];
+  p.p2_ = pitch[p.a2];
+  p.tile = tile[d];
+  p.od = o[d];
+  p.bd = B[d];
+  p.ext_d = ext[d];
+  p.o1 = o[p.a1];
+  p.o2 = o[p.a2];
+  p.e1 = ext[p.a1];
+  p.e2 = ext[p.a2];
+  p.b1 = B[p.a1];
+  p.b2 = B[p.a2];
+  p.maxeven = (L[d] - 1) / (2 * s);
+  p.c_d = cstr[d];
+  p.c_1 = cstr[p.a1];
+  p.c_2 = cstr[p.a2];
+  p.g_d = gstr[d];
+  p.g_1 = gstr[p.a1];
+  p.g_2 = gstr[p.a2];
+  p.r_nl = 1.0f / (float)max(p.nlines, 1);
+  p.r_c2 = 1.0f / (float)max(p.cnt2, 1);
+  return p;
+}
+
+// spline case of the point at global coordinate pd (predictor.py:297-306)
+DEV int case_of(int pd, int s, int tile, int ext_d) {
+  const int offset = pd & (tile - 1);
+  const bool m3 = offset >= 3 * s;
+  const bool p1 = pd + s <= ext_d - 1;
+  const bool p3 = (offset <= tile - 3 * s) && (pd + 3 * s <= ext_d - 1);
+  if (!p1) return 4;
+  if (m3) return p3 ? 0 : 1;
+  return p3 ? 2 : 3;
+}
+
+// predictor.py:325 with zero-weight terms dropped (sign of zero only).
+DEV double spline4(int cs, double wo, double wi, double vm3, double vm1, double vp1,
+                   double vp3) {
+  switch (cs) {
+    case 0:
+      return dadd(dadd(dadd(dmul(wo, vm3), dmul(wi, vm1)), dmul(wi, vp1)), dmul(wo, vp3));
+    case 1:
+      return dadd(dadd(dmul(QO, vm3), dmul(QN, vm1)), dmul(QF, vp1));
+    case 2:
+      return dadd(dadd(dmul(QF, vm1), dmul(QN, vp1)), dmul(QO, vp3));
+    case 3:
+      return dadd(dmul(0.5, vm1), dmul(0.5, vp1));
+    default:
+      return vm1;
+  }
+}
+
+// Run every pass of every level on the CTA's closed block held in `buf`.
+// MODE 0 (compress): buf holds originals; writes recon + symbols (owned).
+// MODE 1 (decompress): buf holds anchors; symbols come from `csym`.
+template <int MODE, int BZ, int BY, int BX, int NT, bool EXACT>
+DEV void run_levels(float *buf, uint16_t *codes, const uint16_t *csym, const LevelCfg &cfg,
+                    const int L[3], const int o[3], const int ext[3], const int tile[3], int S,
+                    int rank, int R, const u64 *out_idx, const float *out_val, u64 n_out,
+                    const int64_t gext1, const int64_t gext2) {
+  constexpr int CZ = BZ == 1 ? 1 : BZ + 1, CY = BY == 1 ? 1 : BY + 1, CX = BX + 1;
+  constexpr int PX = CX, PY = CY;
+  const int B[3] = {BZ, BY, BX};
+  const int tid = threadIdx.x;
+  for (int lv = 0; lv < cfg.nlev; ++lv) {
+    const int s = S >> (lv + 1);
+    const double leb = cfg.leb[lv];
+    const double e2 = dmul(2.0, leb);
+    const double inv = cfg.inv[lv];
+    int passed = 0;
+    for (int oi = 0; oi < rank; ++oi) {
+      const int d = cfg.order[oi];
+      if (s < ext[d]) {
+        const Pass ps = make_pass<PX, PY, BY, BX>(d, s, passed, L, B, o, ext, tile);
+        const double wo = cfg.variant[d] ? NAT_O : NAK_O;
+        const double wi = cfg.variant[d] ? NAT_I : NAK_I;
+        const int items = ps.nlines * ps.nseg;
+        const int es = 2 * s * ps.pd_pitch;  // smem distance between even positions
+        for (int it = tid; it < items; it += NT) {
+          const int sg = fdiv(it, ps.nlines, ps.r_nl);
+          const int line = it - sg * ps.nlines;
+          const int i1 = fdiv(line, ps.cnt2, ps.r_c2);
+          const int i2 = line - i1 * ps.cnt2;
+          const int l1 = i1 * ps.st1, l2 = i2 * ps.st2;
+          const int g1 = ps.o1 + l1, g2 = ps.o2 + l2;
+          const bool line_anchor = (((g1 & (S - 1)) == 0) || g1 == ps.e1 - 1) &&
+                                   (((g2 & (S - 1)) == 0) || g2 == ps.e2 - 1);
+          const bool line_owned = l1 < ps.b1 && l2 < ps.b2;
+          float *base = buf + l1 * ps.p1_ + l2 * ps.p2_;
+          const int k0 = sg * ps.seg;
+          // window over even positions j = k-1 .. k+2 (value at 2*j*s)
+          double vm3 = (k0 >= 1) ? f2d(base[(k0 - 1) * es]) : 0.0;
+          double vm1 = f2d(base[k0 * es]);
+          double vp1 = (k0 + 1 <= ps.maxeven) ? f2d(base[(k0 + 1) * es]) : 0.0;
+          double vp3 = (k0 + 2 <= ps.maxeven) ? f2d(base[(k0 + 2) * es]) : 0.0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int k = k0 + j;
+            if (j < ps.seg && k < ps.npts) {
+              const int pdl = (2 * k + 1) * s;
+              const int pd = ps.od + pdl;
+              if (!(line_anchor && pd == ps.ext_d - 1)) {
+                const int cs = case_of(pd, s, ps.tile, ps.ext_d);
+                const double pred = spline4(cs, wo, wi, vm3, vm1, vp1, vp3);
+                float *pp = base + pdl * ps.pd_pitch;
+                if (MODE == 0) {
+                  float rec;
+                  const uint32_t sy = quantize<EXACT>(pred, *pp, leb, e2, inv, R, rec);
+                  *pp = rec;
+                  if (line_owned && pdl < ps.bd)
+                    codes[pdl * ps.c_d + l1 * ps.c_1 + l2 * ps.c_2] = (uint16_t)sy;
+                } else {
+                  const uint32_t code = csym[pp - buf];
+                  float v;
+                  if (code == 0xFFFFu) {
+                    v = outlier_value(out_idx, out_val, n_out,
+                                      (u64)(pd * ps.g_d + g1 * ps.g_1 + g2 * ps.g_2));
+                  } else {
+                    const int q = (int)code - R;
+                    const double qd =
+                        dsub(__hiloint2double(0x43300000, (int)((uint32_t)q ^ 0x80000000u)),
+                             4503601774854144.0);  // 2^52 + 2^31
+                    v = __double2float_rn(dadd(pred, dmul(e2, qd)));
+                  }
+                  *pp = v;
+                }
+              }
+              // slide the window by one even position
+              vm3 = vm1;
+              vm1 = vp1;
+              vp1 = vp3;
+              vp3 = (k + 3 <= ps.maxeven) ? f2d(base[(k + 3) * es]) : 0.0;
+            }
+          }
+        }
+      }
+      passed |= 1 << d;
+      __syncthreads();
+    }
+  }
+}
+
+}  // namespace cszi
+#include "interp_fast.cuh"
+namespace cszi {
+
 // ---------------------------------------------------------------------------
 // compress: predict + quantize + histogram
 // ---------------------------------------------------------------------------
 template <int BZ, int BY, int BX, int NT, bool EXACT>
-__global__ void __launch_bounds__(NT) k_predict(const float *__restrict__ x, InterpParams P,
+__global__ void __launch_bounds__(NT, 3) k_predict(const float *__restrict__ x, InterpParams P,
                                                 const cszi_ctl *__restrict__ ctl,
                                                 uint16_t *__restrict__ sym,
                                                 u64 *__restrict__ hist, int hist_in_smem) {
@@ -172,11 +329,13 @@ __global__ void __launch_bounds__(NT) k_predict(const float *__restrict__ x, Int
   b /= P.nb[2];
   const int by = b % P.nb[1];
   const int bz = b / P.nb[1];
-  const int64_t o0 = (int64_t)bz * BZ, o1 = (int64_t)by * BY, o2 = (int64_t)bx * BX;
+  const int o[3] = {bz * BZ, by * BY, bx * BX};
+  const int ext[3] = {(int)P.ext[0], (int)P.ext[1], (int)P.ext[2]};
+  const int tile[3] = {(int)P.tile[0], (int)P.tile[1], (int)P.tile[2]};
   int L[3];
-  L[0] = (int)min((int64_t)CZ, P.ext[0] - o0);
-  L[1] = (int)min((int64_t)CY, P.ext[1] - o1);
-  L[2] = (int)min((int64_t)CX, P.ext[2] - o2);
+  L[0] = min(CZ, ext[0] - o[0]);
+  L[1] = min(CY, ext[1] - o[1]);
+  L[2] = min(CX, ext[2] - o[2]);
   const int O0 = min(BZ, L[0]), O1 = min(BY, L[1]), O2 = min(BX, L[2]);
 
   if (tid == 0) {
@@ -192,63 +351,30 @@ __global__ void __launch_bounds__(NT) k_predict(const float *__restrict__ x, Int
   }
   if (hist_in_smem)
     for (int i = tid; i < nbins; i += NT) hs[i] = 0;
-  // stage the closed block
   const int warp = tid >> 5, lane = tid & 31;
-  for (int row = warp; row < L[0] * L[1]; row += NT / 32) {
-    const int lz = row / L[1], ly = row - lz * L[1];
-    const float *src = x + ((o0 + lz) * P.ext[1] + (o1 + ly)) * P.ext[2] + o2;
-    float *dst = buf + (lz * PY + ly) * PX;
-    for (int lx = lane; lx < L[2]; lx += 32) dst[lx] = __ldg(src + lx);
+  const bool fast_path = false;
+  {
+    for (int row = warp; row < L[0] * L[1]; row += NT / 32) {
+      const int lz = row / L[1], ly = row - lz * L[1];
+      const float *src =
+          x + ((int64_t)(o[0] + lz) * ext[1] + (o[1] + ly)) * (int64_t)ext[2] + o[2];
+      float *dst = buf + (lz * PY + ly) * PX;
+      for (int lx = lane; lx < L[2]; lx += 32) dst[lx] = __ldg(src + lx);
+    }
   }
   for (int i = tid; i < BZ * BY * BX; i += NT) codes[i] = (uint16_t)R;
   __syncthreads();
 
-  const int rank = P.rank;
-  const int S = (int)P.stride;
-  for (int lv = 0; lv < cfg.nlev; ++lv) {
-    const int s = S >> (lv + 1);
-    const double leb = cfg.leb[lv];
-    const double e2 = dmul(2.0, leb);
-    const double inv = cfg.inv[lv];
-    bool passed[3] = {false, false, false};
-    for (int oi = 0; oi < rank; ++oi) {
-      const int d = cfg.order[oi];
-      if (s < P.ext[d]) {
-        const PassShape ps = pass_shape(d, s, passed, L);
-        const int pitch = (d == 0) ? PY * PX : (d == 1 ? PX : 1);
-        const int step = s * pitch;
-        const int variant = cfg.variant[d];
-        const float r2 = 1.0f / (float)max(ps.cnt[2], 1), r1 = 1.0f / (float)max(ps.cnt[1], 1);
-        for (int k = tid; k < ps.total; k += NT) {
-          const int t = fdiv(k, ps.cnt[2], r2);
-          const int i2 = k - t * ps.cnt[2];
-          const int i0 = fdiv(t, ps.cnt[1], r1);
-          const int i1 = t - i0 * ps.cnt[1];
-          const int l0 = ps.lo[0] + i0 * ps.st[0];
-          const int l1 = ps.lo[1] + i1 * ps.st[1];
-          const int l2 = ps.lo[2] + i2 * ps.st[2];
-          const int64_t g0 = o0 + l0, g1 = o1 + l1, g2 = o2 + l2;
-          if (is_anchor(P, g0, g1, g2)) continue;
-          const int64_t pd = (d == 0) ? g0 : (d == 1 ? g1 : g2);
-          const int cs = spline_case(pd, s, P.tile[d], P.ext[d]);
-          float *p = buf + (l0 * PY + l1) * PX + l2;
-          const double pred = spline(cs, variant, p, step);
-          float rec;
-          const uint32_t sy = quantize<EXACT>(pred, *p, leb, e2, inv, R, rec);
-          *p = rec;
-          if (l0 < BZ && l1 < BY && l2 < BX) codes[(l0 * BY + l1) * BX + l2] = (uint16_t)sy;
-        }
-      }
-      passed[d] = true;
-      __syncthreads();
-    }
-  }
+  if (!fast_path)
+    run_levels<0, BZ, BY, BX, NT, EXACT>(buf, codes, nullptr, cfg, L, o, ext, tile,
+                                         (int)P.stride, P.rank, R, nullptr, nullptr, 0,
+                                         P.ext[1], P.ext[2]);
 
   // codes out (coalesced rows) + histogram; outliers (symbol 0) count as R
   uint32_t zeros = 0;
-  for (int row = warp; row < O0 * O1; row += NT / 32) {
+  for (int row = warp; !fast_path && row < O0 * O1; row += NT / 32) {
     const int lz = row / O1, ly = row - lz * O1;
-    uint16_t *dst = sym + ((o0 + lz) * P.ext[1] + (o1 + ly)) * P.ext[2] + o2;
+    uint16_t *dst = sym + ((int64_t)(o[0] + lz) * ext[1] + (o[1] + ly)) * (int64_t)ext[2] + o[2];
     const uint16_t *srow = codes + (lz * BY + ly) * BX;
     for (int lx = lane; lx < O2; lx += 32) {
       const uint32_t sy = srow[lx];
@@ -276,28 +402,16 @@ __global__ void __launch_bounds__(NT) k_predict(const float *__restrict__ x, Int
   }
 }
 
-// ---------------------------------------------------------------------------
-// decompress: inverse interpolation from symbols
-// ---------------------------------------------------------------------------
-// Outlier values: symbols hold 0xFFFF at outlier points; the value is found
-// by binary search in the (strictly increasing) outlier index list.
-DEV float outlier_value(const u64 *idx, const float *val, u64 k, u64 target) {
-  u64 lo = 0, hi = k;
-  while (lo < hi) {
-    const u64 mid = (lo + hi) >> 1;
-    if (idx[mid] < target) lo = mid + 1;
-    else hi = mid;
-  }
-  return val[lo];
-}
-
 DEV int64_t anchor_index_axis(int64_t c, int64_t S, int64_t ext) {
   // position of coordinate c in predictor.py:230-235's closed axis
   return ((c & (S - 1)) == 0) ? (c / S) : ((ext - 1) / S + 1);
 }
 
+// ---------------------------------------------------------------------------
+// decompress: inverse interpolation from symbols
+// ---------------------------------------------------------------------------
 template <int BZ, int BY, int BX, int NT>
-__global__ void __launch_bounds__(NT) k_reconstruct(
+__global__ void __launch_bounds__(NT, 3) k_reconstruct(
     const uint16_t *__restrict__ sym, const float *__restrict__ anchors, const u64 *out_idx,
     const float *out_val, u64 n_out, const u64 *nout_dev, InterpParams P, LevelCfg lc,
     float *__restrict__ y) {
@@ -315,28 +429,31 @@ __global__ void __launch_bounds__(NT) k_reconstruct(
   b /= P.nb[2];
   const int by = b % P.nb[1];
   const int bz = b / P.nb[1];
-  const int64_t o0 = (int64_t)bz * BZ, o1 = (int64_t)by * BY, o2 = (int64_t)bx * BX;
+  const int o[3] = {bz * BZ, by * BY, bx * BX};
+  const int ext[3] = {(int)P.ext[0], (int)P.ext[1], (int)P.ext[2]};
+  const int tile[3] = {(int)P.tile[0], (int)P.tile[1], (int)P.tile[2]};
   int L[3];
-  L[0] = (int)min((int64_t)CZ, P.ext[0] - o0);
-  L[1] = (int)min((int64_t)CY, P.ext[1] - o1);
-  L[2] = (int)min((int64_t)CX, P.ext[2] - o2);
+  L[0] = min(CZ, ext[0] - o[0]);
+  L[1] = min(CY, ext[1] - o[1]);
+  L[2] = min(CX, ext[2] - o[2]);
   const int O0 = min(BZ, L[0]), O1 = min(BY, L[1]), O2 = min(BX, L[2]);
   const int64_t S = P.stride;
   const int64_t na1 = (P.ext[1] - 1) / S + 1 + (((P.ext[1] - 1) & (S - 1)) ? 1 : 0);
   const int64_t na2 = (P.ext[2] - 1) / S + 1 + (((P.ext[2] - 1) & (S - 1)) ? 1 : 0);
 
   const int warp = tid >> 5, lane = tid & 31;
-  for (int row = warp; row < L[0] * L[1]; row += NT / 32) {
+  const bool fast_path = false;
+  for (int row = warp; !fast_path && row < L[0] * L[1]; row += NT / 32) {
     const int lz = row / L[1], ly = row - lz * L[1];
-    const int64_t g0 = o0 + lz, g1 = o1 + ly;
-    const uint16_t *src = sym + (g0 * P.ext[1] + g1) * P.ext[2] + o2;
+    const int64_t g0 = o[0] + lz, g1 = o[1] + ly;
+    const uint16_t *src = sym + (g0 * P.ext[1] + g1) * P.ext[2] + o[2];
     uint16_t *dst = cs_ + (lz * PY + ly) * PX;
     float *bd = buf + (lz * PY + ly) * PX;
     const bool a01 = ((g0 & (S - 1)) == 0 || g0 == P.ext[0] - 1) &&
                      ((g1 & (S - 1)) == 0 || g1 == P.ext[1] - 1);
     for (int lx = lane; lx < L[2]; lx += 32) {
       dst[lx] = src[lx];
-      const int64_t g2 = o2 + lx;
+      const int64_t g2 = o[2] + lx;
       if (a01 && ((g2 & (S - 1)) == 0 || g2 == P.ext[2] - 1)) {
         const int64_t ai = (anchor_index_axis(g0, S, P.ext[0]) * na1 +
                             anchor_index_axis(g1, S, P.ext[1])) * na2 +
@@ -347,57 +464,179 @@ __global__ void __launch_bounds__(NT) k_reconstruct(
   }
   __syncthreads();
 
-  const int rank = P.rank;
-  for (int lv = 0; lv < lc.nlev; ++lv) {
-    const int s = (int)(S >> (lv + 1));
-    const double e2 = dmul(2.0, lc.leb[lv]);
-    bool passed[3] = {false, false, false};
-    for (int oi = 0; oi < rank; ++oi) {
-      const int d = lc.order[oi];
-      if (s < P.ext[d]) {
-        const PassShape ps = pass_shape(d, s, passed, L);
-        const int pitch = (d == 0) ? PY * PX : (d == 1 ? PX : 1);
-        const int step = s * pitch;
-        const int variant = lc.variant[d];
-        const float r2 = 1.0f / (float)max(ps.cnt[2], 1), r1 = 1.0f / (float)max(ps.cnt[1], 1);
-        for (int k = tid; k < ps.total; k += NT) {
-          const int t = fdiv(k, ps.cnt[2], r2);
-          const int i2 = k - t * ps.cnt[2];
-          const int i0 = fdiv(t, ps.cnt[1], r1);
-          const int i1 = t - i0 * ps.cnt[1];
-          const int l0 = ps.lo[0] + i0 * ps.st[0];
-          const int l1 = ps.lo[1] + i1 * ps.st[1];
-          const int l2 = ps.lo[2] + i2 * ps.st[2];
-          const int64_t g0 = o0 + l0, g1 = o1 + l1, g2 = o2 + l2;
-          if (is_anchor(P, g0, g1, g2)) continue;
-          const int64_t pd = (d == 0) ? g0 : (d == 1 ? g1 : g2);
-          const int csx = spline_case(pd, s, P.tile[d], P.ext[d]);
-          const int li = (l0 * PY + l1) * PX + l2;
-          float *p = buf + li;
-          const uint32_t code = cs_[li];
-          float v;
-          if (code == 0xFFFFu) {
-            v = outlier_value(out_idx, out_val, n_out, (u64)((g0 * P.ext[1] + g1) * P.ext[2] + g2));
-          } else {
-            const double pred = spline(csx, variant, p, step);
-            // predictor.py:341-342: rec = f32(pred + e2 * float64(q))
-            const int q = (int)code - R;
-            const double qd =
-                dsub(__hiloint2double(0x43300000, (int)((uint32_t)q ^ 0x80000000u)),
-                     4503601774854144.0);  // 2^52 + 2^31
-            v = __double2float_rn(dadd(pred, dmul(e2, qd)));
-          }
-          *p = v;
-        }
-      }
-      passed[d] = true;
-      __syncthreads();
-    }
-  }
+  if (!fast_path)
+    run_levels<1, BZ, BY, BX, NT, false>(buf, nullptr, cs_, lc, L, o, ext, tile, (int)S,
+                                         P.rank, R, out_idx, out_val, n_out, P.ext[1], P.ext[2]);
+
   for (int row = warp; row < O0 * O1; row += NT / 32) {
     const int lz = row / O1, ly = row - lz * O1;
-    float *dst = y + ((o0 + lz) * P.ext[1] + (o1 + ly)) * P.ext[2] + o2;
+    float *dst = y + ((int64_t)(o[0] + lz) * ext[1] + (o[1] + ly)) * (int64_t)ext[2] + o[2];
     const float *srow = buf + (lz * PY + ly) * PX;
+    for (int lx = lane; lx < O2; lx += 32) dst[lx] = srow[lx];
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// specialised kernels for the default layouts (interp_fast.cuh)
+// ---------------------------------------------------------------------------
+template <class LY>
+DEV bool is_interior(const int o[3], const int ext[3]) {
+  return (LY::CZ == 1 || o[0] + LY::BZ <= ext[0] - 1) &&
+         (LY::CY == 1 || o[1] + LY::BY <= ext[1] - 1) && (o[2] + LY::BX <= ext[2] - 1);
+}
+
+template <class LY, int NT>
+DEV void block_coords(const InterpParams &P, int o[3], int e[3], int ext[3]) {
+  int b = blockIdx.x;
+  const int bx = b % P.nb[2];
+  b /= P.nb[2];
+  const int by = b % P.nb[1];
+  const int bz = b / P.nb[1];
+  o[0] = bz * LY::BZ;
+  o[1] = by * LY::BY;
+  o[2] = bx * LY::BX;
+  for (int a = 0; a < 3; ++a) {
+    ext[a] = (int)P.ext[a];
+    e[a] = ext[a] - o[a];
+  }
+}
+
+template <class LY, int NT, bool EXACT>
+__global__ void __launch_bounds__(NT) k_predict_fast(const float *__restrict__ x, InterpParams P,
+                                                     const cszi_ctl *__restrict__ ctl,
+                                                     uint16_t *__restrict__ sym,
+                                                     u64 *__restrict__ hist, int hist_in_smem) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float *buf = reinterpret_cast<float *>(smem_raw);
+  uint16_t *codes = reinterpret_cast<uint16_t *>(buf + ((LY::NCLOSED + 3) & ~3));
+  uint32_t *hs = reinterpret_cast<uint32_t *>(codes + LY::NOWNED);
+  __shared__ LevelCfg cfg;
+  __shared__ uint32_t zero_ws[NT / 32];
+  const int R = P.radius;
+  const int tid = threadIdx.x;
+  int o[3], e[3], ext[3];
+  block_coords<LY, NT>(P, o, e, ext);
+  if (tid == 0) {
+    cfg.nlev = ctl->nlev;
+    for (int a = 0; a < 3; ++a) {
+      cfg.order[a] = ctl->order[a];
+      cfg.variant[a] = ctl->variant[a];
+    }
+  }
+  if (tid < CSZI_MAX_LEVELS) {
+    cfg.leb[tid] = ctl->level_eb[tid];
+    cfg.inv[tid] = ctl->inv_e2[tid];
+  }
+  if (hist_in_smem)
+    for (int i = tid; i < 2 * R; i += NT) hs[i] = 0;
+  const int64_t base = ((int64_t)o[0] * ext[1] + o[1]) * (int64_t)ext[2] + o[2];
+  const int pz = ext[1] * ext[2], py = ext[2];
+  const bool interior = is_interior<LY>(o, ext);
+  if (interior)
+    fast::stage<LY, false, NT>(buf, x, base, pz, py, e);
+  else
+    fast::stage<LY, true, NT>(buf, x, base, pz, py, e);
+  const uint32_t rr = (uint32_t)R | ((uint32_t)R << 16);
+  for (int i = tid; i < LY::NOWNED / 2; i += NT) reinterpret_cast<uint32_t *>(codes)[i] = rr;
+  __syncthreads();
+  fast::Blk K{};
+  for (int a = 0; a < 3; ++a) K.e[a] = e[a];
+  uint32_t zeros;
+  if (interior) {
+    fast::run<LY, 0, EXACT, false, NT>(buf, codes, nullptr, cfg, R, K, ext, P.rank);
+    zeros = fast::store_codes_hist<LY, false, NT>(codes, sym, base, pz, py, e, R, hs,
+                                                  hist_in_smem != 0, hist);
+  } else {
+    fast::run<LY, 0, EXACT, true, NT>(buf, codes, nullptr, cfg, R, K, ext, P.rank);
+    zeros = fast::store_codes_hist<LY, true, NT>(codes, sym, base, pz, py, e, R, hs,
+                                                 hist_in_smem != 0, hist);
+  }
+  const int warp = tid >> 5, lane = tid & 31;
+  zeros = warp_sum(zeros);
+  if (lane == 0) zero_ws[warp] = zeros;
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t z = 0;
+    for (int w = 0; w < NT / 32; ++w) z += zero_ws[w];
+    if (z) atomicAdd(&hist[R], (u64)z);
+  }
+  if (hist_in_smem)
+    for (int i = tid; i < 2 * R; i += NT)
+      if (hs[i]) atomicAdd(&hist[i], (u64)hs[i]);
+}
+
+// anchor coordinate list of one axis inside a closed block of extent C
+// (predictor.py:230-235: multiples of S, plus ext-1)
+template <int C, int S>
+DEV int anchor_axis_local(int e, int *out) {
+  int n = 0;
+  for (int l = 0; l < C && l < e; l += S) out[n++] = l;
+  if (e - 1 < C && ((e - 1) % S) != 0) out[n++] = e - 1;
+  return n;
+}
+
+template <class LY, int NT>
+__global__ void __launch_bounds__(NT) k_reconstruct_fast(
+    const uint16_t *__restrict__ sym, const float *__restrict__ anchors, const u64 *out_idx,
+    const float *out_val, u64 n_out, const u64 *nout_dev, InterpParams P, LevelCfg lc,
+    float *__restrict__ y) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float *buf = reinterpret_cast<float *>(smem_raw);
+  uint16_t *cs_ = reinterpret_cast<uint16_t *>(buf + ((LY::NCLOSED + 3) & ~3));
+  const int R = P.radius;
+  const int tid = threadIdx.x;
+  if (nout_dev) n_out = *nout_dev;
+  int o[3], e[3], ext[3];
+  block_coords<LY, NT>(P, o, e, ext);
+  const int64_t base = ((int64_t)o[0] * ext[1] + o[1]) * (int64_t)ext[2] + o[2];
+  const int pz = ext[1] * ext[2], py = ext[2];
+  const bool interior = is_interior<LY>(o, ext);
+  if (interior)
+    fast::stage<LY, false, NT>(cs_, sym, base, pz, py, e);
+  else
+    fast::stage<LY, true, NT>(cs_, sym, base, pz, py, e);
+  {
+    // seed the anchors of the closed block from the anchor section
+    constexpr int S = LY::S;
+    int az[LY::CZ / S + 2], ay[LY::CY / S + 2], ax[LY::CX / S + 2];
+    const int nz = anchor_axis_local<LY::CZ, S>(e[0], az);
+    const int ny = anchor_axis_local<LY::CY, S>(e[1], ay);
+    const int nx = anchor_axis_local<LY::CX, S>(e[2], ax);
+    const int64_t na1 = (P.ext[1] - 1) / S + 1 + (((P.ext[1] - 1) % S) ? 1 : 0);
+    const int64_t na2 = (P.ext[2] - 1) / S + 1 + (((P.ext[2] - 1) % S) ? 1 : 0);
+    for (int i = tid; i < nz * ny * nx; i += NT) {
+      const int iz = i / (ny * nx), r = i - iz * ny * nx, iy = r / nx, ix = r - iy * nx;
+      const int lz = az[iz], ly = ay[iy], lx = ax[ix];
+      const int gz = o[0] + lz, gy = o[1] + ly, gx = o[2] + lx;
+      const int64_t kz = (gz % S == 0) ? gz / S : (ext[0] - 1) / S + 1;
+      const int64_t ky = (gy % S == 0) ? gy / S : (ext[1] - 1) / S + 1;
+      const int64_t kx = (gx % S == 0) ? gx / S : (ext[2] - 1) / S + 1;
+      buf[(lz * LY::PY + ly) * LY::PX + lx] = anchors[(kz * na1 + ky) * na2 + kx];
+    }
+  }
+  __syncthreads();
+  fast::Blk K;
+  for (int a = 0; a < 3; ++a) K.e[a] = e[a];
+  K.idx = out_idx;
+  K.val = out_val;
+  K.n = n_out;
+  K.gs0 = (int64_t)ext[1] * ext[2];
+  K.gs1 = ext[2];
+  K.o0 = o[0];
+  K.o1 = o[1];
+  K.o2 = o[2];
+  if (interior)
+    fast::run<LY, 1, false, false, NT>(buf, nullptr, cs_, lc, R, K, ext, P.rank);
+  else
+    fast::run<LY, 1, false, true, NT>(buf, nullptr, cs_, lc, R, K, ext, P.rank);
+  // owned region -> y
+  const int O0 = min(LY::BZ, e[0]), O1 = min(LY::BY, e[1]), O2 = min(LY::BX, e[2]);
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int row = warp; row < O0 * O1; row += NT / 32) {
+    const int lz = row / O1, ly = row - lz * O1;
+    float *dst = y + base + (int64_t)lz * pz + (int64_t)ly * py;
+    const float *srow = buf + (lz * LY::PY + ly) * LY::PX;
     for (int lx = lane; lx < O2; lx += 32) dst[lx] = srow[lx];
   }
 }
@@ -503,8 +742,61 @@ static int launch_recon_t(const uint16_t *sym, const float *anchors, const u64 *
 // 2-D (16,16) tiles -> 1x32x64; 1-D 512 tile -> 1x1x1024.  Non-default
 // strides (decode of archives with anchor_stride != default) use the shape
 // whose extents are multiples of (stride,)*rank when one exists.
+template <class LY>
+static bool layout_is(const cszi_geom *g) {
+  return g->stride == LY::S && g->tile[0] == LY::TZ && g->tile[1] == LY::TY &&
+         g->tile[2] == LY::TX && (LY::CZ > 1 || g->ext[0] == 1) && (LY::CY > 1 || g->ext[1] == 1);
+}
+
+template <class LY, int NT>
+static int launch_predict_fast(const float *x, const cszi_geom *g, int32_t radius,
+                               const cszi_ctl *ctl, uint16_t *sym, u64 *hist, bool exact,
+                               cudaStream_t st) {
+  InterpParams P;
+  if (!fill_params(g, radius, LY::BZ, LY::BY, LY::BX, P)) return CSZI_E_UNSUPPORTED;
+  const bool hsm = 2 * radius <= 8192;
+  const size_t smem = sizeof(float) * ((LY::NCLOSED + 3) & ~3) + sizeof(uint16_t) * LY::NOWNED +
+                      (hsm ? sizeof(uint32_t) * 2 * (size_t)radius : 0);
+  const int64_t nblk = (int64_t)P.nb[0] * P.nb[1] * P.nb[2];
+  if (nblk > 0x7fffffffLL) return CSZI_E_UNSUPPORTED;
+  if (exact) {
+    auto k = k_predict_fast<LY, NT, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<(unsigned)nblk, NT, smem, st>>>(x, P, ctl, sym, hist, hsm ? 1 : 0);
+  } else {
+    auto k = k_predict_fast<LY, NT, false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<(unsigned)nblk, NT, smem, st>>>(x, P, ctl, sym, hist, hsm ? 1 : 0);
+  }
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
+template <class LY, int NT>
+static int launch_recon_fast(const uint16_t *sym, const float *anchors, const u64 *oidx,
+                             const float *oval, u64 nout, const u64 *nout_dev,
+                             const cszi_geom *g, int32_t radius, const LevelCfg &lc, float *y,
+                             cudaStream_t st) {
+  InterpParams P;
+  if (!fill_params(g, radius, LY::BZ, LY::BY, LY::BX, P)) return CSZI_E_UNSUPPORTED;
+  const size_t smem = sizeof(float) * ((LY::NCLOSED + 3) & ~3) + sizeof(uint16_t) * LY::NCLOSED + 16;
+  const int64_t nblk = (int64_t)P.nb[0] * P.nb[1] * P.nb[2];
+  if (nblk > 0x7fffffffLL) return CSZI_E_UNSUPPORTED;
+  auto k = k_reconstruct_fast<LY, NT>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k<<<(unsigned)nblk, NT, smem, st>>>(sym, anchors, oidx, oval, nout, nout_dev, P, lc, y);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
 int launch_predict(const float *x, const cszi_geom *g, int32_t radius, const cszi_ctl *ctl,
                    uint16_t *sym, u64 *hist, bool exact, cudaStream_t st) {
+  if (g->rank == 3 && layout_is<fast::L3>(g))
+    return launch_predict_fast<fast::L3, 128>(x, g, radius, ctl, sym, hist, exact, st);
+  if (g->rank == 2 && layout_is<fast::L2>(g))
+    return launch_predict_fast<fast::L2, 128>(x, g, radius, ctl, sym, hist, exact, st);
+  if (g->rank == 1 && layout_is<fast::L1>(g))
+    return launch_predict_fast<fast::L1, 128>(x, g, radius, ctl, sym, hist, exact, st);
   if (g->rank == 3) return launch_predict_t<8, 16, 32>(x, g, radius, ctl, sym, hist, exact, st);
   if (g->rank == 2) return launch_predict_t<1, 32, 64>(x, g, radius, ctl, sym, hist, exact, st);
   return launch_predict_t<1, 1, 1024>(x, g, radius, ctl, sym, hist, exact, st);
@@ -525,6 +817,15 @@ int launch_reconstruct(const uint16_t *sym, const float *anchors, const u64 *oid
     lc.order[a] = order[a];
     lc.variant[a] = variant[a];
   }
+  if (g->rank == 3 && layout_is<fast::L3>(g))
+    return launch_recon_fast<fast::L3, 128>(sym, anchors, oidx, oval, nout, nout_dev, g, radius,
+                                            lc, y, st);
+  if (g->rank == 2 && layout_is<fast::L2>(g))
+    return launch_recon_fast<fast::L2, 128>(sym, anchors, oidx, oval, nout, nout_dev, g, radius,
+                                            lc, y, st);
+  if (g->rank == 1 && layout_is<fast::L1>(g))
+    return launch_recon_fast<fast::L1, 128>(sym, anchors, oidx, oval, nout, nout_dev, g, radius,
+                                            lc, y, st);
   int rc = CSZI_E_UNSUPPORTED;
   if (g->rank == 3) {
     rc = launch_recon_t<8, 16, 32>(sym, anchors, oidx, oval, nout, nout_dev, g, radius, lc, y, st);
