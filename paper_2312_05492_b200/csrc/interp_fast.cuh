@@ -90,6 +90,7 @@ DEV uint32_t quant(double pred, float o32, const Quant &Q, float &recon) {
 template <class LY, int MODE, bool EXACT, bool BND, int NT, int S, int D, int PASSED>
 DEV void pass(float *buf, uint16_t *codes, const uint16_t *csym, double wo, double wi,
               const Quant &Q, const Blk &K) {
+  const bool nak = wo == NAK_O;
   constexpr int A1 = (D == 0) ? 1 : 0;
   constexpr int A2 = (D == 2) ? 1 : 2;
   constexpr int ST1 = ((PASSED >> A1) & 1) ? S : 2 * S;
@@ -140,17 +141,23 @@ DEV void pass(float *buf, uint16_t *codes, const uint16_t *csym, double wo, doub
         p3 = p3 && (pdl + 3 * S <= ed - 1);
       }
       if (!skip) {
+        // ((w0 v0 + w1 v1) + w2 v2) + w3 v3 in float64.  For the dyadic
+        // weights (not-a-knot, quadratic, linear) every w*v of a float v is
+        // exact, so fma(w, v, acc) == RN(RN(w*v) + acc) bit for bit; the
+        // natural-spline weights (/40) are not and keep mul + add.
         double pred;
         if (!p1)
           pred = vm1;
         else if (m3 && p3)
-          pred = dadd(dadd(dadd(dmul(wo, vm3), dmul(wi, vm1)), dmul(wi, vp1)), dmul(wo, vp3));
+          pred = nak ? __fma_rn(wo, vp3, __fma_rn(wi, vp1, __fma_rn(wi, vm1, dmul(wo, vm3))))
+                     : dadd(dadd(dadd(dmul(wo, vm3), dmul(wi, vm1)), dmul(wi, vp1)),
+                            dmul(wo, vp3));
         else if (m3)
-          pred = dadd(dadd(dmul(QO, vm3), dmul(QN, vm1)), dmul(QF, vp1));
+          pred = __fma_rn(QF, vp1, __fma_rn(QN, vm1, dmul(QO, vm3)));
         else if (p3)
-          pred = dadd(dadd(dmul(QF, vm1), dmul(QN, vp1)), dmul(QO, vp3));
+          pred = __fma_rn(QO, vp3, __fma_rn(QN, vp1, dmul(QF, vm1)));
         else
-          pred = dadd(dmul(0.5, vm1), dmul(0.5, vp1));
+          pred = __fma_rn(0.5, vp1, dmul(0.5, vm1));
         float *pp = base + pdl * PD;
         if (MODE == 0) {
           float rec;
@@ -258,27 +265,67 @@ DEV void run(float *buf, uint16_t *codes, const uint16_t *csym, const LevelCfg &
   }
 }
 
-// Stage the closed block into smem with all loads in flight before the
-// stores; points outside the grid (boundary blocks) read as zero.
+DEV void cp_async4(void *sdst, const void *gsrc, bool valid) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(sdst);
+  const int n = valid ? 4 : 0;  // src-size 0 zero-fills
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(gsrc), "r"(n)
+               : "memory");
+}
+DEV void cp_async_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Stage the closed block into smem: one warp per row (z, y), lanes over x.
+// 4-byte elements go through cp.async (all rows in flight at once, no
+// registers); 2-byte symbols are loaded in batches of 8 rows per warp
+// before being stored.  Points outside the grid read as zero.
 template <class LY, bool BND, int NT, typename T>
 DEV void stage(T *dst, const T *__restrict__ src, int64_t base, int pz, int py, const int e[3]) {
-  constexpr int PER = (LY::NCLOSED + NT - 1) / NT;
-  T v[PER];
   const T *sb = src + base;  // block origin; in-block offsets fit 32 bits
-#pragma unroll
-  for (int k = 0; k < PER; ++k) {
-    const int i = threadIdx.x + k * NT;
-    v[k] = T(0);
-    if (i < LY::NCLOSED) {
-      const int row = i / LY::CX, col = i - row * LY::CX;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NROWS = LY::CZ * LY::CY;
+  constexpr int NW = NT / 32;
+  if constexpr (sizeof(T) == 4) {
+    for (int row = warp; row < NROWS; row += NW) {
       const int z = row / LY::CY, y = row - z * LY::CY;
-      if (!BND || (z < e[0] && y < e[1] && col < e[2])) v[k] = __ldg(sb + (z * pz + y * py + col));
-    }
-  }
+      const bool rv = !BND || (z < e[0] && y < e[1]);
+      const T *g = sb + (z * pz + y * py);
+      T *d = dst + row * LY::CX;
 #pragma unroll
-  for (int k = 0; k < PER; ++k) {
-    const int i = threadIdx.x + k * NT;
-    if (i < LY::NCLOSED) dst[i] = v[k];
+      for (int x0 = 0; x0 < LY::CX; x0 += 32) {
+        const int x = x0 + lane;
+        if (x < LY::CX) {
+          const bool v = rv && (!BND || x < e[2]);
+          cp_async4(d + x, v ? (const void *)(g + x) : (const void *)sb, v);
+        }
+      }
+    }
+    cp_async_wait();
+  } else {
+    constexpr int XW = (LY::CX + 31) / 32;  // elements per lane per row
+    constexpr int RB = 8;                   // rows per batch
+    for (int r0 = warp; r0 < NROWS; r0 += NW * RB) {
+      T v[RB][XW];
+#pragma unroll
+      for (int b = 0; b < RB; ++b) {
+        const int row = r0 + b * NW;
+        const int z = row / LY::CY, y = row - z * LY::CY;
+        const bool rv = row < NROWS && (!BND || (z < e[0] && y < e[1]));
+        const T *g = sb + (z * pz + y * py);
+#pragma unroll
+        for (int c = 0; c < XW; ++c) {
+          const int x = c * 32 + lane;
+          v[b][c] = (rv && x < LY::CX && (!BND || x < e[2])) ? __ldg(g + x) : T(0);
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < RB; ++b) {
+        const int row = r0 + b * NW;
+#pragma unroll
+        for (int c = 0; c < XW; ++c) {
+          const int x = c * 32 + lane;
+          if (row < NROWS && x < LY::CX) dst[row * LY::CX + x] = v[b][c];
+        }
+      }
+    }
   }
 }
 

@@ -538,7 +538,8 @@ __global__ void __launch_bounds__(NT) k_predict_fast(const float *__restrict__ x
   else
     fast::stage<LY, true, NT>(buf, x, base, pz, py, e);
   const uint32_t rr = (uint32_t)R | ((uint32_t)R << 16);
-  for (int i = tid; i < LY::NOWNED / 2; i += NT) reinterpret_cast<uint32_t *>(codes)[i] = rr;
+  for (int i = tid; i < LY::NOWNED / 8; i += NT)
+    reinterpret_cast<uint4 *>(codes)[i] = make_uint4(rr, rr, rr, rr);
   __syncthreads();
   fast::Blk K{};
   for (int a = 0; a < 3; ++a) K.e[a] = e[a];
