@@ -272,8 +272,16 @@ __global__ void __launch_bounds__(CB_NT) k_canonical(const uint8_t *__restrict__
 // ---------------------------------------------------------------------------
 // encode: one MSB-first stream; tile offsets by decoupled look-back
 // ---------------------------------------------------------------------------
+// Each thread owns ENC_SPT consecutive symbols.  Pass 1 sums their code
+// lengths; a block scan plus a decoupled look-back over tiles gives every
+// thread its global bit offset.  Pass 2 packs the codes MSB-first in a
+// 64-bit register accumulator and writes whole 32-bit words to a shared
+// staging buffer — only the (at most two) words shared with neighbouring
+// threads use atomicOr.  Staged words go to global memory with plain stores
+// except the two words a tile shares with its neighbour tiles, which are
+// merged by whichever of the two tiles arrives second.
 constexpr int ENC_NT = 256;
-constexpr int ENC_SPT = 16;
+constexpr int ENC_SPT = 32;
 constexpr int ENC_TILE = ENC_NT * ENC_SPT;
 
 struct EncScratch {  // zeroed before each launch (except head/tail)
@@ -297,17 +305,12 @@ __global__ void __launch_bounds__(ENC_NT) k_encode(const void *__restrict__ src,
                                                   u64 ntiles, cszi_ctl *ctl) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   const int nbins = 2 * R;
-  uint32_t *sw = reinterpret_cast<uint32_t *>(sm_raw);
-  uint32_t *stage = sw + nbins;              // ENC_TILE words worst case
-  uint8_t *sl = reinterpret_cast<uint8_t *>(stage + ENC_TILE + 2);
-  __shared__ u64 scan_ws[ENC_NT / 32 + 1];
+  uint2 *lut = reinterpret_cast<uint2 *>(sm_raw);  // (word, length)
+  uint32_t *stage = reinterpret_cast<uint32_t *>(lut + nbins);  // ENC_TILE + 2 words
   __shared__ uint32_t scan_ws32[ENC_NT / 32 + 1];
   __shared__ u64 s_tile, s_B, s_O;
   const int tid = threadIdx.x;
-  for (int i = tid; i < nbins; i += ENC_NT) {
-    sw[i] = words[i];
-    sl[i] = lengths[i];
-  }
+  for (int i = tid; i < nbins; i += ENC_NT) lut[i] = make_uint2(words[i], lengths[i]);
   for (;;) {
     __syncthreads();
     if (tid == 0) s_tile = atomicAdd(S.ticket, 1u);
@@ -319,13 +322,15 @@ __global__ void __launch_bounds__(ENC_NT) k_encode(const void *__restrict__ src,
     if (MODE == 0) {
       const uint16_t *sp = reinterpret_cast<const uint16_t *>(src) + base;
       if (base + ENC_SPT <= n && (((uintptr_t)sp) & 15) == 0) {
-        const uint4 a = __ldcs(reinterpret_cast<const uint4 *>(sp));
-        const uint4 b = __ldcs(reinterpret_cast<const uint4 *>(sp) + 1);
-        const uint32_t w8[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          sy[2 * j] = w8[j] & 0xffffu;
-          sy[2 * j + 1] = w8[j] >> 16;
+        for (int q = 0; q < ENC_SPT / 8; ++q) {
+          const uint4 a = __ldcs(reinterpret_cast<const uint4 *>(sp) + q);
+          const uint32_t w4[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            sy[8 * q + 2 * j] = w4[j] & 0xffffu;
+            sy[8 * q + 2 * j + 1] = w4[j] >> 16;
+          }
         }
       } else {
 #pragma unroll
@@ -336,37 +341,44 @@ __global__ void __launch_bounds__(ENC_NT) k_encode(const void *__restrict__ src,
 #pragma unroll
       for (int j = 0; j < ENC_SPT; ++j) {
         if (base + j < n) {
-          const int64_t s = (int64_t)cp[j] + R;
-          sy[j] = (s >= 0 && s < nbins) ? (uint32_t)s : 0xfffffffeu;
+          const int64_t v = (int64_t)cp[j] + R;
+          sy[j] = (v >= 0 && v < nbins) ? (uint32_t)v : 0xfffffffeu;
         } else {
           sy[j] = 0xffffffffu;
         }
       }
     }
-    uint32_t nbits = 0, nout = 0;
+    // pass 1: bit and outlier counts (sentinel 0 -> coded as R)
+    uint32_t nbits = 0, nout = 0, outmask = 0;
     bool unknown = false;
 #pragma unroll
     for (int j = 0; j < ENC_SPT; ++j) {
       uint32_t s = sy[j];
-      if (s == 0xffffffffu) continue;  // past the end
-      if (MODE == 0 && s == 0) {
-        nout++;
-        s = (uint32_t)R;
-      }
-      if (s == 0xfffffffeu || sl[s] == 0) {
+      if (s == 0xffffffffu) continue;
+      if (s == 0xfffffffeu) {
         unknown = true;
-        s = 0;
-        sy[j] = 0xfffffffdu;
+        sy[j] = 0xffffffffu;
         continue;
       }
-      nbits += sl[s];
+      if (MODE == 0 && s == 0) {
+        nout++;
+        outmask |= 1u << j;
+        s = (uint32_t)R;
+        sy[j] = s;
+      }
+      const uint32_t l = lut[s].y;
+      if (l == 0) {
+        unknown = true;
+        sy[j] = 0xffffffffu;
+        continue;
+      }
+      nbits += l;
     }
     if (unknown) atomicOr(&ctl->flags, (uint32_t)CSZI_F_UNKNOWN_SYMBOL);
-    uint32_t tot_bits, tot_out;
+    uint32_t tot_bits, tot_out = 0;
     const uint32_t bexcl = block_excl_scan<ENC_NT, uint32_t>(nbits, scan_ws32, tot_bits);
-    const uint32_t oexcl =
-        (MODE == 0) ? block_excl_scan<ENC_NT, uint32_t>(nout, scan_ws32, tot_out) : 0u;
-    if (MODE != 0) tot_out = 0;
+    uint32_t oexcl = 0;
+    if (MODE == 0) oexcl = block_excl_scan<ENC_NT, uint32_t>(nout, scan_ws32, tot_out);
     if (tid < 32) {
       const u64 B = lookback_exclusive(S.st_bits, t, tot_bits);
       u64 O = 0;
@@ -382,14 +394,13 @@ __global__ void __launch_bounds__(ENC_NT) k_encode(const void *__restrict__ src,
     const uint32_t nw = (off0 + tot_bits + 31) >> 5;
     for (uint32_t i = tid; i < nw; i += ENC_NT) stage[i] = 0;
     __syncthreads();
-    uint32_t pos = off0 + bexcl;
-    uint32_t ocount = 0;
-#pragma unroll
-    for (int j = 0; j < ENC_SPT; ++j) {
-      uint32_t s = sy[j];
-      if (s >= 0xfffffffdu) continue;
-      if (MODE == 0 && s == 0) {
-        const u64 k = O + oexcl + ocount++;
+    // outlier records in flat order
+    if (MODE == 0 && outmask) {
+      u64 k = O + oexcl;
+      uint32_t m = outmask;
+      while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
         const u64 gi = base + j;
         if (k < o_cap) {
           o_idx[k] = gi;
@@ -397,14 +408,35 @@ __global__ void __launch_bounds__(ENC_NT) k_encode(const void *__restrict__ src,
         } else {
           atomicOr(&ctl->flags, (uint32_t)CSZI_F_CAPACITY);
         }
-        s = (uint32_t)R;
+        k++;
       }
-      const uint32_t len = sl[s];
-      const u64 v = ((u64)sw[s] << (64 - len)) >> (pos & 31);
-      const uint32_t hi = (uint32_t)(v >> 32), lo = (uint32_t)v;
-      if (hi) atomicOr(&stage[pos >> 5], hi);
-      if (lo) atomicOr(&stage[(pos >> 5) + 1], lo);
-      pos += len;
+    }
+    // pass 2: pack MSB-first
+    {
+      const uint32_t pos = off0 + bexcl;
+      uint32_t w = pos >> 5;
+      const uint32_t fill = pos & 31;
+      u64 acc = 0;
+      uint32_t nb = fill;  // leading bits of word w owned by the previous thread
+      bool shared_head = fill != 0;
+#pragma unroll
+      for (int j = 0; j < ENC_SPT; ++j) {
+        const uint32_t s = sy[j];
+        if (s == 0xffffffffu) continue;
+        const uint2 e = lut[s];
+        acc = (acc << e.y) | (u64)e.x;
+        nb += e.y;
+        if (nb >= 32) {
+          const uint32_t v = (uint32_t)(acc >> (nb - 32));
+          if (shared_head) atomicOr(&stage[w], v);
+          else stage[w] = v;
+          shared_head = false;
+          ++w;
+          nb -= 32;
+          acc &= (nb ? ((1ull << nb) - 1) : 0ull);
+        }
+      }
+      if (nb > 0 && (nb > fill || !shared_head)) atomicOr(&stage[w], (uint32_t)(acc << (32 - nb)));
     }
     __syncthreads();
     const u64 gw0 = B >> 5;
@@ -447,7 +479,7 @@ __global__ void __launch_bounds__(ENC_NT) k_encode(const void *__restrict__ src,
 // ---------------------------------------------------------------------------
 // decode: self-synchronising chunked decode of one stream
 // ---------------------------------------------------------------------------
-constexpr u64 DEC_C = 2048;  // bits per chunk
+constexpr u64 DEC_C = 1024;  // bits per chunk (32 words)
 
 struct DecSmem {
   uint32_t lut[4096];
@@ -516,15 +548,60 @@ DEV uint32_t decode_at(const DecSmem &T, const uint16_t *sorted, uint32_t win, u
   return 0;
 }
 
+// Stream words of a block's chunks staged in shared memory: thread j of the
+// block decodes chunk j0 + j; a chunk walk never reads more than one word
+// past the block's last chunk (a codeword is at most 32 bits).
+constexpr int DEC_NT = 128;
+constexpr int DEC_W = (int)(DEC_C / 32);           // words per chunk
+constexpr int DEC_SW = DEC_NT * DEC_W + 4;         // staged words per block
+
+struct SmemStream {
+  const uint32_t *w;  // staged words; w[0] = stream word wbase
+  u64 wbase;
+  u64 b0, nb;
+};
+
+DEV void stage_words(uint32_t *sw, const Stream &s, u64 j0, SmemStream &ss) {
+  const u64 wbase = (j0 * DEC_C + s.b0) >> 5;
+  for (int i = threadIdx.x; i < DEC_SW; i += blockDim.x) {
+    const u64 wi = wbase + i;
+    sw[i] = wi < s.nwords ? bswap32(__ldg(s.w + wi)) : 0u;
+  }
+  ss.w = sw;
+  ss.wbase = wbase;
+  ss.b0 = s.b0;
+  ss.nb = s.nb;
+}
+
+struct SmemReader {
+  u64 buf;
+  int cw;
+  DEV void init() { cw = -2; }
+  DEV uint32_t peek(const SmemStream &s, u64 pos) {
+    const u64 a = pos + s.b0;
+    const int wi = (int)((a >> 5) - s.wbase);
+    if (wi != cw) {
+      if (wi == cw + 1) buf = (buf << 32) | s.w[wi + 1];
+      else buf = ((u64)s.w[wi] << 32) | s.w[wi + 1];
+      cw = wi;
+    }
+    return (uint32_t)((buf << (a & 31)) >> 32);
+  }
+};
+
 // Phase 1: speculative decode of chunk j from its first bit.
-__global__ void __launch_bounds__(256) k_dec_spec(Stream s, const DecTables *G,
-                                                 const uint16_t *sorted, u64 M, u64 *spec_exit,
-                                                 uint32_t *spec_cnt, uint8_t *spec_dead) {
+__global__ void __launch_bounds__(DEC_NT) k_dec_spec(Stream s, const DecTables *G,
+                                                    const uint16_t *sorted, u64 M, u64 *spec_exit,
+                                                    uint32_t *spec_cnt, uint8_t *spec_dead) {
   __shared__ DecSmem T;
-  load_dec_smem(T, G);
-  const u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+  __shared__ uint32_t sw[DEC_SW];
+  const u64 j0 = (u64)blockIdx.x * DEC_NT;
+  SmemStream ss;
+  stage_words(sw, s, j0, ss);
+  load_dec_smem(T, G);  // ends with __syncthreads()
+  const u64 j = j0 + threadIdx.x;
   if (j >= M) return;
-  BitReader br;
+  SmemReader br;
   br.init();
   u64 pos = j * DEC_C;
   const u64 end = min((j + 1) * DEC_C, s.nb);
@@ -532,7 +609,7 @@ __global__ void __launch_bounds__(256) k_dec_spec(Stream s, const DecTables *G,
   uint8_t dead = 0;
   while (pos < end) {
     uint32_t len;
-    decode_at(T, sorted, br.peek(s, pos), len);
+    decode_at(T, sorted, br.peek(ss, pos), len);
     if (len == 0 || pos + len > s.nb) {
       dead = 1;
       break;
@@ -686,30 +763,56 @@ __global__ void k_dec_from_tab(u64 M, int lmax, const uint8_t *E, const uint32_t
   X[j] = (j + 1 < M) ? (j + 1) * DEC_C + E[j + 1] : 0;
 }
 
-// Phase 4: final decode of each chunk from its true entry, writing symbols.
+// Phase 4: final decode of each chunk from its true entry.  Symbols are
+// produced in rounds of DEC_K per thread into a per-warp shared buffer and
+// flushed cooperatively (lane l writes symbol l of one thread's run), so
+// every store instruction of a warp covers one contiguous 64-128 B span.
+constexpr int DEC_K = 32;
+
 template <typename OutT>
-__global__ void __launch_bounds__(256) k_dec_write(Stream s, const DecTables *G,
-                                                  const uint16_t *sorted, u64 M, const u64 *X,
-                                                  const u64 *off, u64 n, int R,
-                                                  OutT *__restrict__ out) {
+__global__ void __launch_bounds__(DEC_NT) k_dec_write(Stream s, const DecTables *G,
+                                                     const uint16_t *sorted, u64 M, const u64 *X,
+                                                     const u64 *off, u64 n, int R,
+                                                     OutT *__restrict__ out) {
   __shared__ DecSmem T;
+  __shared__ uint32_t sw[DEC_SW];
+  constexpr int K = (sizeof(OutT) == 2) ? DEC_K : DEC_K / 2;
+  __shared__ OutT ob[DEC_NT / 32][32][K + 1];
+  const u64 j0 = (u64)blockIdx.x * DEC_NT;
+  SmemStream ss;
+  stage_words(sw, s, j0, ss);
   load_dec_smem(T, G);
-  const u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x;
-  if (j >= M) return;
-  u64 k = off[j];
-  if (k >= n) return;
-  u64 pos = (j == 0) ? 0 : X[j - 1];
-  const u64 end = min((j + 1) * DEC_C, s.nb);
-  BitReader br;
+  const u64 j = j0 + threadIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  u64 k = (j < M) ? off[j] : n;
+  u64 pos = (j < M) ? ((j == 0) ? 0 : X[j - 1]) : 0;
+  const u64 end = (j < M) ? min((j + 1) * DEC_C, s.nb) : 0;
+  bool active = j < M && k < n;
+  SmemReader br;
   br.init();
-  while (pos < end && k < n) {
-    uint32_t len;
-    const uint32_t sym = decode_at(T, sorted, br.peek(s, pos), len);
-    if (len == 0 || pos + len > s.nb) break;
-    pos += len;
-    if (sizeof(OutT) == 4) out[k] = (OutT)((int32_t)sym - R);
-    else out[k] = (OutT)sym;
-    k++;
+  while (__any_sync(CSZI_FULL, active)) {
+    int cnt = 0;
+    if (active) {
+      while (cnt < K && pos < end && k + cnt < n) {
+        uint32_t len;
+        const uint32_t sym = decode_at(T, sorted, br.peek(ss, pos), len);
+        if (len == 0 || pos + len > s.nb) {
+          pos = end;  // dead chain: truncation is reported by k_dec_check
+          break;
+        }
+        pos += len;
+        ob[warp][lane][cnt++] = (sizeof(OutT) == 4) ? (OutT)((int32_t)sym - R) : (OutT)sym;
+      }
+    }
+    __syncwarp();
+    for (int i = 0; i < 32; ++i) {
+      const int ci = __shfl_sync(CSZI_FULL, cnt, i);
+      const u64 ki = __shfl_sync(CSZI_FULL, k, i);
+      if (lane < ci) out[ki + lane] = ob[warp][i][lane];
+    }
+    __syncwarp();
+    k += cnt;
+    active = active && cnt == K && pos < end && k < n;
   }
 }
 
@@ -778,7 +881,7 @@ int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *length
   S.btail = S.bhead + nt;
   cudaMemsetAsync(p, 0, (size_t)(nt * 8 * 2 + nt * 4 + 16), st);
   const int nbins = 2 * R;
-  const size_t smem = sizeof(uint32_t) * nbins + sizeof(uint32_t) * (ENC_TILE + 2) + nbins + 16;
+  const size_t smem = sizeof(uint2) * nbins + sizeof(uint32_t) * (ENC_TILE + 2) + 16;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -857,8 +960,9 @@ int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *de
   cudaMemsetAsync(misc, 0, 16, st);
   cudaMemsetAsync(first_dead, 0xff, 8, st);
   const unsigned blocks = (unsigned)((M + 255) / 256);
+  const unsigned dblocks = (unsigned)((M + DEC_NT - 1) / DEC_NT);
   if (!table_mode) {
-    k_dec_spec<<<blocks, 256, 0, st>>>(s, G, sorted, M, spec_exit, spec_cnt, spec_dead);
+    k_dec_spec<<<dblocks, DEC_NT, 0, st>>>(s, G, sorted, M, spec_exit, spec_cnt, spec_dead);
     note_launch();
     // iteration 0 verifies every chunk; two more iterations repair chunks
     // whose predecessor did not synchronise.  A chain still moving after
@@ -894,11 +998,11 @@ int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *de
   k_dec_check<<<1, 1, 0, st>>>(off, K, first_dead, total, n, ctl);
   note_launch();
   if (out_kind == 0)
-    k_dec_write<uint16_t><<<blocks, 256, 0, st>>>(s, G, sorted, M, X0, off, n, R,
-                                                  reinterpret_cast<uint16_t *>(out));
+    k_dec_write<uint16_t><<<dblocks, DEC_NT, 0, st>>>(s, G, sorted, M, X0, off, n, R,
+                                                      reinterpret_cast<uint16_t *>(out));
   else
-    k_dec_write<int32_t><<<blocks, 256, 0, st>>>(s, G, sorted, M, X0, off, n, R,
-                                                 reinterpret_cast<int32_t *>(out));
+    k_dec_write<int32_t><<<dblocks, DEC_NT, 0, st>>>(s, G, sorted, M, X0, off, n, R,
+                                                     reinterpret_cast<int32_t *>(out));
   note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
