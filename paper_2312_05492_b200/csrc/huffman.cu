@@ -272,14 +272,16 @@ __global__ void __launch_bounds__(CB_NT) k_canonical(const uint8_t *__restrict__
 // ---------------------------------------------------------------------------
 // encode: one MSB-first stream; tile offsets by decoupled look-back
 // ---------------------------------------------------------------------------
-// Each thread owns ENC_SPT consecutive symbols.  Pass 1 sums their code
-// lengths; a block scan plus a decoupled look-back over tiles gives every
-// thread its global bit offset.  Pass 2 packs the codes MSB-first in a
-// 64-bit register accumulator and writes whole 32-bit words to a shared
-// staging buffer — only the (at most two) words shared with neighbouring
-// threads use atomicOr.  Staged words go to global memory with plain stores
-// except the two words a tile shares with its neighbour tiles, which are
-// merged by whichever of the two tiles arrives second.
+// Each persistent block owns a contiguous range of tiles (ENC_SPT symbols
+// per thread per tile).  Pass 1 sums the code lengths (and outliers) of the
+// whole range; ONE decoupled look-back across blocks gives the range its
+// global bit / outlier offsets.  Pass 2 re-reads the range tile by tile:
+// a block scan gives every thread its bit offset, codes are packed MSB-first
+// in a 64-bit register accumulator and written as whole 32-bit words to a
+// shared staging buffer (atomicOr only on the <= 2 words a thread shares
+// with its neighbours); the partial last word of a tile is carried into the
+// next tile.  The two words a range shares with its neighbour ranges are
+// merged by whichever block arrives second.
 constexpr int ENC_NT = 256;
 constexpr int ENC_SPT = 32;
 constexpr int ENC_TILE = ENC_NT * ENC_SPT;
@@ -293,8 +295,83 @@ struct EncScratch {  // zeroed before each launch (except head/tail)
   uint32_t *ticket;
 };
 
-// MODE 0: uint16 symbols from the predictor (symbol 0 = outlier sentinel,
-// encoded as symbol R and recorded in flat order).  MODE 1: int32 codes.
+template <int MODE>
+DEV void enc_load(const void *src, u64 n, int R, int nbins, u64 base, uint32_t (&sy)[ENC_SPT]) {
+  if (MODE == 0) {
+    const uint16_t *sp = reinterpret_cast<const uint16_t *>(src) + base;
+    if (base + ENC_SPT <= n && (((uintptr_t)sp) & 15) == 0) {
+#pragma unroll
+      for (int q = 0; q < ENC_SPT / 8; ++q) {
+        const uint4 a = __ldcs(reinterpret_cast<const uint4 *>(sp) + q);
+        const uint32_t w4[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          sy[8 * q + 2 * j] = w4[j] & 0xffffu;
+          sy[8 * q + 2 * j + 1] = w4[j] >> 16;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < ENC_SPT; ++j) sy[j] = (base + j < n) ? sp[j] : 0xffffffffu;
+    }
+  } else {
+    const int32_t *cp = reinterpret_cast<const int32_t *>(src) + base;
+#pragma unroll
+    for (int j = 0; j < ENC_SPT; ++j) {
+      if (base + j < n) {
+        const int64_t v = (int64_t)cp[j] + R;
+        sy[j] = (v >= 0 && v < nbins) ? (uint32_t)v : 0xfffffffeu;
+      } else {
+        sy[j] = 0xffffffffu;
+      }
+    }
+  }
+}
+
+// classify + count: returns bits; marks invalid symbols 0xffffffff
+template <int MODE>
+DEV uint32_t enc_count(uint32_t (&sy)[ENC_SPT], const uint2 *lut, int R, uint32_t &nout,
+                       uint32_t &outmask, bool &unknown) {
+  uint32_t nbits = 0;
+  nout = 0;
+  outmask = 0;
+#pragma unroll
+  for (int j = 0; j < ENC_SPT; ++j) {
+    uint32_t s = sy[j];
+    if (s == 0xffffffffu) continue;
+    if (s == 0xfffffffeu) {
+      unknown = true;
+      sy[j] = 0xffffffffu;
+      continue;
+    }
+    if (MODE == 0 && s == 0) {
+      nout++;
+      outmask |= 1u << j;
+      s = (uint32_t)R;
+      sy[j] = s;
+    }
+    const uint32_t l = lut[s].y;
+    if (l == 0) {
+      unknown = true;
+      sy[j] = 0xffffffffu;
+      continue;
+    }
+    nbits += l;
+  }
+  return nbits;
+}
+
+// merge a word shared with the neighbouring range (second arriver writes)
+DEV void enc_boundary(uint32_t *out, u64 gw, uint32_t val, uint32_t *mine, uint32_t *other,
+                      uint32_t *flag) {
+  *mine = val;
+  __threadfence();
+  if (atomicAdd(flag, 1u) == 1u) {
+    __threadfence();
+    out[gw] = bswap32(val | ld_volatile_u32(other));
+  }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(ENC_NT) k_encode(const void *__restrict__ src, u64 n, int R,
                                                   const uint8_t *__restrict__ lengths,
@@ -302,101 +379,69 @@ __global__ void __launch_bounds__(ENC_NT) k_encode(const void *__restrict__ src,
                                                   uint32_t *__restrict__ out, u64 cap_words,
                                                   const float *__restrict__ xval, u64 *o_idx,
                                                   float *o_val, u64 o_cap, EncScratch S,
-                                                  u64 ntiles, cszi_ctl *ctl) {
+                                                  u64 ntiles, u64 tiles_per_block, u64 nranges,
+                                                  cszi_ctl *ctl) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   const int nbins = 2 * R;
   uint2 *lut = reinterpret_cast<uint2 *>(sm_raw);  // (word, length)
   uint32_t *stage = reinterpret_cast<uint32_t *>(lut + nbins);  // ENC_TILE + 2 words
   __shared__ uint32_t scan_ws32[ENC_NT / 32 + 1];
-  __shared__ u64 s_tile, s_B, s_O;
+  __shared__ u64 red_ws[ENC_NT / 32 + 1];
+  __shared__ u64 s_r, s_B, s_O;
   const int tid = threadIdx.x;
   for (int i = tid; i < nbins; i += ENC_NT) lut[i] = make_uint2(words[i], lengths[i]);
-  for (;;) {
-    __syncthreads();
-    if (tid == 0) s_tile = atomicAdd(S.ticket, 1u);
-    __syncthreads();
-    const u64 t = s_tile;
-    if (t >= ntiles) break;
+  if (tid == 0) s_r = atomicAdd(S.ticket, 1u);  // ranges in ticket order
+  __syncthreads();
+  const u64 r = s_r;
+  if (r >= nranges) return;
+  const u64 t0 = r * tiles_per_block;
+  const u64 t1 = min(t0 + tiles_per_block, ntiles);
+  // ---- pass 1: range totals ----
+  u64 my_bits = 0, my_out = 0;
+  bool unknown = false;
+  for (u64 t = t0; t < t1; ++t) {
+    uint32_t sy[ENC_SPT];
+    enc_load<MODE>(src, n, R, nbins, t * ENC_TILE + (u64)tid * ENC_SPT, sy);
+    uint32_t nout, outmask;
+    my_bits += enc_count<MODE>(sy, lut, R, nout, outmask, unknown);
+    my_out += nout;
+  }
+  if (unknown) atomicOr(&ctl->flags, (uint32_t)CSZI_F_UNKNOWN_SYMBOL);
+  u64 range_bits, range_out;
+  block_excl_scan<ENC_NT, u64>(my_bits, red_ws, range_bits);
+  block_excl_scan<ENC_NT, u64>(my_out, red_ws, range_out);
+  if (tid < 32) {
+    const u64 B = lookback_exclusive(S.st_bits, r, range_bits);
+    const u64 O = (MODE == 0) ? lookback_exclusive(S.st_out, r, range_out) : 0;
+    if (tid == 0) {
+      s_B = B;
+      s_O = O;
+    }
+  }
+  __syncthreads();
+  const u64 RB = s_B, RO = s_O;  // range offsets
+  const bool last_range = (r + 1 == nranges);
+  // ---- pass 2: pack ----
+  u64 tb = RB;  // global bit offset of the current tile
+  u64 to = RO;
+  uint32_t carry = 0;  // partial last word carried from the previous tile
+  for (u64 t = t0; t < t1; ++t) {
     const u64 base = t * ENC_TILE + (u64)tid * ENC_SPT;
     uint32_t sy[ENC_SPT];
-    if (MODE == 0) {
-      const uint16_t *sp = reinterpret_cast<const uint16_t *>(src) + base;
-      if (base + ENC_SPT <= n && (((uintptr_t)sp) & 15) == 0) {
-#pragma unroll
-        for (int q = 0; q < ENC_SPT / 8; ++q) {
-          const uint4 a = __ldcs(reinterpret_cast<const uint4 *>(sp) + q);
-          const uint32_t w4[4] = {a.x, a.y, a.z, a.w};
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            sy[8 * q + 2 * j] = w4[j] & 0xffffu;
-            sy[8 * q + 2 * j + 1] = w4[j] >> 16;
-          }
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < ENC_SPT; ++j) sy[j] = (base + j < n) ? sp[j] : 0xffffffffu;
-      }
-    } else {
-      const int32_t *cp = reinterpret_cast<const int32_t *>(src) + base;
-#pragma unroll
-      for (int j = 0; j < ENC_SPT; ++j) {
-        if (base + j < n) {
-          const int64_t v = (int64_t)cp[j] + R;
-          sy[j] = (v >= 0 && v < nbins) ? (uint32_t)v : 0xfffffffeu;
-        } else {
-          sy[j] = 0xffffffffu;
-        }
-      }
-    }
-    // pass 1: bit and outlier counts (sentinel 0 -> coded as R)
-    uint32_t nbits = 0, nout = 0, outmask = 0;
-    bool unknown = false;
-#pragma unroll
-    for (int j = 0; j < ENC_SPT; ++j) {
-      uint32_t s = sy[j];
-      if (s == 0xffffffffu) continue;
-      if (s == 0xfffffffeu) {
-        unknown = true;
-        sy[j] = 0xffffffffu;
-        continue;
-      }
-      if (MODE == 0 && s == 0) {
-        nout++;
-        outmask |= 1u << j;
-        s = (uint32_t)R;
-        sy[j] = s;
-      }
-      const uint32_t l = lut[s].y;
-      if (l == 0) {
-        unknown = true;
-        sy[j] = 0xffffffffu;
-        continue;
-      }
-      nbits += l;
-    }
-    if (unknown) atomicOr(&ctl->flags, (uint32_t)CSZI_F_UNKNOWN_SYMBOL);
+    enc_load<MODE>(src, n, R, nbins, base, sy);
+    uint32_t nout, outmask;
+    bool unk2 = false;
+    const uint32_t nbits = enc_count<MODE>(sy, lut, R, nout, outmask, unk2);
     uint32_t tot_bits, tot_out = 0;
     const uint32_t bexcl = block_excl_scan<ENC_NT, uint32_t>(nbits, scan_ws32, tot_bits);
     uint32_t oexcl = 0;
     if (MODE == 0) oexcl = block_excl_scan<ENC_NT, uint32_t>(nout, scan_ws32, tot_out);
-    if (tid < 32) {
-      const u64 B = lookback_exclusive(S.st_bits, t, tot_bits);
-      u64 O = 0;
-      if (MODE == 0) O = lookback_exclusive(S.st_out, t, tot_out);
-      if (tid == 0) {
-        s_B = B;
-        s_O = O;
-      }
-    }
-    __syncthreads();
-    const u64 B = s_B, O = s_O;
-    const uint32_t off0 = (uint32_t)(B & 31);
+    const uint32_t off0 = (uint32_t)(tb & 31);
     const uint32_t nw = (off0 + tot_bits + 31) >> 5;
-    for (uint32_t i = tid; i < nw; i += ENC_NT) stage[i] = 0;
+    for (uint32_t i = tid; i < nw + 1; i += ENC_NT) stage[i] = (i == 0) ? carry : 0u;
     __syncthreads();
-    // outlier records in flat order
     if (MODE == 0 && outmask) {
-      u64 k = O + oexcl;
+      u64 k = to + oexcl;
       uint32_t m = outmask;
       while (m) {
         const int j = __ffs(m) - 1;
@@ -411,13 +456,12 @@ __global__ void __launch_bounds__(ENC_NT) k_encode(const void *__restrict__ src,
         k++;
       }
     }
-    // pass 2: pack MSB-first
     {
       const uint32_t pos = off0 + bexcl;
       uint32_t w = pos >> 5;
       const uint32_t fill = pos & 31;
       u64 acc = 0;
-      uint32_t nb = fill;  // leading bits of word w owned by the previous thread
+      uint32_t nb = fill;
       bool shared_head = fill != 0;
 #pragma unroll
       for (int j = 0; j < ENC_SPT; ++j) {
@@ -439,40 +483,43 @@ __global__ void __launch_bounds__(ENC_NT) k_encode(const void *__restrict__ src,
       if (nb > 0 && (nb > fill || !shared_head)) atomicOr(&stage[w], (uint32_t)(acc << (32 - nb)));
     }
     __syncthreads();
-    const u64 gw0 = B >> 5;
-    const bool last_tile = (t + 1 == ntiles);
-    const bool tail_partial = ((B + tot_bits) & 31) != 0 && !last_tile;
+    const u64 gw0 = tb >> 5;
+    const u64 end_bits = tb + tot_bits;
+    const bool tail_partial = (end_bits & 31) != 0;
+    const bool is_range_last_tile = (t + 1 == t1);
+    // words [0, nw): word 0 is the range head when t == t0 and unaligned;
+    // the last partial word is carried to the next tile, or is the range
+    // tail (merged with the next range) on the range's last tile.
     for (uint32_t i = tid; i < nw; i += ENC_NT) {
       const u64 gw = gw0 + i;
       const uint32_t val = stage[i];
+      const bool last_w = (i == nw - 1) && tail_partial;
+      if (last_w && !is_range_last_tile) continue;  // carried
       if (gw >= cap_words) {
         atomicOr(&ctl->flags, (uint32_t)CSZI_F_CAPACITY);
         continue;
       }
-      const bool is_first = (i == 0) && off0 != 0;
-      const bool is_last = (i == nw - 1) && tail_partial;
-      if (!is_first && !is_last) {
-        out[gw] = bswap32(val);
-      } else if (is_first) {
-        S.bhead[t] = val;
-        __threadfence();
-        if (atomicAdd(&S.bflag[t], 1u) == 1u) {
-          __threadfence();
-          out[gw] = bswap32(val | ld_volatile_u32(&S.btail[t]));
-        }
+      const bool head_w = (t == t0) && (i == 0) && (RB & 31) != 0;
+      if (head_w && last_w && !last_range) {
+        // the whole range fits inside one word shared on both sides: merge
+        // with the previous range first (as head) and the next (as tail)
+        enc_boundary(out, gw, val, &S.bhead[r], &S.btail[r], &S.bflag[r]);
+      } else if (head_w) {
+        enc_boundary(out, gw, val, &S.bhead[r], &S.btail[r], &S.bflag[r]);
+      } else if (last_w && !last_range) {
+        enc_boundary(out, gw, val, &S.btail[r + 1], &S.bhead[r + 1], &S.bflag[r + 1]);
       } else {
-        S.btail[t + 1] = val;
-        __threadfence();
-        if (atomicAdd(&S.bflag[t + 1], 1u) == 1u) {
-          __threadfence();
-          out[gw] = bswap32(val | ld_volatile_u32(&S.bhead[t + 1]));
-        }
+        out[gw] = bswap32(val);
       }
     }
-    if (last_tile && tid == 0) {
-      ctl->bits = B + tot_bits;
-      if (MODE == 0) ctl->n_outliers = O + tot_out;
-    }
+    carry = (tail_partial && !is_range_last_tile) ? stage[nw - 1] : 0u;
+    tb = end_bits;
+    to += tot_out;
+    __syncthreads();
+  }
+  if (last_range && tid == 0) {
+    ctl->bits = RB + range_bits;
+    if (MODE == 0) ctl->n_outliers = RO + range_out;
   }
 }
 
@@ -870,7 +917,13 @@ int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *length
                   cudaStream_t st) {
   if (n == 0) return CSZI_OK;
   const u64 ntiles = (n + ENC_TILE - 1) / ENC_TILE;
-  const u64 nt = ntiles + 2;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const u64 want = (u64)sms * 4;
+  const u64 tpb = (ntiles + want - 1) / want;
+  const u64 nranges = (ntiles + tpb - 1) / tpb;
+  const u64 nt = nranges + 2;
   unsigned char *p = reinterpret_cast<unsigned char *>(scratch);
   EncScratch S;
   S.st_bits = reinterpret_cast<u64 *>(p);
@@ -882,24 +935,18 @@ int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *length
   cudaMemsetAsync(p, 0, (size_t)(nt * 8 * 2 + nt * 4 + 16), st);
   const int nbins = 2 * R;
   const size_t smem = sizeof(uint2) * nbins + sizeof(uint32_t) * (ENC_TILE + 2) + 16;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  u64 grid = (u64)sms * 4;
-  if (grid > ntiles) grid = ntiles;
   if (mode == 0) {
     cudaFuncSetAttribute(k_encode<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_encode<0><<<(unsigned)grid, ENC_NT, smem, st>>>(src, n, R, lengths, words, out,
-                                                     cap_bytes / 4, xval, o_idx, o_val, o_cap,
-                                                     S, ntiles, ctl);
-    note_launch();
+    k_encode<0><<<(unsigned)nranges, ENC_NT, smem, st>>>(src, n, R, lengths, words, out,
+                                                        cap_bytes / 4, xval, o_idx, o_val, o_cap,
+                                                        S, ntiles, tpb, nranges, ctl);
   } else {
     cudaFuncSetAttribute(k_encode<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_encode<1><<<(unsigned)grid, ENC_NT, smem, st>>>(src, n, R, lengths, words, out,
-                                                     cap_bytes / 4, xval, o_idx, o_val, o_cap,
-                                                     S, ntiles, ctl);
-    note_launch();
+    k_encode<1><<<(unsigned)nranges, ENC_NT, smem, st>>>(src, n, R, lengths, words, out,
+                                                        cap_bytes / 4, xval, o_idx, o_val, o_cap,
+                                                        S, ntiles, tpb, nranges, ctl);
   }
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
