@@ -76,6 +76,10 @@ typedef struct cszi_geom {
   int64_t ext[3];      /* padded extents, slowest first                   */
   int64_t stride;      /* anchor stride S (power of two)                  */
   int64_t tile[3];     /* super-chunk tile per padded axis (1 if padded)  */
+  int64_t slab[2];     /* owned global z range [z0, z1) of a z-slab shard;
+                          {0, 0} = the whole grid.  Shard buffers hold planes
+                          [z0, min(z1 + 1, ext[0])) (one closing halo plane);
+                          3-D default layout only.                          */
 } cszi_geom;
 
 /* Host-provided compression parameters (pipeline.py:66-101). */
@@ -180,9 +184,10 @@ int cszi_ctl_init(cszi_ctl *ctl, void *stream);
 int cszi_range(const float *x, uint64_t n, cszi_ctl *ctl, void *stream);
 
 /* profile_samples + select_config + plan_levels (tuning.py:42-129,
- * predictor.py:122-136) on a ctl holding the range of x. */
-int cszi_tune(const float *x, const cszi_geom *g, const cszi_params *p, cszi_ctl *ctl,
-              void *stream);
+ * predictor.py:122-136) on a ctl holding the range of x; samples is a
+ * device scratch of CSZI_SAMPLE_WORDS int32. */
+int cszi_tune(const float *x, const cszi_geom *g, const cszi_params *p, int32_t *samples,
+              cszi_ctl *ctl, void *stream);
 
 /* compress_predict (predictor.py:395-420) on a tuned ctl:
  * sym uint16[n] = q + R (0 for outliers, R at anchors), hist uint64[2R]
@@ -198,8 +203,37 @@ int cszi_reconstruct(const uint16_t *sym, const float *anchors, const uint64_t *
                      const double *level_eb, int32_t nlev, const int32_t variant[3],
                      const int32_t order[3], float *y, void *stream);
 
-/* gather_anchors (predictor.py:250-256): lattice row-major float32 values. */
+/* gather_anchors (predictor.py:250-256): lattice row-major float32 values
+ * (of the anchor planes inside g->slab when a slab is set). */
 int cszi_gather_anchors(const float *x, const cszi_geom *g, float *out, void *stream);
+uint64_t cszi_slab_anchor_count(const cszi_geom *g);
+
+/* profile_samples split for sharding (tuning.py:42-74): gather the packed
+ * sample values (float32 bit patterns, 0 where the point lies outside the
+ * owned planes of g->slab) ... */
+#define CSZI_SAMPLE_WORDS (64 * 3 * 5)
+int cszi_sample_gather(const float *x, const cszi_geom *g, int32_t *vals, void *stream);
+/* ... and select_config + plan_levels from the (all-reduced) samples; ctl
+ * must hold the global range keys. */
+int cszi_tune_from_samples(const int32_t *vals, const cszi_geom *g, const cszi_params *p,
+                           cszi_ctl *ctl, void *stream);
+
+/* Huffman-encode predictor symbols (uint16, 0 = outlier sentinel) with a
+ * global flat-index offset for the outlier records; ctl->bits /
+ * ctl->n_outliers receive the counts.  out is 4-byte aligned. */
+uint64_t cszi_encode_sym_workspace_size(uint64_t n);
+int cszi_encode_sym(const uint16_t *sym, uint64_t n, int32_t radius, const uint8_t *lengths,
+                    const uint32_t *words, const float *x, uint64_t idx_offset, uint8_t *out,
+                    uint64_t cap_bytes, uint64_t *out_idx, float *out_val, uint64_t out_cap,
+                    void *workspace, cszi_ctl *ctl, void *stream);
+
+/* dst (zeroed, bytes) |= nbits of src placed at bit offset dst_bit (MSB-first). */
+int cszi_concat_bits(uint8_t *dst, uint64_t dst_bit, const uint8_t *src, uint64_t nbits,
+                     void *stream);
+
+/* archive.py:184-189 outlier section: u64 count + packed (u64, f32) pairs. */
+int cszi_pack_outliers(const uint64_t *idx, const float *val, uint64_t k, uint8_t *out,
+                       void *stream);
 
 /* build_histogram (huffman.py:60-74): int32 codes -> uint64[2R];
  * out-of-range codes set bit 31 of ctl->flags. */

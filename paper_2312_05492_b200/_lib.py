@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libcszi.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 MAX_LEVELS = 16
+SAMPLE_WORDS = 64 * 3 * 5
 
 # status codes (include/cszi.h)
 OK = 0
@@ -60,6 +61,7 @@ class Geom(ctypes.Structure):
         ("ext", ctypes.c_int64 * 3),
         ("stride", ctypes.c_int64),
         ("tile", ctypes.c_int64 * 3),
+        ("slab", ctypes.c_int64 * 2),
     ]
 
 
@@ -135,12 +137,22 @@ _SIGS = {
     ),
     "cszi_ctl_init": (ctypes.c_int, [_vp, _vp]),
     "cszi_range": (ctypes.c_int, [_vp, _u64, _vp, _vp]),
-    "cszi_tune": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "cszi_tune": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "cszi_predict": (ctypes.c_int, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
     "cszi_reconstruct": (
         ctypes.c_int, [_vp, _vp, _vp, _vp, _u64, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp]
     ),
     "cszi_gather_anchors": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "cszi_slab_anchor_count": (_u64, [_vp]),
+    "cszi_sample_gather": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "cszi_tune_from_samples": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "cszi_encode_sym_workspace_size": (_u64, [_u64]),
+    "cszi_encode_sym": (
+        ctypes.c_int,
+        [_vp, _u64, _i32, _vp, _vp, _vp, _u64, _vp, _u64, _vp, _vp, _u64, _vp, _vp, _vp],
+    ),
+    "cszi_concat_bits": (ctypes.c_int, [_vp, _u64, _vp, _u64, _vp]),
+    "cszi_pack_outliers": (ctypes.c_int, [_vp, _vp, _u64, _vp, _vp]),
     "cszi_histogram_i32": (ctypes.c_int, [_vp, _u64, _i32, _vp, _vp, _vp]),
     "cszi_codebook": (ctypes.c_int, [_vp, _u32, _vp, _vp, _vp, _vp]),
     "cszi_dec_tables_size": (_u64, [_u32]),

@@ -10,7 +10,15 @@ namespace cszi {
 int launch_ctl_init(cszi_ctl *ctl, cudaStream_t st);
 int launch_range(const float *x, uint64_t n, cszi_ctl *ctl, cudaStream_t st);
 int launch_tune(const float *x, const cszi_geom *g, const cszi_params *p, cszi_ctl *ctl,
-                cudaStream_t st);
+                int32_t *vals, cudaStream_t st);
+int launch_sample_gather(const float *x, const cszi_geom *g, int32_t *vals, cudaStream_t st);
+int launch_tune_from_samples(const int32_t *vals, const cszi_geom *g, const cszi_params *p,
+                             cszi_ctl *ctl, cudaStream_t st);
+uint64_t slab_anchor_count(const cszi_geom *g);
+int launch_concat_bits(uint8_t *dst, u64 dst_bit, const uint8_t *src, u64 nbits,
+                       cudaStream_t st);
+int launch_pack_outliers(const u64 *idx, const float *val, u64 k, uint8_t *out,
+                         cudaStream_t st);
 int launch_predict(const float *x, const cszi_geom *g, int32_t radius, const cszi_ctl *ctl,
                    uint16_t *sym, u64 *hist, bool exact, cudaStream_t st);
 int launch_reconstruct(const uint16_t *sym, const float *anchors, const u64 *oidx,
@@ -30,7 +38,7 @@ u64 enc_scratch_bytes(u64 n);
 int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *lengths,
                   const uint32_t *words, uint32_t *out, u64 cap_bytes, const float *xval,
                   u64 *o_idx, float *o_val, u64 o_cap, void *scratch, cszi_ctl *ctl,
-                  cudaStream_t st);
+                  cudaStream_t st, u64 idx_offset);
 u64 dec_scratch_bytes(u64 nbytes, int table_mode);
 int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *dec_tables,
                   void *out, int out_kind, void *scratch, cszi_ctl *ctl, cudaStream_t st,
@@ -168,6 +176,7 @@ static u64 raw_capacity(const cszi_geom *g, int32_t R, const cszi_caps *caps) {
 }
 
 struct CompressWS {
+  int32_t *samples;
   uint16_t *sym;
   u64 *hist;
   uint32_t *words;
@@ -184,6 +193,7 @@ static u64 layout_compress(const cszi_geom *g, int32_t R, const cszi_caps *caps,
   const u64 n = grid_n(g);
   Carver c{reinterpret_cast<unsigned char *>(base), 0};
   CompressWS w;
+  w.samples = reinterpret_cast<int32_t *>(c.take(4 * CSZI_SAMPLE_WORDS));
   w.sym = reinterpret_cast<uint16_t *>(c.take(2 * n + 32));
   w.hist = reinterpret_cast<u64 *>(c.take(8 * 2 * (u64)R));
   w.words = reinterpret_cast<uint32_t *>(c.take(4 * 2 * (u64)R));
@@ -293,7 +303,7 @@ int cszi_compress(const float *x, const cszi_geom *g, const cszi_params *p,
     k_ctl_reset_outputs<<<1, 1, 0, st>>>(ctl);
     note_launch();
   }
-  CK(launch_tune(x, g, p, ctl, st));
+  CK(launch_tune(x, g, p, ctl, W.samples, st));
   cudaMemsetAsync(W.hist, 0, 8 * nbins, st);
   CK(launch_predict(x, g, R, ctl, W.sym, W.hist, p->exact != 0, st));
   uint8_t *raw = pass2 ? W.raw : payload;
@@ -301,7 +311,7 @@ int cszi_compress(const float *x, const cszi_geom *g, const cszi_params *p,
   uint8_t *lengths = raw + 4 * na;  // the codebook section is the length table
   CK(launch_codebook(W.hist, (int)nbins, lengths, W.words, ctl, st));
   CK(launch_encode(0, W.sym, n, R, lengths, W.words, W.bits, caps->bits_cap, x, W.oidx, W.oval,
-                   caps->outlier_cap, W.enc_scratch, ctl, st));
+                   caps->outlier_cap, W.enc_scratch, ctl, st, 0));
   const u64 head = 4 * na + nbins;
   k_assemble<<<grid_for(n / 16), 256, 0, st>>>(raw, head, reinterpret_cast<uint8_t *>(W.bits),
                                                 W.oidx, W.oval, raw_cap, caps->bits_cap,
@@ -370,10 +380,45 @@ int cszi_range(const float *x, uint64_t n, cszi_ctl *ctl, void *stream) {
   return launch_range(x, n, ctl, reinterpret_cast<cudaStream_t>(stream));
 }
 
-int cszi_tune(const float *x, const cszi_geom *g, const cszi_params *p, cszi_ctl *ctl,
-              void *stream) {
+int cszi_tune(const float *x, const cszi_geom *g, const cszi_params *p, int32_t *samples,
+              cszi_ctl *ctl, void *stream) {
   CK(check_geom(g, p->radius));
-  return launch_tune(x, g, p, ctl, reinterpret_cast<cudaStream_t>(stream));
+  return launch_tune(x, g, p, ctl, samples, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int cszi_sample_gather(const float *x, const cszi_geom *g, int32_t *vals, void *stream) {
+  return launch_sample_gather(x, g, vals, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int cszi_tune_from_samples(const int32_t *vals, const cszi_geom *g, const cszi_params *p,
+                           cszi_ctl *ctl, void *stream) {
+  CK(check_geom(g, p->radius));
+  return launch_tune_from_samples(vals, g, p, ctl, reinterpret_cast<cudaStream_t>(stream));
+}
+
+uint64_t cszi_slab_anchor_count(const cszi_geom *g) { return slab_anchor_count(g); }
+
+uint64_t cszi_encode_sym_workspace_size(uint64_t n) { return enc_scratch_bytes(n) + 256; }
+
+int cszi_encode_sym(const uint16_t *sym, uint64_t n, int32_t radius, const uint8_t *lengths,
+                    const uint32_t *words, const float *x, uint64_t idx_offset, uint8_t *out,
+                    uint64_t cap_bytes, uint64_t *out_idx, float *out_val, uint64_t out_cap,
+                    void *workspace, cszi_ctl *ctl, void *stream) {
+  if (reinterpret_cast<uintptr_t>(out) & 3) return CSZI_E_INVALID_ARG;
+  return launch_encode(0, sym, n, radius, lengths, words, reinterpret_cast<uint32_t *>(out),
+                       cap_bytes, x, reinterpret_cast<u64 *>(out_idx), out_val, out_cap,
+                       workspace, ctl, reinterpret_cast<cudaStream_t>(stream), idx_offset);
+}
+
+int cszi_concat_bits(uint8_t *dst, uint64_t dst_bit, const uint8_t *src, uint64_t nbits,
+                     void *stream) {
+  return launch_concat_bits(dst, dst_bit, src, nbits, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int cszi_pack_outliers(const uint64_t *idx, const float *val, uint64_t k, uint8_t *out,
+                       void *stream) {
+  return launch_pack_outliers(reinterpret_cast<const u64 *>(idx), val, k, out,
+                              reinterpret_cast<cudaStream_t>(stream));
 }
 
 int cszi_predict(const float *x, const cszi_geom *g, int32_t radius, int32_t exact,
@@ -427,7 +472,7 @@ int cszi_huff_encode_i32(const int32_t *codes, uint64_t n, int32_t radius,
   if (reinterpret_cast<uintptr_t>(out) & 3) return CSZI_E_INVALID_ARG;
   return launch_encode(1, codes, n, radius, lengths, words, reinterpret_cast<uint32_t *>(out),
                        cap, nullptr, nullptr, nullptr, 0, workspace, ctl,
-                       reinterpret_cast<cudaStream_t>(stream));
+                       reinterpret_cast<cudaStream_t>(stream), 0);
 }
 
 uint64_t cszi_huff_decode_workspace_size(uint64_t nbytes, int32_t table_mode) {

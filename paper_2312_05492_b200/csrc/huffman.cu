@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(ENC_NT) k_encode(const void *__restrict__ src,
                                                   const float *__restrict__ xval, u64 *o_idx,
                                                   float *o_val, u64 o_cap, EncScratch S,
                                                   u64 ntiles, u64 tiles_per_block, u64 nranges,
-                                                  cszi_ctl *ctl) {
+                                                  u64 idx_offset, cszi_ctl *ctl) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   const int nbins = 2 * R;
   uint2 *lut = reinterpret_cast<uint2 *>(sm_raw);  // (word, length)
@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(ENC_NT) k_encode(const void *__restrict__ src,
         m &= m - 1;
         const u64 gi = base + j;
         if (k < o_cap) {
-          o_idx[k] = gi;
+          o_idx[k] = gi + idx_offset;
           o_val[k] = xval[gi];
         } else {
           atomicOr(&ctl->flags, (uint32_t)CSZI_F_CAPACITY);
@@ -905,6 +905,54 @@ int launch_canonical(const uint8_t *lengths, int nbins, uint32_t *words, void *d
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
+// dst |= src bits placed at bit offset dst_bit (both MSB-first byte streams)
+__global__ void k_concat_bits(uint8_t *dst, u64 dst_bit, const uint8_t *src, u64 nbits) {
+  const u64 b0 = dst_bit >> 3;
+  const int sh = (int)(dst_bit & 7);
+  const u64 nbytes_out = ((dst_bit + nbits + 7) >> 3) - b0;
+  const u64 nsrc = (nbits + 7) >> 3;
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nbytes_out;
+       i += (u64)gridDim.x * blockDim.x) {
+    uint32_t v = 0;
+    if (i < nsrc) v |= (uint32_t)src[i] >> sh;
+    if (sh && i >= 1 && i - 1 < nsrc) v |= ((uint32_t)src[i - 1] << (8 - sh)) & 0xffu;
+    if (v) dst[b0 + i] |= (uint8_t)v;
+  }
+}
+
+__global__ void k_pack_outliers(const u64 *idx, const float *val, u64 k, uint8_t *out) {
+  const u64 tid = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+  if (tid < 8) out[tid] = (uint8_t)(k >> (8 * tid));
+  for (u64 r = tid; r < k; r += (u64)gridDim.x * blockDim.x) {
+    uint8_t *q = out + 8 + 12 * r;
+    const u64 ix = idx[r];
+    const uint32_t vb = __float_as_uint(val[r]);
+    for (int b = 0; b < 8; ++b) q[b] = (uint8_t)(ix >> (8 * b));
+    for (int b = 0; b < 4; ++b) q[8 + b] = (uint8_t)(vb >> (8 * b));
+  }
+}
+
+int launch_concat_bits(uint8_t *dst, u64 dst_bit, const uint8_t *src, u64 nbits,
+                       cudaStream_t st) {
+  if (nbits == 0) return CSZI_OK;
+  const u64 nb = (nbits + 8 + 7) / 8;
+  u64 blocks = (nb + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  k_concat_bits<<<(unsigned)blocks, 256, 0, st>>>(dst, dst_bit, src, nbits);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
+int launch_pack_outliers(const u64 *idx, const float *val, u64 k, uint8_t *out,
+                         cudaStream_t st) {
+  u64 blocks = (k + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  if (blocks < 1) blocks = 1;
+  k_pack_outliers<<<(unsigned)blocks, 256, 0, st>>>(idx, val, k, out);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
 u64 enc_scratch_bytes(u64 n) {
   const u64 nt = (n + ENC_TILE - 1) / ENC_TILE + 2;
   return nt * (8 + 8 + 4 + 4 + 4) + 64;
@@ -914,7 +962,7 @@ u64 enc_scratch_bytes(u64 n) {
 int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *lengths,
                   const uint32_t *words, uint32_t *out, u64 cap_bytes, const float *xval,
                   u64 *o_idx, float *o_val, u64 o_cap, void *scratch, cszi_ctl *ctl,
-                  cudaStream_t st) {
+                  cudaStream_t st, u64 idx_offset) {
   if (n == 0) return CSZI_OK;
   const u64 ntiles = (n + ENC_TILE - 1) / ENC_TILE;
   int dev = 0, sms = 148;
@@ -939,12 +987,14 @@ int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *length
     cudaFuncSetAttribute(k_encode<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_encode<0><<<(unsigned)nranges, ENC_NT, smem, st>>>(src, n, R, lengths, words, out,
                                                         cap_bytes / 4, xval, o_idx, o_val, o_cap,
-                                                        S, ntiles, tpb, nranges, ctl);
+                                                        S, ntiles, tpb, nranges, idx_offset,
+                                                        ctl);
   } else {
     cudaFuncSetAttribute(k_encode<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_encode<1><<<(unsigned)nranges, ENC_NT, smem, st>>>(src, n, R, lengths, words, out,
                                                         cap_bytes / 4, xval, o_idx, o_val, o_cap,
-                                                        S, ntiles, tpb, nranges, ctl);
+                                                        S, ntiles, tpb, nranges, idx_offset,
+                                                        ctl);
   }
   note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;

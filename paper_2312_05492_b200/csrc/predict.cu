@@ -20,6 +20,8 @@
 // quantize()).  Zero-weight spline terms are dropped: they can only change
 // the sign of a zero prediction, which never reaches q, rec or the guard
 // because the reconstruction always adds e2*q with q == +0.0.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace cszi {
@@ -30,7 +32,8 @@ struct InterpParams {
   int64_t stride;
   int32_t rank;
   int32_t radius;
-  int32_t nb[3];  // blocks per axis
+  int32_t nb[3];  // blocks per axis (axis 0: over the owned planes of a slab)
+  int32_t z0;     // global z of local plane 0 (slab shards), else 0
 };
 
 // ---------------------------------------------------------------------------
@@ -493,7 +496,7 @@ DEV void block_coords(const InterpParams &P, int o[3], int e[3], int ext[3]) {
   b /= P.nb[2];
   const int by = b % P.nb[1];
   const int bz = b / P.nb[1];
-  o[0] = bz * LY::BZ;
+  o[0] = P.z0 + bz * LY::BZ;
   o[1] = by * LY::BY;
   o[2] = bx * LY::BX;
   for (int a = 0; a < 3; ++a) {
@@ -530,7 +533,7 @@ __global__ void __launch_bounds__(NT) k_predict_fast(const float *__restrict__ x
   }
   if (hist_in_smem)
     for (int i = tid; i < 2 * R; i += NT) hs[i] = 0;
-  const int64_t base = ((int64_t)o[0] * ext[1] + o[1]) * (int64_t)ext[2] + o[2];
+  const int64_t base = ((int64_t)(o[0] - P.z0) * ext[1] + o[1]) * (int64_t)ext[2] + o[2];
   const int pz = ext[1] * ext[2], py = ext[2];
   const bool interior = is_interior<LY>(o, ext);
   if (interior)
@@ -590,7 +593,7 @@ __global__ void __launch_bounds__(NT) k_reconstruct_fast(
   if (nout_dev) n_out = *nout_dev;
   int o[3], e[3], ext[3];
   block_coords<LY, NT>(P, o, e, ext);
-  const int64_t base = ((int64_t)o[0] * ext[1] + o[1]) * (int64_t)ext[2] + o[2];
+  const int64_t base = ((int64_t)(o[0] - P.z0) * ext[1] + o[1]) * (int64_t)ext[2] + o[2];
   const int pz = ext[1] * ext[2], py = ext[2];
   const bool interior = is_interior<LY>(o, ext);
   if (interior)
@@ -645,17 +648,45 @@ __global__ void __launch_bounds__(NT) k_reconstruct_fast(
 // ---------------------------------------------------------------------------
 // anchors: gather_anchors (predictor.py:250-256) / lattice row-major order
 // ---------------------------------------------------------------------------
-__global__ void k_gather_anchors(const float *__restrict__ x, InterpParams P, int64_t na0,
-                                 int64_t na1, int64_t na2, float *__restrict__ out) {
+// anchor planes i0 in [ia0, ia0 + na0) of the lattice; x holds planes from z0
+__global__ void k_gather_anchors(const float *__restrict__ x, InterpParams P, int64_t ia0,
+                                 int64_t na0, int64_t na1, int64_t na2, int64_t z0,
+                                 float *__restrict__ out) {
   const int64_t total = na0 * na1 * na2;
   const int64_t S = P.stride;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i2 = i % na2, t = i / na2, i1 = t % na1, i0 = t / na1;
+    const int64_t i2 = i % na2, t = i / na2, i1 = t % na1, i0 = ia0 + t / na1;
     const int64_t c0 = min(i0 * S, P.ext[0] - 1), c1 = min(i1 * S, P.ext[1] - 1),
                   c2 = min(i2 * S, P.ext[2] - 1);
-    out[i] = x[(c0 * P.ext[1] + c1) * P.ext[2] + c2];
+    out[i] = x[((c0 - z0) * P.ext[1] + c1) * P.ext[2] + c2];
   }
+}
+
+// anchor-lattice planes [ia0, ia1) whose z coordinate lies in the slab
+static void slab_anchor_planes(const cszi_geom *g, int64_t &ia0, int64_t &ia1) {
+  const int64_t e = g->ext[0], S = g->stride;
+  const int64_t na = (e - 1) / S + 1 + (((e - 1) % S) ? 1 : 0);
+  if (g->slab[1] <= g->slab[0]) {
+    ia0 = 0;
+    ia1 = na;
+    return;
+  }
+  const int64_t z0 = g->slab[0], z1 = g->slab[1];
+  ia0 = (z0 + S - 1) / S;
+  ia1 = ia0;
+  while (ia1 < na && std::min(ia1 * S, e - 1) < z1) ++ia1;
+}
+
+uint64_t slab_anchor_count(const cszi_geom *g) {
+  int64_t ia0, ia1;
+  slab_anchor_planes(g, ia0, ia1);
+  int64_t c = ia1 - ia0;
+  for (int a = 1; a < 3; ++a) {
+    const int64_t e = g->ext[a], S = g->stride;
+    c *= (e - 1) / S + 1 + (((e - 1) % S) ? 1 : 0);
+  }
+  return (uint64_t)c;
 }
 
 // ---------------------------------------------------------------------------
@@ -693,6 +724,12 @@ static bool fill_params(const cszi_geom *g, int32_t radius, int bz, int by, int 
     if (g->tile[a] & (g->tile[a] - 1)) return false;
     P.nb[a] = (int)((g->ext[a] + B[a] - 1) / B[a]);
   }
+  P.z0 = 0;
+  if (g->slab[1] > g->slab[0]) {  // z-slab shard: blocks over the owned planes
+    if (g->slab[0] % bz != 0) return false;
+    P.z0 = (int)g->slab[0];
+    P.nb[0] = (int)((g->slab[1] - g->slab[0] + bz - 1) / bz);
+  }
   return true;
 }
 
@@ -703,7 +740,8 @@ static int launch_predict_t(const float *x, const cszi_geom *g, int32_t radius,
                             const cszi_ctl *ctl, uint16_t *sym, u64 *hist, bool exact,
                             cudaStream_t st) {
   InterpParams P;
-  if (!fill_params(g, radius, BZ, BY, BX, P)) return CSZI_E_UNSUPPORTED;
+  if (!fill_params(g, radius, BZ, BY, BX, P) || P.z0 != 0 || g->slab[1] > g->slab[0])
+    return CSZI_E_UNSUPPORTED;
   const bool hsm = 2 * radius <= 8192;
   const size_t smem = predict_smem<BZ, BY, BX>(radius, hsm);
   const int64_t nblk = (int64_t)P.nb[0] * P.nb[1] * P.nb[2];
@@ -728,7 +766,8 @@ static int launch_recon_t(const uint16_t *sym, const float *anchors, const u64 *
                           const cszi_geom *g, int32_t radius,
                           const LevelCfg &lc, float *y, cudaStream_t st) {
   InterpParams P;
-  if (!fill_params(g, radius, BZ, BY, BX, P)) return CSZI_E_UNSUPPORTED;
+  if (!fill_params(g, radius, BZ, BY, BX, P) || g->slab[1] > g->slab[0])
+    return CSZI_E_UNSUPPORTED;
   const size_t smem = recon_smem<BZ, BY, BX>();
   const int64_t nblk = (int64_t)P.nb[0] * P.nb[1] * P.nb[2];
   if (nblk > 0x7fffffffLL) return CSZI_E_UNSUPPORTED;
@@ -852,12 +891,17 @@ int launch_gather_anchors(const float *x, const cszi_geom *g, float *out, cudaSt
     const int64_t e = g->ext[a], S = g->stride;
     na[a] = (e - 1) / S + 1 + (((e - 1) % S) ? 1 : 0);
   }
-  const int64_t total = na[0] * na[1] * na[2];
+  int64_t ia0, ia1;
+  slab_anchor_planes(g, ia0, ia1);
+  const int64_t z0 = (g->slab[1] > g->slab[0]) ? g->slab[0] : 0;
+  const int64_t total = (ia1 - ia0) * na[1] * na[2];
+  if (total <= 0) return CSZI_OK;
   const int threads = 256;
   int64_t blocks = (total + threads - 1) / threads;
   if (blocks > 148 * 32) blocks = 148 * 32;
   if (blocks < 1) blocks = 1;
-  k_gather_anchors<<<(unsigned)blocks, threads, 0, st>>>(x, P, na[0], na[1], na[2], out);
+  k_gather_anchors<<<(unsigned)blocks, threads, 0, st>>>(x, P, ia0, ia1 - ia0, na[1], na[2], z0,
+                                                         out);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }

@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(256) k_range(const float *__restrict__ x, uint
 }
 
 struct TuneArgs {
-  int64_t ext[3];  // padded
+  int64_t ext[3];  // padded (global)
   int32_t rank;
   int32_t pad_axes;  // 3 - rank
   int32_t mode_rel;
@@ -104,6 +104,8 @@ struct TuneArgs {
   double alpha_pow[CSZI_MAX_LEVELS];
   int32_t variant[3];
   int32_t order[3];
+  int64_t z0;        // global z of local plane 0
+  int64_t zlo, zhi;  // owned global z range (values outside read as 0)
 };
 
 // tuning.py:32-39 on one axis.
@@ -116,72 +118,101 @@ DEV int sample_axis(int64_t extent, int64_t *out) {
   return (int)k;
 }
 
-// One block of 256 threads.  Samples are gathered in parallel; the error
-// sums are accumulated in the reference's order (mesh order, per (d, v)).
-__global__ void __launch_bounds__(256) k_tune(const float *__restrict__ x, TuneArgs A,
-                                              cszi_ctl *ctl) {
-  __shared__ int64_t pts[3][4];
-  __shared__ int npts[3];
-  __shared__ int prof[3];
+struct SamplePlan {
+  int64_t pts[3][4];
+  int npts[3];
+  int prof[3];
+  int P;
+};
+
+DEV void sample_plan(const TuneArgs &A, SamplePlan &sp) {
+  const int rank = A.rank, pad = A.pad_axes;
+  for (int d = 0; d < rank; ++d) {
+    const int64_t e = A.ext[pad + d];
+    const int k = sample_axis(e, sp.pts[d]);
+    sp.prof[d] = k > 0;
+    if (k == 0) {
+      sp.pts[d][0] = e / 2;
+      sp.npts[d] = 1;
+    } else {
+      sp.npts[d] = k;
+    }
+  }
+  for (int d = rank; d < 3; ++d) {
+    sp.npts[d] = 1;
+    sp.prof[d] = 0;
+    sp.pts[d][0] = 0;
+  }
+  sp.P = sp.npts[0] * sp.npts[1] * sp.npts[2];  // <= 64 mesh points, ij order
+}
+
+// Gather the profiled values (tuning.py:55-62): for mesh point p and
+// profiled dim d, vals[(p*3 + d)*5 + k] = bits of the values at offsets
+// -3, -1, +1, +3 along d (k = 0..3) and of the point itself (k = 4); 0 when
+// the value's plane is outside [zlo, zhi) (another shard owns it).
+__global__ void __launch_bounds__(256) k_sample_gather(const float *__restrict__ x, TuneArgs A,
+                                                       int32_t *vals) {
+  SamplePlan sp;
+  sample_plan(A, sp);
+  const int rank = A.rank, pad = A.pad_axes;
+  for (int w = threadIdx.x; w < CSZI_SAMPLE_WORDS; w += blockDim.x) vals[w] = 0;
+  __syncthreads();
+  for (int w = threadIdx.x; w < sp.P * rank * 5; w += blockDim.x) {
+    const int k = w % 5, pd = w / 5, p = pd / rank, d = pd - p * rank;
+    if (!sp.prof[d]) continue;
+    int idx[3];
+    int rem = p;
+    for (int a = rank - 1; a >= 0; --a) {
+      idx[a] = rem % sp.npts[a];
+      rem /= sp.npts[a];
+    }
+    int64_t c[3] = {0, 0, 0};
+    for (int a = 0; a < rank; ++a) c[pad + a] = sp.pts[a][idx[a]];
+    const int offs[5] = {-3, -1, 1, 3, 0};
+    c[pad + d] += offs[k];
+    if (c[0] < A.zlo || c[0] >= A.zhi) continue;
+    const int64_t li = ((c[0] - A.z0) * A.ext[1] + c[1]) * A.ext[2] + c[2];
+    vals[(p * 3 + d) * 5 + k] = __float_as_int(x[li]);
+  }
+}
+
+// select_config + plan_levels from the gathered samples; the error sums are
+// accumulated in the reference's order (mesh order, per (d, v)).
+__global__ void __launch_bounds__(256) k_tune_decide(const int32_t *__restrict__ vals,
+                                                     TuneArgs A, cszi_ctl *ctl) {
+  __shared__ SamplePlan sp;
   __shared__ double errs[64][3][2];
   __shared__ double err_sum[3][2];
   __shared__ int64_t cnt[3];
   const int tid = threadIdx.x;
   const int rank = A.rank, pad = A.pad_axes;
-  if (tid == 0) {
-    for (int d = 0; d < rank; ++d) {
-      const int64_t e = A.ext[pad + d];
-      const int k = sample_axis(e, pts[d]);
-      prof[d] = k > 0;
-      if (k == 0) {
-        pts[d][0] = e / 2;
-        npts[d] = 1;
-      } else {
-        npts[d] = k;
-      }
-    }
-    for (int d = rank; d < 3; ++d) {
-      npts[d] = 1;
-      prof[d] = 0;
-      pts[d][0] = 0;
-    }
-  }
+  if (tid == 0) sample_plan(A, sp);
   __syncthreads();
-  const int P = npts[0] * npts[1] * npts[2];  // <= 64 mesh points, ij order
+  const int P = sp.P;
   for (int w = tid; w < P * rank; w += blockDim.x) {
     const int p = w / rank, d = w - p * rank;
-    if (!prof[d]) continue;
-    int idx[3];
-    int rem = p;
-    for (int a = rank - 1; a >= 0; --a) {
-      idx[a] = rem % npts[a];
-      rem /= npts[a];
-    }
-    int64_t c[3] = {0, 0, 0};
-    for (int a = 0; a < rank; ++a) c[pad + a] = pts[a][idx[a]];
-    const int ax = pad + d;
-    const int64_t stride_d = (ax == 0) ? A.ext[1] * A.ext[2] : (ax == 1 ? A.ext[2] : 1);
-    const int64_t base = (c[0] * A.ext[1] + c[1]) * A.ext[2] + c[2];
-    const double v0 = (double)x[base - 3 * stride_d], v1 = (double)x[base - stride_d];
-    const double v2 = (double)x[base + stride_d], v3 = (double)x[base + 3 * stride_d];
-    const double actual = (double)x[base];
+    if (!sp.prof[d]) continue;
+    const int32_t *v = vals + (p * 3 + d) * 5;
+    const double v0 = (double)__int_as_float(v[0]), v1 = (double)__int_as_float(v[1]);
+    const double v2 = (double)__int_as_float(v[2]), v3 = (double)__int_as_float(v[3]);
+    const double actual = (double)__int_as_float(v[4]);
     // tuning.py:63-66, weights predictor.py:62-65
     const double wts[2][2] = {{-1.0 / 16.0, 9.0 / 16.0}, {-3.0 / 40.0, 23.0 / 40.0}};
-    for (int v = 0; v < 2; ++v) {
+    for (int vv = 0; vv < 2; ++vv) {
       const double pred =
-          dadd(dadd(dadd(dmul(wts[v][0], v0), dmul(wts[v][1], v1)), dmul(wts[v][1], v2)),
-               dmul(wts[v][0], v3));
-      errs[p][d][v] = fabs(dsub(pred, actual));
+          dadd(dadd(dadd(dmul(wts[vv][0], v0), dmul(wts[vv][1], v1)), dmul(wts[vv][1], v2)),
+               dmul(wts[vv][0], v3));
+      errs[p][d][vv] = fabs(dsub(pred, actual));
     }
   }
   __syncthreads();
   if (tid < 6) {
     const int d = tid >> 1, v = tid & 1;
     double acc = 0.0;
-    if (d < rank && prof[d])
+    if (d < rank && sp.prof[d])
       for (int p = 0; p < P; ++p) acc = dadd(acc, errs[p][d][v]);
     err_sum[d][v] = acc;
-    if (v == 0) cnt[d] = (d < rank && prof[d]) ? P : 0;
+    if (v == 0) cnt[d] = (d < rank && sp.prof[d]) ? P : 0;
   }
   __syncthreads();
   if (tid != 0) return;
@@ -276,9 +307,7 @@ int launch_range(const float *x, uint64_t n, cszi_ctl *ctl, cudaStream_t st) {
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
-int launch_tune(const float *x, const cszi_geom *g, const cszi_params *p, cszi_ctl *ctl,
-                cudaStream_t st) {
-  TuneArgs A;
+static int tune_args(const cszi_geom *g, const cszi_params *p, TuneArgs &A) {
   for (int a = 0; a < 3; ++a) A.ext[a] = g->ext[a];
   A.rank = g->rank;
   A.pad_axes = 3 - g->rank;
@@ -297,9 +326,40 @@ int launch_tune(const float *x, const cszi_geom *g, const cszi_params *p, cszi_c
     A.variant[a] = p->variant[a];
     A.order[a] = p->order[a];
   }
-  k_tune<<<1, 256, 0, st>>>(x, A, ctl);
+  const bool slab = g->slab[1] > g->slab[0];
+  A.z0 = slab ? g->slab[0] : 0;
+  A.zlo = slab ? g->slab[0] : 0;
+  A.zhi = slab ? g->slab[1] : g->ext[0];
+  return CSZI_OK;
+}
+
+int launch_sample_gather(const float *x, const cszi_geom *g, int32_t *vals, cudaStream_t st) {
+  TuneArgs A;
+  cszi_params p{};
+  p.have_alpha = 1;
+  const int rc = tune_args(g, &p, A);
+  if (rc != CSZI_OK) return rc;
+  k_sample_gather<<<1, 256, 0, st>>>(x, A, vals);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
+int launch_tune_from_samples(const int32_t *vals, const cszi_geom *g, const cszi_params *p,
+                             cszi_ctl *ctl, cudaStream_t st) {
+  TuneArgs A;
+  const int rc = tune_args(g, p, A);
+  if (rc != CSZI_OK) return rc;
+  k_tune_decide<<<1, 256, 0, st>>>(vals, A, ctl);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
+// single device: gather (into ctl->scratch-sized device buffer) + decide
+int launch_tune(const float *x, const cszi_geom *g, const cszi_params *p, cszi_ctl *ctl,
+                int32_t *vals, cudaStream_t st) {
+  int rc = launch_sample_gather(x, g, vals, st);
+  if (rc != CSZI_OK) return rc;
+  return launch_tune_from_samples(vals, g, p, ctl, st);
 }
 
 }  // namespace cszi

@@ -1,0 +1,389 @@
+"""Multi-GPU compression by z-slabs.
+
+One field, one archive, byte-identical to single-GPU ``compress``.  The
+⌈nz/8⌉ anchor tiles along z are split as evenly as possible over the ranks;
+rank r owns planes [z0, z1) and holds one closing halo plane (z1) as well,
+which is all the tile-confined predictor needs (predictor.py:293-299), so
+prediction runs without any exchange.  Collectives:
+
+1. allreduce MIN of (range key min, -range key max, first non-finite index);
+2. allreduce SUM of the packed tuner samples (each sample value is owned by
+   exactly one rank; float bit patterns, so the sum is exact);
+3. allreduce SUM of the uint64[2R] histogram -> identical codebook everywhere;
+4. allgather of per-slab (bit count, outlier count);
+5. gather of anchors / bitstream / outliers to rank 0, which concatenates the
+   bitstreams at their global bit offsets and runs pass-2.
+
+``Comm`` abstracts the collectives: ``TorchComm`` (torch.distributed: NCCL on
+GPU tensors, gloo on CPU), ``SimComm`` (N slabs in one process, used to check
+GPU-count determinism on a single GPU).  ``GpuSlabBackend`` runs every
+per-slab stage in libcszi.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .archive import EB_ABS, EB_REL, PREDICTOR_INTERP, pack_header
+from .errors import EmptyHistogram, Inconsistent, LengthOverflow, NonFiniteValue
+from .pipeline import DeviceArchive
+from .predictor import count_anchors, ctl_order, ctl_variants, default_layout, make_geom, make_params
+from .tuning import compute_alpha
+
+INT64_MAX = (1 << 63) - 1
+ANCHOR_TILE = 8  # z-slabs align to the 3-D anchor stride
+
+
+def slab_bounds(nz: int, world: int, tile: int = ANCHOR_TILE) -> list:
+    """Owned z ranges: ⌈nz/tile⌉ tiles, the first (tiles mod world) ranks get one more."""
+    tiles = -(-nz // tile)
+    base, extra = divmod(tiles, world)
+    out, t = [], 0
+    for r in range(world):
+        cnt = base + (1 if r < extra else 0)
+        z0 = min(nz, t * tile)
+        z1 = min(nz, (t + cnt) * tile)
+        out.append((z0, z1))
+        t += cnt
+    return out
+
+
+# ---------------------------------------------------------------------------
+# communicators
+# ---------------------------------------------------------------------------
+class SimComm:
+    """All slabs live in this process; collectives reduce across the list."""
+
+    def __init__(self, world: int):
+        self.world = world
+
+    def allreduce(self, ts, op: str):
+        t = _lib.torch()
+        stack = t.stack([x.reshape(-1) for x in ts])
+        r = {"sum": stack.sum(0), "min": stack.min(0).values, "max": stack.max(0).values}[op]
+        for x in ts:
+            x.copy_(r.view_as(x).to(x.dtype))
+
+    def allgather(self, ts):
+        return [list(ts) for _ in ts]
+
+    def gather(self, ts):
+        return list(ts)  # every slab is local: "root" sees all
+
+
+class TorchComm:
+    """torch.distributed collectives (one slab per process)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def allreduce(self, ts, op: str):
+        d = self.dist
+        o = {"sum": d.ReduceOp.SUM, "min": d.ReduceOp.MIN, "max": d.ReduceOp.MAX}[op]
+        for x in ts:
+            d.all_reduce(x, op=o, group=self.group)
+
+    def allgather(self, ts):
+        out = []
+        for x in ts:
+            parts = [x.new_empty(x.shape) for _ in range(self.world)]
+            self.dist.all_gather(parts, x, group=self.group)
+            out.append(parts)
+        return out
+
+    def gather(self, ts):
+        """Variable-length 1-D tensors -> list on rank 0 (None elsewhere)."""
+        t = _lib.torch()
+        (x,) = ts
+        n = t.tensor([x.numel()], dtype=t.int64, device=x.device)
+        sizes = [t.empty_like(n) for _ in range(self.world)]
+        self.dist.all_gather(sizes, n, group=self.group)
+        sizes = [int(s.item()) for s in sizes]
+        m = max(max(sizes), 1)
+        pad = x.new_zeros(m)
+        pad[: x.numel()] = x.reshape(-1)
+        if self.rank == 0:
+            parts = [x.new_empty(m) for _ in range(self.world)]
+            self.dist.gather(pad, parts, dst=0, group=self.group)
+            return [p[:s] for p, s in zip(parts, sizes)]
+        self.dist.gather(pad, None, dst=0, group=self.group)
+        return None
+
+
+# ---------------------------------------------------------------------------
+# per-slab state + GPU backend
+# ---------------------------------------------------------------------------
+@dataclass
+class SlabState:
+    x: object            # local planes [z0, min(z1 + 1, nz)) as float32 (device)
+    extents: tuple       # global extents (rank 3)
+    z0: int
+    z1: int
+    eb: float
+    mode: str
+    radius: int
+    scratch: dict = field(default_factory=dict)
+
+
+def _ctl_field(ctl, name, dtype):
+    """Device view of one cszi_ctl field (for collectives on device)."""
+    t = _lib.torch()
+    off = getattr(_lib.Ctl, name).offset
+    size = getattr(_lib.Ctl, name).size
+    return ctl.dev[off: off + size].view(dtype)
+
+
+class GpuSlabBackend:
+    def geom(self, s: SlabState):
+        g = make_geom(s.extents, default_layout(3))
+        g.slab[0] = s.z0
+        g.slab[1] = s.z1
+        return g
+
+    def range_keys(self, s: SlabState):
+        t = _lib.require_cuda()
+        lib = _lib.load()
+        st = _lib.stream_ptr()
+        ctl = _lib.DeviceCtl()
+        s.scratch["ctl"] = ctl
+        ny, nx = s.extents[1], s.extents[2]
+        n_own = (s.z1 - s.z0) * ny * nx
+        _lib.check(lib.cszi_ctl_init(ctl.ptr, st), "ctl_init")
+        if n_own:
+            _lib.check(lib.cszi_range(_lib.ptr(s.x), n_own, ctl.ptr, st), "range")
+        keys = _ctl_field(ctl, "vmin_key", t.int32).to(t.int64) & 0xFFFFFFFF
+        kmax = _ctl_field(ctl, "vmax_key", t.int32).to(t.int64) & 0xFFFFFFFF
+        fnf = _ctl_field(ctl, "first_nonfinite", t.int64).clone()
+        fnf = t.where(fnf == -1, t.full_like(fnf, INT64_MAX), fnf + s.z0 * ny * nx)
+        return t.cat([keys, -kmax, fnf])
+
+    def set_range(self, s: SlabState, k):
+        t = _lib.torch()
+        ctl = s.scratch["ctl"]
+        _ctl_field(ctl, "vmin_key", t.int32).copy_(k[0:1].to(t.int32))
+        _ctl_field(ctl, "vmax_key", t.int32).copy_((-k[1:2]).to(t.int32))
+        fnf = t.where(k[2:3] == INT64_MAX, t.full_like(k[2:3], -1), k[2:3])
+        _ctl_field(ctl, "first_nonfinite", t.int64).copy_(fnf)
+        s.scratch["range"] = k
+
+    def samples(self, s: SlabState):
+        t = _lib.torch()
+        lib = _lib.load()
+        if s.z1 <= s.z0:  # empty slab (more ranks than z tiles)
+            return t.zeros(_lib.SAMPLE_WORDS, dtype=t.int32, device="cuda")
+        v = t.empty(_lib.SAMPLE_WORDS, dtype=t.int32, device="cuda")
+        g = self.geom(s)
+        _lib.check(lib.cszi_sample_gather(_lib.ptr(s.x), ctypes.byref(g), _lib.ptr(v),
+                                          _lib.stream_ptr()), "sample_gather")
+        return v
+
+    def tune(self, s: SlabState, samples, alpha: float):
+        lib = _lib.load()
+        g = self.geom(s)
+        p = make_params(3, s.mode == "rel", s.eb, s.radius, alpha, 8)
+        _lib.check(lib.cszi_tune_from_samples(_lib.ptr(samples), ctypes.byref(g), ctypes.byref(p),
+                                              s.scratch["ctl"].ptr, _lib.stream_ptr()), "tune")
+
+    def predict(self, s: SlabState):
+        t = _lib.torch()
+        lib = _lib.load()
+        ny, nx = s.extents[1], s.extents[2]
+        n_own = (s.z1 - s.z0) * ny * nx
+        sym = t.empty(n_own + 16, dtype=t.int16, device="cuda")
+        hist = t.zeros(2 * s.radius, dtype=t.int64, device="cuda")
+        g = self.geom(s)
+        if n_own:
+            _lib.check(lib.cszi_predict(_lib.ptr(s.x), ctypes.byref(g), s.radius, 0, _lib.ptr(sym),
+                                        _lib.ptr(hist), s.scratch["ctl"].ptr, _lib.stream_ptr()),
+                       "predict")
+        s.scratch["sym"] = sym
+        s.scratch["n_own"] = n_own
+        return hist
+
+    def codebook(self, s: SlabState, hist):
+        t = _lib.torch()
+        lib = _lib.load()
+        nb = 2 * s.radius
+        lengths = t.zeros(nb, dtype=t.uint8, device="cuda")
+        words = t.zeros(nb, dtype=t.int32, device="cuda")
+        _lib.check(lib.cszi_codebook(_lib.ptr(hist), nb, _lib.ptr(lengths), _lib.ptr(words),
+                                     s.scratch["ctl"].ptr, _lib.stream_ptr()), "codebook")
+        s.scratch["lengths"] = lengths
+        s.scratch["words"] = words
+
+    def encode(self, s: SlabState):
+        t = _lib.torch()
+        lib = _lib.load()
+        n = s.scratch["n_own"]
+        ny, nx = s.extents[1], s.extents[2]
+        cap = ((4 * n + 64) + 15) & ~15
+        bits = t.zeros(cap + 16, dtype=t.uint8, device="cuda")
+        ocap = n + 16
+        oidx = t.empty(ocap, dtype=t.int64, device="cuda")
+        oval = t.empty(ocap, dtype=t.float32, device="cuda")
+        ws = _lib.WS.get(int(lib.cszi_encode_sym_workspace_size(max(n, 1))), "enc_slab")
+        ctl = s.scratch["ctl"]
+        if n:
+            _lib.check(lib.cszi_encode_sym(
+                _lib.ptr(s.scratch["sym"]), n, s.radius, _lib.ptr(s.scratch["lengths"]),
+                _lib.ptr(s.scratch["words"]), _lib.ptr(s.x), s.z0 * ny * nx, _lib.ptr(bits), cap,
+                _lib.ptr(oidx), _lib.ptr(oval), ocap, _lib.ptr(ws), ctl.ptr, _lib.stream_ptr()),
+                "encode")
+        s.scratch.update(bits=bits, oidx=oidx, oval=oval)
+        return t.cat([_ctl_field(ctl, "bits", t.int64), _ctl_field(ctl, "n_outliers", t.int64)])
+
+    def anchors(self, s: SlabState):
+        t = _lib.torch()
+        lib = _lib.load()
+        if s.z1 <= s.z0:
+            return t.empty(0, dtype=t.float32, device="cuda")
+        g = self.geom(s)
+        na = int(lib.cszi_slab_anchor_count(ctypes.byref(g)))
+        out = t.empty(max(na, 1), dtype=t.float32, device="cuda")
+        if na:
+            _lib.check(lib.cszi_gather_anchors(_lib.ptr(s.x), ctypes.byref(g), _lib.ptr(out),
+                                               _lib.stream_ptr()), "gather_anchors")
+        return out[:na]
+
+    def pieces(self, s: SlabState, counts):
+        """Variable-length payload pieces of this slab (device tensors)."""
+        nbits, nout = int(counts[0]), int(counts[1])
+        bits = s.scratch["bits"][: (nbits + 7) // 8]
+        return bits, s.scratch["oidx"][:nout], s.scratch["oval"][:nout]
+
+    def assemble(self, s0: SlabState, anchors, bit_pieces, nbits, oidx, oval, pass2: bool,
+                 alpha: float):
+        """Root: raw payload (anchors ‖ lengths ‖ bitstream ‖ outliers), pass-2,
+        header -> DeviceArchive."""
+        payload, sec = self._payload(s0, anchors, s0.scratch["lengths"], bit_pieces, nbits, oidx,
+                                     oval, pass2)
+        c = s0.scratch["ctl"].fetch()
+        if c.flags & _lib.F_EB_NONPOSITIVE:
+            raise Inconsistent("absolute error bound must be positive")
+        if c.flags & _lib.F_LENGTH_OVERFLOW:
+            raise LengthOverflow("a symbol would need more than 32 bits")
+        if c.flags & _lib.F_EMPTY_HISTOGRAM:
+            raise EmptyHistogram("cannot build a codebook from all-zero counts")
+        header = pack_header(3, PREDICTOR_INTERP, EB_REL if s0.mode == "rel" else EB_ABS, pass2,
+                             0, ctl_variants(c, 3), ctl_order(c, 3), s0.radius, 8, s0.extents,
+                             float(s0.eb), float(c.eb_abs), alpha, sec, int(payload.numel()))
+        return DeviceArchive(header=header, payload=payload)
+
+    def _payload(self, s0, anchors, lengths, bit_pieces, nbits, oidx, oval, pass2):
+        t = _lib.torch()
+        lib = _lib.load()
+        st = _lib.stream_ptr()
+        a = t.cat([x.reshape(-1) for x in anchors]).view(t.uint8)
+        total_bits = sum(nbits)
+        nbytes = (total_bits + 7) // 8
+        k = sum(int(x.numel()) for x in oidx)
+        head = a.numel() + lengths.numel()
+        raw_len = head + nbytes + 8 + 12 * k
+        raw = t.zeros(raw_len + 16, dtype=t.uint8, device="cuda")
+        raw[: a.numel()] = a
+        raw[a.numel(): head] = lengths
+        off = 0
+        for piece, nb in zip(bit_pieces, nbits):
+            if nb:
+                _lib.check(lib.cszi_concat_bits(_lib.ptr(raw[head:]), off, _lib.ptr(piece), nb, st),
+                           "concat_bits")
+            off += nb
+        idx = t.cat([x.reshape(-1) for x in oidx]) if k else t.zeros(1, dtype=t.int64, device="cuda")
+        val = t.cat([x.reshape(-1) for x in oval]) if k else t.zeros(1, dtype=t.float32, device="cuda")
+        _lib.check(lib.cszi_pack_outliers(_lib.ptr(idx), _lib.ptr(val), k,
+                                          _lib.ptr(raw[head + nbytes:]), st), "pack_outliers")
+        sec = (int(a.numel()), int(lengths.numel()), nbytes, 8 + 12 * k)
+        if pass2:
+            from .pass2 import encode_device
+
+            out, m = encode_device(raw, raw_len)
+            return out[:m], sec
+        return raw[:raw_len], sec
+
+
+# ---------------------------------------------------------------------------
+# orchestration
+# ---------------------------------------------------------------------------
+def compress_slabs(states: list, comm, backend=None, pass2: bool = True):
+    """Run the sharded compress over this process's slabs.  Returns the
+    archive (backend.assemble) on the root (the first slab's process), else
+    None."""
+    backend = backend or GpuSlabBackend()
+    s0 = states[0]
+    # (1) range
+    keys = [backend.range_keys(s) for s in states]
+    comm.allreduce(keys, "min")
+    for s, k in zip(states, keys):
+        backend.set_range(s, k)
+    k0 = keys[0].cpu().numpy().astype(np.int64)
+    if int(k0[2]) != INT64_MAX:
+        raise NonFiniteValue(int(k0[2]))
+    # alpha: rel mode -> compute_alpha(eb); abs mode -> from the global range
+    if s0.mode == "rel":
+        alpha = compute_alpha(float(s0.eb))
+    else:
+        from ._keys import key_to_float
+
+        rng = key_to_float(int(-k0[1])) - key_to_float(int(k0[0]))
+        alpha = compute_alpha(float(s0.eb) / rng if rng > 0 else float(s0.eb))
+    # (2) tuner samples
+    samp = [backend.samples(s) for s in states]
+    comm.allreduce(samp, "sum")
+    for s, v in zip(states, samp):
+        backend.tune(s, v, alpha)
+    # (3) histogram -> shared codebook
+    hists = [backend.predict(s) for s in states]
+    comm.allreduce(hists, "sum")
+    for s, h in zip(states, hists):
+        backend.codebook(s, h)
+    # (4) bit / outlier counts
+    counts = [backend.encode(s) for s in states]
+    allc = comm.allgather(counts)[0]
+    allc = [c.cpu().numpy() for c in allc]
+    # (5) gather pieces to the root
+    anchors = comm.gather([backend.anchors(s) for s in states])
+    pieces = [backend.pieces(s, c) for s, c in zip(states, [allc[i] for i in _local_ranks(comm, states)])]
+    bits = comm.gather([p[0] for p in pieces])
+    oidx = comm.gather([p[1] for p in pieces])
+    oval = comm.gather([p[2] for p in pieces])
+    if anchors is None:
+        return None
+    nbits = [int(c[0]) for c in allc]
+    return backend.assemble(s0, anchors, bits, nbits, oidx, oval, pass2, alpha)
+
+
+def _local_ranks(comm, states):
+    if isinstance(comm, SimComm):
+        return list(range(len(states)))
+    return [comm.rank]
+
+
+def compress_sharded(local_x, extents, z0: int, z1: int, eb: float, mode: str = "rel",
+                     pass2: bool = True, quant_radius: int = 512, group=None):
+    """torch.distributed entry point: this rank owns planes [z0, z1) of the
+    global 3-D field ``extents``; ``local_x`` holds planes [z0, min(z1+1, nz))."""
+    st = SlabState(x=local_x.contiguous(), extents=tuple(int(e) for e in extents), z0=z0, z1=z1,
+                   eb=float(eb), mode=mode, radius=int(quant_radius))
+    return compress_slabs([st], TorchComm(group), pass2=pass2)
+
+
+def compress_simulated(x, world: int, eb: float, mode: str = "rel", pass2: bool = True,
+                       quant_radius: int = 512):
+    """All ``world`` slabs of a 3-D CUDA field in this process (GPU-count
+    determinism check on one device)."""
+    nz = int(x.shape[0])
+    states = []
+    for z0, z1 in slab_bounds(nz, world):
+        states.append(SlabState(x=x[z0:min(z1 + 1, nz)].contiguous(), extents=tuple(x.shape),
+                                z0=z0, z1=z1, eb=float(eb), mode=mode, radius=int(quant_radius)))
+    return compress_slabs(states, SimComm(world), pass2=pass2)

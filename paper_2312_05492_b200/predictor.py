@@ -277,8 +277,9 @@ def _run_predict(grid: Grid, config: PredictorConfig, exact: bool = False):
     sym = t.empty(n + 16, dtype=t.int16, device="cuda")
     hist = t.empty(2 * config.quant_radius, dtype=t.int64, device="cuda")
     _lib.check(lib.cszi_ctl_init(ctl.ptr, st), "ctl_init")
-    _lib.check(lib.cszi_tune(_lib.ptr(x), ctypes.byref(geom), ctypes.byref(params), ctl.ptr, st),
-               "tune")
+    samples = t.empty(_lib.SAMPLE_WORDS, dtype=t.int32, device="cuda")
+    _lib.check(lib.cszi_tune(_lib.ptr(x), ctypes.byref(geom), ctypes.byref(params),
+                             _lib.ptr(samples), ctl.ptr, st), "tune")
     _lib.check(lib.cszi_predict(_lib.ptr(x), ctypes.byref(geom), config.quant_radius,
                                 1 if exact else 0, _lib.ptr(sym), _lib.ptr(hist), ctl.ptr, st),
                "predict")
