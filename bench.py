@@ -11,8 +11,11 @@ PSNR and the bound check ride along in the same JSON line.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 runs one process per GPU (torchrun); every rank compresses its own
-512^3 field (weak scaling) and the step time is the max over ranks.
+N > 1 runs one process per GPU (torchrun): one (512*N) x 512 x 512 field is
+sharded by z-slabs (512 planes per GPU, weak scaling) into ONE archive with
+NCCL collectives (range / sampler / histogram all-reduce, count all-gather,
+gather to rank 0); the step time is the max over ranks.  --sharded forces
+that path at N = 1 (a 1-rank process group).
 --impl reference times the reference algorithm's CPU implementation (the
 oracle port in oracle/, C + OpenMP on all host cores) on the same workload.
 """
@@ -38,13 +41,14 @@ METRIC = "compress/decompress GB/s at REL eb 1e-3 (1/2/4/8 B200, HBM %), CR & PS
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--shape", default="512,512,512")
     ap.add_argument("--eb", type=float, default=1e-3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sharded", action="store_true")
     return ap.parse_args()
 
 
@@ -66,7 +70,7 @@ def dist_init(n):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or "MASTER_ADDR" in os.environ:
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
@@ -77,18 +81,20 @@ def dist_init(n):
 
 
 def barrier(world):
-    if world > 1:
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized():
         import torch.distributed as dist
 
         dist.barrier()
 
 
 def max_over_ranks(v, world):
-    if world == 1:
-        return v
     import torch
     import torch.distributed as dist
 
+    if not (dist.is_available() and dist.is_initialized()):
+        return v
     t = torch.tensor([v], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -98,6 +104,9 @@ def max_over_ranks(v, world):
 # clocks during the timed region
 # ---------------------------------------------------------------------------
 class Clocks:
+    """nvidia-smi sampler (20 ms) started before the warm-up; only samples
+    whose host timestamp falls inside [mark_start, mark_stop] count."""
+
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
@@ -105,28 +114,51 @@ class Clocks:
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.lines = []
+        self.t0 = self.t1 = None
 
     def start(self):
+        import threading
+
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100", "-i", str(self.index)],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20", "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True, bufsize=1)
         except Exception:
             self.proc = None
+            return
+
+        def reader():
+            for line in self.proc.stdout:
+                self.lines.append((time.time(), line))
+
+        self.thread = threading.Thread(target=reader, daemon=True)
+        self.thread.start()
+        time.sleep(0.5)  # let nvidia-smi come up
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_stop(self):
+        self.t1 = time.time()
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
         self.proc.terminate()
         try:
-            out, _ = self.proc.communicate(timeout=5)
+            self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-            out = ""
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.splitlines():
+        t0 = self.t0 or 0.0
+        t1 = self.t1 or time.time()
+        for ts, line in self.lines:
+            if not (t0 - 0.05 <= ts <= t1 + 0.05):
+                continue
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 6:
                 continue
@@ -139,18 +171,21 @@ class Clocks:
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "window_s": round(t1 - t0, 3)}
 
 
 # ---------------------------------------------------------------------------
 # workload
 # ---------------------------------------------------------------------------
-def smooth_field_gpu(shape, phase=0.0):
-    """SURVEY.md §8d smooth field, float64 math on the device, cast to float32."""
+def smooth_field_gpu(shape, phase=0.0, zrange=None):
+    """SURVEY.md §8d smooth field, float64 math on the device, cast to float32.
+    ``zrange=(za, zb)`` generates only planes [za, zb) of the global field."""
     import torch
 
     nz, ny, nx = shape
-    z = torch.arange(nz, dtype=torch.float64, device="cuda").view(nz, 1, 1)
+    za, zb = zrange if zrange is not None else (0, nz)
+    z = torch.arange(za, zb, dtype=torch.float64, device="cuda").view(zb - za, 1, 1)
     y = torch.arange(ny, dtype=torch.float64, device="cuda").view(1, ny, 1)
     x = torch.arange(nx, dtype=torch.float64, device="cuda").view(1, 1, nx)
     two_pi = 2 * math.pi
@@ -206,6 +241,8 @@ def run_ours(args, rank, world, local):
         g = P.Grid(dims, x)
         return P.compress_device(g, eb)
 
+    clocks = Clocks(torch.cuda.current_device())
+    clocks.start()
     # warm-up (also the correctness probe of this run)
     for _ in range(max(args.warmup, 1)):
         arch = step_compress()
@@ -222,12 +259,11 @@ def run_ours(args, rank, world, local):
     bound_ok = max_err <= eb_abs
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clocks = Clocks(torch.cuda.current_device())
     # ---- compress (device-resident) ----
     launches0 = lib.cszi_launch_count()
     barrier(world)
     torch.cuda.synchronize()
-    clocks.start()
+    clocks.mark_start()
     ev0.record()
     for _ in range(args.steps):
         arch = step_compress()
@@ -244,6 +280,7 @@ def run_ours(args, rank, world, local):
         yg = P.decompress_device(arch)
     ev1.record()
     torch.cuda.synchronize()
+    clocks.mark_stop()
     barrier(world)
     clk = clocks.stop()
     d_ms = ev0.elapsed_time(ev1) / args.steps
@@ -382,6 +419,90 @@ def run_ours(args, rank, world, local):
     return result
 
 
+def run_sharded(args, rank, world, local):
+    """N > 1: one (512*N) x 512 x 512 field sharded by z-slabs (weak scaling:
+    512 planes per GPU), one archive; NCCL collectives inside the step."""
+    import torch
+
+    import paper_2312_05492_b200 as P
+    from paper_2312_05492_b200 import _lib
+    from paper_2312_05492_b200.distributed import compress_sharded, slab_bounds
+
+    per = tuple(int(s) for s in args.shape.split(","))
+    shape = (per[0] * world, per[1], per[2])
+    nz = shape[0]
+    z0, z1 = slab_bounds(nz, world)[rank]
+    x = smooth_field_gpu(shape, zrange=(z0, min(z1 + 1, nz)))
+    own_bytes = 4 * (z1 - z0) * shape[1] * shape[2]
+    total_bytes = 4 * nz * shape[1] * shape[2]
+    lib = _lib.load()
+    torch.cuda.synchronize()
+    clocks = Clocks(torch.cuda.current_device())
+    clocks.start()
+    for _ in range(max(args.warmup, 1)):
+        arch = compress_sharded(x, shape, z0, z1, args.eb)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = lib.cszi_launch_count()
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks.mark_start()
+    ev0.record()
+    for _ in range(args.steps):
+        arch = compress_sharded(x, shape, z0, z1, args.eb)
+    ev1.record()
+    torch.cuda.synchronize()
+    barrier(world)
+    launches = lib.cszi_launch_count() - launches0
+    c_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world)
+    # decompress: replicas (each rank decodes an archive of its own slab field)
+    own = x[: z1 - z0].contiguous()
+    local_arch = P.compress_device(P.Grid(P.Dims(tuple(own.shape)), own), args.eb)
+    for _ in range(max(args.warmup, 1)):
+        P.decompress_device(local_arch)
+    barrier(world)
+    torch.cuda.synchronize()
+    ev0.record()
+    for _ in range(args.steps):
+        P.decompress_device(local_arch)
+    ev1.record()
+    torch.cuda.synchronize()
+    clocks.mark_stop()
+    clk = clocks.stop()
+    d_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world)
+    res = {
+        "metric": METRIC,
+        "value": round(total_bytes / (c_ms * 1e-3) / 1e9, 3),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(c_ms, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {
+            "workload": f"{nz}x{shape[1]}x{shape[2]} float32 smooth field (SURVEY §8d) sharded "
+                        f"by z-slabs ({per[0]} planes per GPU), REL eb {args.eb:g}, one archive; "
+                        "NCCL: range/sample/histogram all-reduce, count all-gather, gather to "
+                        "rank 0 + pass-2",
+            "shape": list(shape), "eb": args.eb, "mode": "rel",
+            "parallelism": f"z-slab x{world}",
+            "l2": "per-GPU input 537 MB > 126 MB L2; no flush needed",
+        },
+        "decompress_gbs": round(world * own_bytes / (d_ms * 1e-3) / 1e9, 3),
+        "decompress_parallelism": "replicas (one slab archive per GPU)",
+        "archive_bytes": (len(arch) if arch is not None else None),
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if rank == 0 and arch is not None:
+        res["cr"] = round(total_bytes / len(arch), 4)
+    return res
+
+
 # ---------------------------------------------------------------------------
 # reference arm (the reference algorithm's CPU implementation: oracle port)
 # ---------------------------------------------------------------------------
@@ -451,12 +572,13 @@ def main():
             print(json.dumps(res), flush=True)
         return
     rank, world, local = dist_init(args.gpus)
-    res = run_ours(args, rank, world, local)
+    sharded = world > 1 or args.sharded
+    res = run_sharded(args, rank, world, local) if sharded else run_ours(args, rank, world, local)
     if rank == 0:
         print(json.dumps(res), flush=True)
-    if world > 1:
-        import torch.distributed as dist
+    import torch.distributed as dist
 
+    if dist.is_available() and dist.is_initialized():
         dist.destroy_process_group()
 
 

@@ -105,6 +105,16 @@ class Grid:
         self._ctl = ctl
 
     @classmethod
+    def wrap_host(cls, dims: Dims, arr) -> "Grid":
+        """Wrap a float32 array already checked finite by this library."""
+        g = cls.__new__(cls)
+        g.dims = dims
+        g._np = arr.reshape(dims.extents)
+        g._dev = None
+        g._ctl = None
+        return g
+
+    @classmethod
     def wrap_device(cls, dims: Dims, tensor) -> "Grid":
         """Wrap a CUDA float32 tensor produced by this library (no finite scan)."""
         g = cls.__new__(cls)

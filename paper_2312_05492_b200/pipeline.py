@@ -391,6 +391,22 @@ def decompress_device(data, threads: int = None) -> Grid:
 
 
 def decompress(data: bytes, threads: int = None) -> Grid:
-    """Decode archive bytes back to a grid (pipeline.py:166-204), on the GPU."""
+    """Decode archive bytes back to a grid (pipeline.py:166-204), on the GPU.
+
+    The reference wraps the result in Grid(), whose finite scan raises
+    NonFiniteValue for NaN/Inf outlier or anchor values of a crafted archive;
+    that scan runs on the device here before one pinned device->host copy."""
     g = decompress_device(data, threads)
-    return Grid(g.dims, g.tensor.cpu().numpy())
+    t = _lib.torch()
+    lib = _lib.load()
+    y = g.tensor.reshape(-1)
+    ctl = _lib.DeviceCtl()
+    st = _lib.stream_ptr()
+    _lib.check(lib.cszi_ctl_init(ctl.ptr, st), "ctl_init")
+    _lib.check(lib.cszi_range(_lib.ptr(y), y.numel(), ctl.ptr, st), "range")
+    host = t.empty(y.numel(), dtype=t.float32, pin_memory=True)
+    host.copy_(y, non_blocking=True)
+    c = ctl.fetch()  # synchronises the stream (covers the copy)
+    if c.first_nonfinite != 2**64 - 1:
+        raise NonFiniteValue(int(c.first_nonfinite))
+    return Grid.wrap_host(g.dims, host.numpy())
