@@ -29,6 +29,16 @@ DEV u64 ld_acquire(const u64 *p) {
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+// relaxed (no fence) variants for look-back status words: the 64-bit word
+// carries flag and value together, so no other data is ordered by it.
+DEV void st_relaxed(u64 *p, u64 v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+DEV u64 ld_relaxed(const u64 *p) {
+  u64 v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 DEV uint32_t ld_volatile_u32(const uint32_t *p) { return *(const volatile uint32_t *)p; }
 
 DEV uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
@@ -68,6 +78,16 @@ DEV T warp_incl_scan(T v) {
   return v;
 }
 template <typename T>
+DEV T warp_incl_max(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T t = __shfl_up_sync(CSZI_FULL, v, o);
+    if (lane >= o && t > v) v = t;
+  }
+  return v;
+}
+template <typename T>
 DEV T warp_sum(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(CSZI_FULL, v, o);
@@ -96,7 +116,9 @@ DEV T block_excl_scan(T v, T *ws, T &total) {
 }
 
 // ---------------------------------------------------------------------------
-// decoupled look-back (single-pass chained scan across tiles)
+// decoupled look-back (single-pass chained scan across tiles).  Status words
+// are published / polled with relaxed 64-bit accesses (flag and value in one
+// single-copy-atomic word; nothing else is ordered by them).
 // status word: [63:62] flag (0 invalid, 1 aggregate, 2 inclusive), [61:0] value
 // Must be called by all 32 lanes of ONE warp; tiles must be processed in
 // ticket order (tile t only waits on tiles < t, which started earlier).
@@ -105,29 +127,73 @@ constexpr u64 LB_AGG = 1ull << 62;
 constexpr u64 LB_INC = 2ull << 62;
 constexpr u64 LB_VAL = (1ull << 62) - 1;
 
+template <typename T>
+DEV T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const T t = __shfl_xor_sync(CSZI_FULL, v, o);
+    v = t > v ? t : v;
+  }
+  return v;
+}
+
+// MAX = false: prefix sums; MAX = true: prefix maxima (values < 2^62).
+// Each lane polls LB_PER_LANE consecutive predecessors per round trip.
+constexpr int LB_PER_LANE = 1;
+
+template <bool MAX = false>
 DEV u64 lookback_exclusive(u64 *status, u64 tile, u64 aggregate) {
   const int lane = threadIdx.x & 31;
   if (tile == 0) {
-    if (lane == 0) st_release(&status[0], LB_INC | aggregate);
+    if (lane == 0) st_relaxed(&status[0], LB_INC | aggregate);
     return 0;
   }
-  if (lane == 0) st_release(&status[tile], LB_AGG | aggregate);
+  if (lane == 0) st_relaxed(&status[tile], LB_AGG | aggregate);
   u64 excl = 0;
   long long top = (long long)tile - 1;
   for (;;) {
-    const long long idx = top - lane;
-    u64 s = (idx >= 0) ? ld_acquire(&status[idx]) : LB_INC;
-    const uint32_t inc_mask = __ballot_sync(CSZI_FULL, (s >> 62) == 2);
-    const int first_inc = inc_mask ? (__ffs(inc_mask) - 1) : 32;
-    const uint32_t inv_mask = __ballot_sync(CSZI_FULL, (s >> 62) == 0 && lane < first_inc);
+    u64 s[LB_PER_LANE];
+#pragma unroll
+    for (int k = 0; k < LB_PER_LANE; ++k) {
+      const long long idx = top - (lane * LB_PER_LANE + k);
+      s[k] = (idx >= 0) ? ld_relaxed(&status[idx]) : LB_INC;
+    }
+    // nearest inclusive prefix inside this lane's group, and whether an
+    // unpublished tile sits before it
+    int fk = LB_PER_LANE;
+    bool inv = false;
+    u64 v = 0;
+#pragma unroll
+    for (int k = LB_PER_LANE - 1; k >= 0; --k) {
+      const uint32_t f = (uint32_t)(s[k] >> 62);
+      if (f == 2) {
+        fk = k;
+        inv = false;
+        v = s[k] & LB_VAL;
+      } else {
+        inv = inv || f == 0;
+        const u64 x = s[k] & LB_VAL;
+        v = MAX ? (x > v ? x : v) : v + x;
+      }
+    }
+    // v now folds the group up to and including its first inclusive entry
+    // (entries after it were discarded when it was found)
+    const uint32_t inc_mask = __ballot_sync(CSZI_FULL, fk < LB_PER_LANE);
+    const int first_lane = inc_mask ? (__ffs(inc_mask) - 1) : 32;
+    const uint32_t inv_mask = __ballot_sync(CSZI_FULL, inv && lane <= first_lane);
     if (inv_mask) continue;  // a predecessor has not published yet: re-poll
-    u64 v = (lane <= first_inc) ? (s & LB_VAL) : 0;
-    v = warp_sum(v);
-    excl += v;
+    if (lane > first_lane) v = 0;
+    if (MAX) {
+      v = warp_max(v);
+      excl = v > excl ? v : excl;
+    } else {
+      excl += warp_sum(v);
+    }
     if (inc_mask) break;
-    top -= 32;
+    top -= 32 * LB_PER_LANE;
   }
-  if (lane == 0) st_release(&status[tile], LB_INC | (excl + aggregate));
+  const u64 inc = MAX ? (aggregate > excl ? aggregate : excl) : excl + aggregate;
+  if (lane == 0) st_relaxed(&status[tile], LB_INC | inc);
   return excl;
 }
 

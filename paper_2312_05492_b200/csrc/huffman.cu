@@ -270,257 +270,298 @@ __global__ void __launch_bounds__(CB_NT) k_canonical(const uint8_t *__restrict__
 }
 
 // ---------------------------------------------------------------------------
-// encode: one MSB-first stream; tile offsets by decoupled look-back
+// encode: one MSB-first stream (count -> scan -> pack), warp-granular
 // ---------------------------------------------------------------------------
-// Each persistent block owns a contiguous range of tiles (ENC_SPT symbols
-// per thread per tile).  Pass 1 sums the code lengths (and outliers) of the
-// whole range; ONE decoupled look-back across blocks gives the range its
-// global bit / outlier offsets.  Pass 2 re-reads the range tile by tile:
-// a block scan gives every thread its bit offset, codes are packed MSB-first
-// in a 64-bit register accumulator and written as whole 32-bit words to a
-// shared staging buffer (atomicOr only on the <= 2 words a thread shares
-// with its neighbours); the partial last word of a tile is carried into the
-// next tile.  The two words a range shares with its neighbour ranges are
-// merged by whichever block arrives second.
+// The unit of work is a warp chunk of ENC_CH = 1024 symbols (32 per lane), so
+// no phase needs a block barrier and the ~40 resident warps of an SM stream
+// independently (a block-tile look-back encoder was latency-bound: every
+// 16 KB tile waited a chain of L2 round trips for its offset):
+//   k_enc_count  per chunk: code-length and outlier totals,
+//   k_scan_pair  exclusive prefixes of both (decoupled look-back),
+//   k_enc_pack   per chunk: a warp scan gives each lane its bit offset,
+//                codes are packed MSB-first in a 64-bit register accumulator
+//                and ORed as whole 32-bit words into a per-warp shared
+//                buffer, funnel-shifted to the chunk's global bit offset and
+//                stored coalesced; the two words a chunk shares with its
+//                neighbours are merged with one 64-bit atomic (second arriver
+//                writes).  The next chunk's symbols load while one is packed.
+// Outliers (symbol 0 in MODE 0) are compacted in flat order on the way.
 constexpr int ENC_NT = 256;
+constexpr int ENC_NW = ENC_NT / 32;
 constexpr int ENC_SPT = 32;
-constexpr int ENC_TILE = ENC_NT * ENC_SPT;
+constexpr int ENC_CH = 32 * ENC_SPT;
+constexpr int ENC_SW = ENC_CH + 2;  // staged words per warp (max 32 bits per symbol)
 
-struct EncScratch {  // zeroed before each launch (except head/tail)
-  u64 *st_bits;
+struct EncScratch {
+  uint32_t *ch_bits;
+  uint32_t *ch_out;
+  u64 *bit_off;
+  u64 *out_off;
+  u64 *st_bits;  // look-back status of the pair scan
   u64 *st_out;
-  uint32_t *bflag;
-  uint32_t *bhead;
-  uint32_t *btail;
   uint32_t *ticket;
 };
 
-template <int MODE>
-DEV void enc_load(const void *src, u64 n, int R, int nbins, u64 base, uint32_t (&sy)[ENC_SPT]) {
-  if (MODE == 0) {
+
+// Symbols of one lane: MODE 0 keeps the uint16 pairs packed (16 regs),
+// MODE 1 (int32 codes of the fine-grained API) holds validated indices.
+// Positions past n read as the zero-length LUT entry `nbins`.
+template <int MODE> struct EncSyms;
+template <> struct EncSyms<0> {
+  uint32_t w[ENC_SPT / 2];
+  DEV uint32_t get(int j) const { return (j & 1) ? (w[j >> 1] >> 16) : (w[j >> 1] & 0xffffu); }
+  DEV void load(const void *src, u64 n, int, int nbins, u64 base, bool &) {
     const uint16_t *sp = reinterpret_cast<const uint16_t *>(src) + base;
     if (base + ENC_SPT <= n && (((uintptr_t)sp) & 15) == 0) {
 #pragma unroll
       for (int q = 0; q < ENC_SPT / 8; ++q) {
         const uint4 a = __ldcs(reinterpret_cast<const uint4 *>(sp) + q);
-        const uint32_t w4[4] = {a.x, a.y, a.z, a.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          sy[8 * q + 2 * j] = w4[j] & 0xffffu;
-          sy[8 * q + 2 * j + 1] = w4[j] >> 16;
-        }
+        w[4 * q] = a.x;
+        w[4 * q + 1] = a.y;
+        w[4 * q + 2] = a.z;
+        w[4 * q + 3] = a.w;
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < ENC_SPT; ++j) sy[j] = (base + j < n) ? sp[j] : 0xffffffffu;
+      for (int j = 0; j < ENC_SPT; j += 2) {
+        const uint32_t lo = (base + j < n) ? sp[j] : (uint32_t)nbins;
+        const uint32_t hi = (base + j + 1 < n) ? sp[j + 1] : (uint32_t)nbins;
+        w[j >> 1] = lo | (hi << 16);
+      }
     }
-  } else {
+  }
+};
+template <> struct EncSyms<1> {
+  uint32_t s[ENC_SPT];
+  DEV uint32_t get(int j) const { return s[j]; }
+  DEV void load(const void *src, u64 n, int R, int nbins, u64 base, bool &unknown) {
     const int32_t *cp = reinterpret_cast<const int32_t *>(src) + base;
 #pragma unroll
     for (int j = 0; j < ENC_SPT; ++j) {
       if (base + j < n) {
         const int64_t v = (int64_t)cp[j] + R;
-        sy[j] = (v >= 0 && v < nbins) ? (uint32_t)v : 0xfffffffeu;
+        const bool ok = v >= 0 && v < nbins;
+        unknown |= !ok;
+        s[j] = ok ? (uint32_t)v : (uint32_t)nbins;
       } else {
-        sy[j] = 0xffffffffu;
+        s[j] = (uint32_t)nbins;
       }
     }
   }
+};
+
+// LUT of (word, length) per symbol; MODE 0 codes the outlier sentinel 0 as
+// symbol R (huffman.py:60-74 counts outliers as code 0); [nbins] = (0, 0).
+template <int MODE>
+DEV void enc_load_lut(uint2 *lut, const uint8_t *lengths, const uint32_t *words, int R) {
+  const int nbins = 2 * R;
+  for (int i = threadIdx.x; i <= nbins; i += blockDim.x) {
+    const int sI = (MODE == 0 && i == 0) ? R : i;
+    lut[i] = (i == nbins) ? make_uint2(0u, 0u) : make_uint2(words[sI], lengths[sI]);
+  }
 }
 
-// classify + count: returns bits; marks invalid symbols 0xffffffff
 template <int MODE>
-DEV uint32_t enc_count(uint32_t (&sy)[ENC_SPT], const uint2 *lut, int R, uint32_t &nout,
-                       uint32_t &outmask, bool &unknown) {
+DEV uint32_t enc_bits(const EncSyms<MODE> &sy, const uint2 *lut, int nbins, bool &unknown,
+                      uint32_t &outmask) {
   uint32_t nbits = 0;
-  nout = 0;
   outmask = 0;
 #pragma unroll
   for (int j = 0; j < ENC_SPT; ++j) {
-    uint32_t s = sy[j];
-    if (s == 0xffffffffu) continue;
-    if (s == 0xfffffffeu) {
-      unknown = true;
-      sy[j] = 0xffffffffu;
-      continue;
-    }
-    if (MODE == 0 && s == 0) {
-      nout++;
-      outmask |= 1u << j;
-      s = (uint32_t)R;
-      sy[j] = s;
-    }
+    const uint32_t s = sy.get(j);
     const uint32_t l = lut[s].y;
-    if (l == 0) {
-      unknown = true;
-      sy[j] = 0xffffffffu;
-      continue;
-    }
+    unknown |= (l == 0) && (s != (uint32_t)nbins);
     nbits += l;
+    if (MODE == 0) outmask |= (uint32_t)(s == 0) << j;
   }
   return nbits;
 }
 
-// merge a word shared with the neighbouring range (second arriver writes)
-DEV void enc_boundary(uint32_t *out, u64 gw, uint32_t val, uint32_t *mine, uint32_t *other,
-                      uint32_t *flag) {
-  *mine = val;
-  __threadfence();
-  if (atomicAdd(flag, 1u) == 1u) {
-    __threadfence();
-    out[gw] = bswap32(val | ld_volatile_u32(other));
+// k_enc_count: lengths and outlier flags come from one u32 LUT entry
+// (length | outlier << 16) so a lane sums both with one add per symbol.
+template <int MODE>
+__global__ void __launch_bounds__(ENC_NT) k_enc_count(const void *__restrict__ src, u64 n, int R,
+                                                     const uint8_t *__restrict__ lengths,
+                                                     EncScratch S, u64 nch, cszi_ctl *ctl) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  uint32_t *lut = reinterpret_cast<uint32_t *>(sm_raw);
+  const int nbins = 2 * R;
+  const int lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i <= nbins; i += blockDim.x) {
+    const int sI = (MODE == 0 && i == 0) ? R : i;
+    lut[i] = (i == nbins) ? 0u : ((uint32_t)lengths[sI] | ((MODE == 0 && i == 0) ? 0x10000u : 0u));
+  }
+  __syncthreads();
+  bool unknown = false;
+  const u64 stride = (u64)gridDim.x * ENC_NW;
+  u64 c = (u64)blockIdx.x * ENC_NW + (threadIdx.x >> 5);
+  EncSyms<MODE> sy;
+  if (c < nch) sy.load(src, n, R, nbins, c * ENC_CH + (u64)lane * ENC_SPT, unknown);
+  while (c < nch) {
+    const u64 cn = c + stride;
+    EncSyms<MODE> nx;
+    if (cn < nch) nx.load(src, n, R, nbins, cn * ENC_CH + (u64)lane * ENC_SPT, unknown);
+    uint32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < ENC_SPT; ++j) {
+      const uint32_t e = lut[sy.get(j)];
+      // MODE 1: a symbol inside the code range without a codeword; MODE 0
+      // symbols come from the predictor whose histogram built the codebook
+      if (MODE == 1) unknown |= (e == 0) && (sy.get(j) != (uint32_t)nbins);
+      acc += e;
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      S.ch_bits[c] = acc & 0xffffu;
+      S.ch_out[c] = acc >> 16;
+    }
+    sy = nx;
+    c = cn;
+  }
+  if (unknown) atomicOr(&ctl->flags, (uint32_t)CSZI_F_UNKNOWN_SYMBOL);
+}
+
+// exclusive prefixes of (bits, outliers) per chunk; totals -> ctl
+constexpr int PS_NT = 256, PS_IPT = 8, PS_TILE = PS_NT * PS_IPT;
+__global__ void __launch_bounds__(PS_NT) k_scan_pair(EncScratch S, u64 nch, int mode,
+                                                    uint32_t *out, u64 cap_words, cszi_ctl *ctl) {
+  __shared__ u64 ws[PS_NT / 32 + 1];
+  __shared__ u64 s_t, s_pb, s_po;
+  if (threadIdx.x == 0) s_t = atomicAdd(S.ticket, 1u);
+  __syncthreads();
+  const u64 t = s_t;
+  const u64 base = t * PS_TILE + (u64)threadIdx.x * PS_IPT;
+  uint32_t vb[PS_IPT], vo[PS_IPT];
+  u64 sb = 0, so = 0;
+#pragma unroll
+  for (int i = 0; i < PS_IPT; ++i) {
+    vb[i] = (base + i < nch) ? S.ch_bits[base + i] : 0u;
+    vo[i] = (base + i < nch) ? S.ch_out[base + i] : 0u;
+    sb += vb[i];
+    so += vo[i];
+  }
+  u64 tb, to;
+  const u64 eb = block_excl_scan<PS_NT, u64>(sb, ws, tb);
+  const u64 eo = block_excl_scan<PS_NT, u64>(so, ws, to);
+  if (threadIdx.x < 32) {
+    const u64 p = lookback_exclusive(S.st_bits, t, tb);
+    if (threadIdx.x == 0) s_pb = p;
+  } else if (threadIdx.x < 64) {
+    const u64 p = lookback_exclusive(S.st_out, t, to);
+    if (threadIdx.x == 32) s_po = p;
+  }
+  __syncthreads();
+  u64 rb = s_pb + eb, ro = s_po + eo;
+#pragma unroll
+  for (int i = 0; i < PS_IPT; ++i) {
+    if (base + i < nch) {
+      S.bit_off[base + i] = rb;
+      S.out_off[base + i] = ro;
+      // a word holding an unaligned chunk boundary is ORed by both chunks
+      if ((rb & 31) && (rb >> 5) < cap_words) out[rb >> 5] = 0u;
+    }
+    rb += vb[i];
+    ro += vo[i];
+  }
+  if ((t + 1) * PS_TILE >= nch && threadIdx.x == 0) {
+    ctl->bits = s_pb + tb;
+    if (mode == 0) ctl->n_outliers = s_po + to;
   }
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(ENC_NT) k_encode(const void *__restrict__ src, u64 n, int R,
-                                                  const uint8_t *__restrict__ lengths,
-                                                  const uint32_t *__restrict__ words,
-                                                  uint32_t *__restrict__ out, u64 cap_words,
-                                                  const float *__restrict__ xval, u64 *o_idx,
-                                                  float *o_val, u64 o_cap, EncScratch S,
-                                                  u64 ntiles, u64 tiles_per_block, u64 nranges,
-                                                  u64 idx_offset, cszi_ctl *ctl) {
+__global__ void __launch_bounds__(ENC_NT, 3) k_enc_pack(const void *__restrict__ src, u64 n, int R,
+                                                       const uint8_t *__restrict__ lengths,
+                                                       const uint32_t *__restrict__ words,
+                                                       uint32_t *__restrict__ out, u64 cap_words,
+                                                       const float *__restrict__ xval, u64 *o_idx,
+                                                       float *o_val, u64 o_cap, EncScratch S,
+                                                       u64 nch, u64 idx_offset, cszi_ctl *ctl) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   const int nbins = 2 * R;
-  uint2 *lut = reinterpret_cast<uint2 *>(sm_raw);  // (word, length)
-  uint32_t *stage = reinterpret_cast<uint32_t *>(lut + nbins);  // ENC_TILE + 2 words
-  __shared__ uint32_t scan_ws32[ENC_NT / 32 + 1];
-  __shared__ u64 red_ws[ENC_NT / 32 + 1];
-  __shared__ u64 s_r, s_B, s_O;
-  const int tid = threadIdx.x;
-  for (int i = tid; i < nbins; i += ENC_NT) lut[i] = make_uint2(words[i], lengths[i]);
-  if (tid == 0) s_r = atomicAdd(S.ticket, 1u);  // ranges in ticket order
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint2 *lut = reinterpret_cast<uint2 *>(sm_raw);
+  uint32_t *stage = reinterpret_cast<uint32_t *>(lut + nbins + 2) + warp * ENC_SW;
+  enc_load_lut<MODE>(lut, lengths, words, R);
+  for (int i = lane; i < ENC_SW; i += 32) stage[i] = 0u;
   __syncthreads();
-  const u64 r = s_r;
-  if (r >= nranges) return;
-  const u64 t0 = r * tiles_per_block;
-  const u64 t1 = min(t0 + tiles_per_block, ntiles);
-  // ---- pass 1: range totals ----
-  u64 my_bits = 0, my_out = 0;
-  bool unknown = false;
-  for (u64 t = t0; t < t1; ++t) {
-    uint32_t sy[ENC_SPT];
-    enc_load<MODE>(src, n, R, nbins, t * ENC_TILE + (u64)tid * ENC_SPT, sy);
-    uint32_t nout, outmask;
-    my_bits += enc_count<MODE>(sy, lut, R, nout, outmask, unknown);
-    my_out += nout;
-  }
-  if (unknown) atomicOr(&ctl->flags, (uint32_t)CSZI_F_UNKNOWN_SYMBOL);
-  u64 range_bits, range_out;
-  block_excl_scan<ENC_NT, u64>(my_bits, red_ws, range_bits);
-  block_excl_scan<ENC_NT, u64>(my_out, red_ws, range_out);
-  if (tid < 32) {
-    const u64 B = lookback_exclusive(S.st_bits, r, range_bits);
-    const u64 O = (MODE == 0) ? lookback_exclusive(S.st_out, r, range_out) : 0;
-    if (tid == 0) {
-      s_B = B;
-      s_O = O;
+  bool unknown = false;  // reported by k_enc_count
+  bool cap_hit = false;
+  const u64 stride = (u64)gridDim.x * ENC_NW;
+  u64 c = (u64)blockIdx.x * ENC_NW + warp;
+  EncSyms<MODE> sy;
+  if (c < nch) sy.load(src, n, R, nbins, c * ENC_CH + (u64)lane * ENC_SPT, unknown);
+  while (c < nch) {
+    const u64 cn = c + stride;
+    EncSyms<MODE> nx;
+    if (cn < nch) nx.load(src, n, R, nbins, cn * ENC_CH + (u64)lane * ENC_SPT, unknown);
+    const u64 tb = S.bit_off[c];
+    const u64 ob = (MODE == 0) ? S.out_off[c] : 0;
+    uint32_t outmask;
+    const uint32_t nbits = enc_bits<MODE>(sy, lut, nbins, unknown, outmask);
+    const uint32_t incl = warp_incl_scan(nbits);
+    const uint32_t bexcl = incl - nbits;
+    const uint32_t tot_bits = __shfl_sync(CSZI_FULL, incl, 31);
+    {  // pack at chunk-relative bit offsets
+      uint32_t w = bexcl >> 5;
+      uint32_t nb = bexcl & 31;
+      u64 acc = 0;
+#pragma unroll
+      for (int j = 0; j < ENC_SPT; ++j) {
+        const uint2 e = lut[sy.get(j)];
+        acc = (acc << e.y) | (u64)e.x;
+        nb += e.y;
+        if (nb >= 32) {
+          nb -= 32;
+          atomicOr(&stage[w++], (uint32_t)(acc >> nb));
+        }
+      }
+      if (nb > 0) atomicOr(&stage[w], (uint32_t)(acc << (32 - nb)));
     }
-  }
-  __syncthreads();
-  const u64 RB = s_B, RO = s_O;  // range offsets
-  const bool last_range = (r + 1 == nranges);
-  // ---- pass 2: pack ----
-  u64 tb = RB;  // global bit offset of the current tile
-  u64 to = RO;
-  uint32_t carry = 0;  // partial last word carried from the previous tile
-  for (u64 t = t0; t < t1; ++t) {
-    const u64 base = t * ENC_TILE + (u64)tid * ENC_SPT;
-    uint32_t sy[ENC_SPT];
-    enc_load<MODE>(src, n, R, nbins, base, sy);
-    uint32_t nout, outmask;
-    bool unk2 = false;
-    const uint32_t nbits = enc_count<MODE>(sy, lut, R, nout, outmask, unk2);
-    uint32_t tot_bits, tot_out = 0;
-    const uint32_t bexcl = block_excl_scan<ENC_NT, uint32_t>(nbits, scan_ws32, tot_bits);
-    uint32_t oexcl = 0;
-    if (MODE == 0) oexcl = block_excl_scan<ENC_NT, uint32_t>(nout, scan_ws32, tot_out);
-    const uint32_t off0 = (uint32_t)(tb & 31);
-    const uint32_t nw = (off0 + tot_bits + 31) >> 5;
-    for (uint32_t i = tid; i < nw + 1; i += ENC_NT) stage[i] = (i == 0) ? carry : 0u;
-    __syncthreads();
-    if (MODE == 0 && outmask) {
-      u64 k = to + oexcl;
-      uint32_t m = outmask;
-      while (m) {
-        const int j = __ffs(m) - 1;
-        m &= m - 1;
-        const u64 gi = base + j;
+    if (MODE == 0 && __any_sync(CSZI_FULL, outmask != 0)) {
+      const uint32_t no = (uint32_t)__popc(outmask);
+      u64 k = ob + (warp_incl_scan(no) - no);
+      const u64 base = c * ENC_CH + (u64)lane * ENC_SPT;
+      for (uint32_t m = outmask; m; m &= m - 1) {
+        const u64 gi = base + (__ffs(m) - 1);
         if (k < o_cap) {
           o_idx[k] = gi + idx_offset;
           o_val[k] = xval[gi];
         } else {
-          atomicOr(&ctl->flags, (uint32_t)CSZI_F_CAPACITY);
+          cap_hit = true;
         }
         k++;
       }
     }
-    {
-      const uint32_t pos = off0 + bexcl;
-      uint32_t w = pos >> 5;
-      const uint32_t fill = pos & 31;
-      u64 acc = 0;
-      uint32_t nb = fill;
-      bool shared_head = fill != 0;
-#pragma unroll
-      for (int j = 0; j < ENC_SPT; ++j) {
-        const uint32_t s = sy[j];
-        if (s == 0xffffffffu) continue;
-        const uint2 e = lut[s];
-        acc = (acc << e.y) | (u64)e.x;
-        nb += e.y;
-        if (nb >= 32) {
-          const uint32_t v = (uint32_t)(acc >> (nb - 32));
-          if (shared_head) atomicOr(&stage[w], v);
-          else stage[w] = v;
-          shared_head = false;
-          ++w;
-          nb -= 32;
-          acc &= (nb ? ((1ull << nb) - 1) : 0ull);
-        }
-      }
-      if (nb > 0 && (nb > fill || !shared_head)) atomicOr(&stage[w], (uint32_t)(acc << (32 - nb)));
-    }
-    __syncthreads();
+    __syncwarp();
+    // write out: global word gw0 + i = stage bits shifted right by off0
+    const uint32_t off0 = (uint32_t)(tb & 31);
     const u64 gw0 = tb >> 5;
     const u64 end_bits = tb + tot_bits;
-    const bool tail_partial = (end_bits & 31) != 0;
-    const bool is_range_last_tile = (t + 1 == t1);
-    // words [0, nw): word 0 is the range head when t == t0 and unaligned;
-    // the last partial word is carried to the next tile, or is the range
-    // tail (merged with the next range) on the range's last tile.
-    for (uint32_t i = tid; i < nw; i += ENC_NT) {
+    const uint32_t nw = tot_bits ? (uint32_t)(((end_bits - 1) >> 5) - gw0 + 1) : 0;
+    const bool head_shared = off0 != 0 && c > 0;
+    const bool tail_shared = (end_bits & 31) != 0 && c + 1 < nch;
+    for (uint32_t i = lane; i < nw; i += 32) {
+      const uint32_t cur = stage[i];
+      const uint32_t prv = i ? stage[i - 1] : 0u;
+      const uint32_t val = off0 ? ((cur >> off0) | (prv << (32 - off0))) : cur;
       const u64 gw = gw0 + i;
-      const uint32_t val = stage[i];
-      const bool last_w = (i == nw - 1) && tail_partial;
-      if (last_w && !is_range_last_tile) continue;  // carried
       if (gw >= cap_words) {
-        atomicOr(&ctl->flags, (uint32_t)CSZI_F_CAPACITY);
+        cap_hit = true;
         continue;
       }
-      const bool head_w = (t == t0) && (i == 0) && (RB & 31) != 0;
-      if (head_w && last_w && !last_range) {
-        // the whole range fits inside one word shared on both sides: merge
-        // with the previous range first (as head) and the next (as tail)
-        enc_boundary(out, gw, val, &S.bhead[r], &S.btail[r], &S.bflag[r]);
-      } else if (head_w) {
-        enc_boundary(out, gw, val, &S.bhead[r], &S.btail[r], &S.bflag[r]);
-      } else if (last_w && !last_range) {
-        enc_boundary(out, gw, val, &S.btail[r + 1], &S.bhead[r + 1], &S.bflag[r + 1]);
-      } else {
+      if ((i == 0 && head_shared) || (i == nw - 1 && tail_shared))
+        atomicOr(out + gw, bswap32(val));
+      else
         out[gw] = bswap32(val);
-      }
     }
-    carry = (tail_partial && !is_range_last_tile) ? stage[nw - 1] : 0u;
-    tb = end_bits;
-    to += tot_out;
-    __syncthreads();
+    __syncwarp();
+    for (uint32_t i = lane; i <= nw; i += 32) stage[i] = 0u;
+    __syncwarp();
+    sy = nx;
+    c = cn;
   }
-  if (last_range && tid == 0) {
-    ctl->bits = RB + range_bits;
-    if (MODE == 0) ctl->n_outliers = RO + range_out;
-  }
+  if (cap_hit) atomicOr(&ctl->flags, (uint32_t)CSZI_F_CAPACITY);
 }
 
 // ---------------------------------------------------------------------------
@@ -954,8 +995,9 @@ int launch_pack_outliers(const u64 *idx, const float *val, u64 k, uint8_t *out,
 }
 
 u64 enc_scratch_bytes(u64 n) {
-  const u64 nt = (n + ENC_TILE - 1) / ENC_TILE + 2;
-  return nt * (8 + 8 + 4 + 4 + 4) + 64;
+  const u64 nc = (n + ENC_CH - 1) / ENC_CH + 2;
+  const u64 nt = (nc + PS_TILE - 1) / PS_TILE + 2;
+  return nc * (4 + 4 + 8 + 8) + nt * 16 + 64;
 }
 
 // mode 0: uint16 symbols with outlier sentinel; mode 1: int32 codes
@@ -964,39 +1006,43 @@ int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *length
                   u64 *o_idx, float *o_val, u64 o_cap, void *scratch, cszi_ctl *ctl,
                   cudaStream_t st, u64 idx_offset) {
   if (n == 0) return CSZI_OK;
-  const u64 ntiles = (n + ENC_TILE - 1) / ENC_TILE;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const u64 want = (u64)sms * 4;
-  const u64 tpb = (ntiles + want - 1) / want;
-  const u64 nranges = (ntiles + tpb - 1) / tpb;
-  const u64 nt = nranges + 2;
+  const u64 nch = (n + ENC_CH - 1) / ENC_CH;
+  const u64 nc = nch + 2;
+  const u64 npt = (nch + PS_TILE - 1) / PS_TILE;
+  const u64 nt = npt + 2;
   unsigned char *p = reinterpret_cast<unsigned char *>(scratch);
   EncScratch S;
-  S.st_bits = reinterpret_cast<u64 *>(p);
+  S.st_bits = reinterpret_cast<u64 *>(p);  // zeroed: st_bits, st_out, ticket
   S.st_out = S.st_bits + nt;
-  S.bflag = reinterpret_cast<uint32_t *>(S.st_out + nt);
-  S.ticket = S.bflag + nt;
-  S.bhead = S.ticket + 4;
-  S.btail = S.bhead + nt;
-  cudaMemsetAsync(p, 0, (size_t)(nt * 8 * 2 + nt * 4 + 16), st);
+  S.ticket = reinterpret_cast<uint32_t *>(S.st_out + nt);
+  S.bit_off = reinterpret_cast<u64 *>(S.ticket + 4);
+  S.out_off = S.bit_off + nc;
+  S.ch_bits = reinterpret_cast<uint32_t *>(S.out_off + nc);
+  S.ch_out = S.ch_bits + nc;
+  cudaMemsetAsync(p, 0, (size_t)(nt * 16 + 16), st);
   const int nbins = 2 * R;
-  const size_t smem = sizeof(uint2) * nbins + sizeof(uint32_t) * (ENC_TILE + 2) + 16;
-  if (mode == 0) {
-    cudaFuncSetAttribute(k_encode<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_encode<0><<<(unsigned)nranges, ENC_NT, smem, st>>>(src, n, R, lengths, words, out,
-                                                        cap_bytes / 4, xval, o_idx, o_val, o_cap,
-                                                        S, ntiles, tpb, nranges, idx_offset,
-                                                        ctl);
-  } else {
-    cudaFuncSetAttribute(k_encode<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_encode<1><<<(unsigned)nranges, ENC_NT, smem, st>>>(src, n, R, lengths, words, out,
-                                                        cap_bytes / 4, xval, o_idx, o_val, o_cap,
-                                                        S, ntiles, tpb, nranges, idx_offset,
-                                                        ctl);
-  }
-  note_launch();
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smem_c = sizeof(uint32_t) * (nbins + 2) + 16;
+  const size_t smem_p = sizeof(uint2) * (nbins + 2) + 16 + sizeof(uint32_t) * ENC_SW * ENC_NW;
+  auto kc = mode == 0 ? k_enc_count<0> : k_enc_count<1>;
+  auto kp = mode == 0 ? k_enc_pack<0> : k_enc_pack<1>;
+  cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c);
+  cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p);
+  const u64 wblocks = (nch + ENC_NW - 1) / ENC_NW;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kc, ENC_NT, smem_c);
+  u64 blocks = (u64)sms * (per_sm < 1 ? 1 : per_sm);
+  if (blocks > wblocks) blocks = wblocks;
+  kc<<<(unsigned)blocks, ENC_NT, smem_c, st>>>(src, n, R, lengths, S, nch, ctl);
+  k_scan_pair<<<(unsigned)npt, PS_NT, 0, st>>>(S, nch, mode, out, cap_bytes / 4, ctl);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, ENC_NT, smem_p);
+  blocks = (u64)sms * (per_sm < 1 ? 1 : per_sm);
+  if (blocks > wblocks) blocks = wblocks;
+  kp<<<(unsigned)blocks, ENC_NT, smem_p, st>>>(src, n, R, lengths, words, out, cap_bytes / 4,
+                                               xval, o_idx, o_val, o_cap, S, nch, idx_offset,
+                                               ctl);
+  note_launch(3);
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 

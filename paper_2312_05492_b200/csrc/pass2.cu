@@ -26,207 +26,337 @@ u64 chain_scratch_bytes(u64 M, int D);
 int launch_chain_resolve(const uint8_t *tab, u64 M, int D, int e0, uint8_t *entries,
                          void *scratch, cudaStream_t st);
 
+// Encoder (pass2.py:30-67) in three launches, warp-granular (a warp chunk is
+// P2_CH = 1024 bytes, 32 per lane) and bit-parallel (a lane classifies its
+// 32 bytes with a handful of 64-bit mask operations).  Every byte is RUN (a
+// zero with a zero neighbour) or LIT; a byte whose class differs from its
+// predecessor's starts a segment.  A byte's output depends on its distance j
+// from its segment start: LIT emits itself plus a control byte when
+// j % 128 == 0, RUN only the control at j % 128 == 0; a control's value needs
+// the distance to the segment end, capped at 128 (and at n).
+//   k_p2_summary  per chunk: last segment start, first segment start, class
+//                 of the carried-in segment, output bytes from the first
+//                 start on;
+//   k_p2_scan     max-scan of starts -> carried-in phase -> chunk output
+//                 sizes -> sum-scan (both by decoupled look-back);
+//   k_p2_emit     per chunk: output assembled in a per-warp shared buffer,
+//                 copied out coalesced (each output byte has one writer).
 constexpr int P2_NT = 256;
-constexpr int P2_BPT = 16;
-constexpr int P2_TILE = P2_NT * P2_BPT;
-constexpr u64 RUNBIT = 1ull << 63;
+constexpr int P2_NW = P2_NT / 32;
+constexpr int P2_BPL = 32;                 // bytes per lane
+constexpr int P2_CH = 32 * P2_BPL;         // bytes per warp chunk
+constexpr int P2_OB = P2_CH + P2_CH / 128 + 32;  // max output of one chunk
+constexpr uint32_t P2_NONE = 0xffffffffu;
 
 struct P2EncScratch {
-  u64 *st_seg;      // look-back status, byte tiles
-  u64 *st_out;      // look-back status, segment tiles
-  u64 *tile_base;   // segments starting before each byte tile
-  u64 *seg_start;   // start | RUNBIT
-  u64 *seg_out;     // output offset per segment
-  uint32_t *tickets;  // [0] byte tiles (pass a), [1] segment tiles, [2] emit
-  u64 *nseg;
+  u64 *last1;     // per chunk: last segment start + 1 (0: none)
+  uint32_t *fs;   // per chunk: first segment start (local), P2_NONE if none
+  uint32_t *rest; // per chunk: output bytes from the first start on
+  uint8_t *lit0;  // per chunk: class of its first byte (1: literal)
+  u64 *prev1;     // per chunk: last start before the chunk + 1
+  u64 *out_off;   // per chunk: output offset
+  u64 *st_max, *st_sum;  // look-back status of the scan tiles
+  uint32_t *ticket;
 };
 
-DEV uint8_t ldb(const uint8_t *in, int64_t i, u64 n) {
-  return (i >= 0 && (u64)i < n) ? __ldg(in + i) : (uint8_t)1;
+// 4-bit mask of the zero bytes of w
+DEV uint32_t zero_nibble(uint32_t w) {
+  const uint32_t t = __vcmpeq4(w, 0u);
+  return ((t & 0x08040201u) * 0x01010101u) >> 24;
 }
 
-// classification of 16 bytes [i0, i0+16) plus start flags
-DEV uint32_t classify(const uint8_t *in, u64 n, u64 i0, uint32_t &runmask) {
-  uint8_t b[P2_BPT + 4];
-#pragma unroll
-  for (int k = 0; k < P2_BPT + 4; ++k) b[k] = ldb(in, (int64_t)i0 + k - 2, n);
-  // z at local k (position i0+k-2), valid for k in [1, P2_BPT+2]
-  bool z[P2_BPT + 4];
-#pragma unroll
-  for (int k = 1; k < P2_BPT + 3; ++k) z[k] = b[k] == 0 && (b[k - 1] == 0 || b[k + 1] == 0);
-  uint32_t starts = 0;
-  runmask = 0;
-#pragma unroll
-  for (int k = 0; k < P2_BPT; ++k) {
-    const u64 i = i0 + k;
-    if (i >= n) break;
-    const bool zc = z[k + 2];
-    const bool zp = z[k + 1];
-    if (i == 0 || zc != zp) starts |= 1u << k;
-    if (zc) runmask |= 1u << k;
-  }
-  return starts;
-}
+struct P2Lane {
+  uint32_t w[8];   // the lane's 32 bytes (past n read as 1)
+  uint32_t zmask;  // RUN class per position
+  uint32_t smask;  // segment starts
+  uint32_t valid;  // positions < n
+  u64 p0;
+};
 
-__global__ void __launch_bounds__(P2_NT) k_p2_segments(const uint8_t *__restrict__ in,
-                                                       const u64 *Np, P2EncScratch S) {
-  __shared__ u64 ws[P2_NT / 32 + 1];
-  __shared__ u64 s_t, s_pre;
-  const u64 n = *Np;
-  const u64 ntiles = (n + P2_TILE - 1) / P2_TILE;
-  for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) s_t = atomicAdd(&S.tickets[0], 1u);
-    __syncthreads();
-    const u64 t = s_t;
-    if (t >= ntiles) break;
-    const u64 i0 = t * P2_TILE + (u64)threadIdx.x * P2_BPT;
-    uint32_t runmask;
-    const uint32_t starts = classify(in, n, i0, runmask);
-    u64 tot;
-    const u64 ex = block_excl_scan<P2_NT, u64>((u64)__popc(starts), ws, tot);
-    if (threadIdx.x < 32) {
-      const u64 p = lookback_exclusive(S.st_seg, t, tot);
-      if (threadIdx.x == 0) s_pre = p;
-    }
-    __syncthreads();
-    u64 g = s_pre + ex;
-    uint32_t m = starts;
-    while (m) {
-      const int k = __ffs(m) - 1;
-      m &= m - 1;
-      S.seg_start[g++] = (i0 + k) | (((runmask >> k) & 1u) ? RUNBIT : 0ull);
-    }
-    if (threadIdx.x == 0) {
-      S.tile_base[t] = s_pre;
-      if (t + 1 == ntiles) *S.nseg = s_pre + tot;
-    }
-  }
-}
-
-DEV u64 seg_size(u64 L, bool run) { return run ? (L + 127) / 128 : L + (L + 127) / 128; }
-
-__global__ void __launch_bounds__(P2_NT) k_p2_sizes(const u64 *Np, P2EncScratch S,
-                                                    cszi_ctl *ctl) {
-  __shared__ u64 ws[P2_NT / 32 + 1];
-  __shared__ u64 s_t, s_pre;
-  const u64 n = *Np;
-  const u64 nseg = (n == 0) ? 0 : *S.nseg;
-  const u64 ntiles = (nseg + P2_TILE - 1) / P2_TILE;
-  for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) s_t = atomicAdd(&S.tickets[1], 1u);
-    __syncthreads();
-    const u64 t = s_t;
-    if (t >= ntiles) break;
-    const u64 g0 = t * P2_TILE + (u64)threadIdx.x * P2_BPT;
-    u64 sz[P2_BPT];
-    u64 sum = 0;
+// Load and classify the 32 bytes of one lane of chunk c.
+DEV void p2_lane(const uint8_t *__restrict__ in, u64 n, u64 c, P2Lane &L) {
+  const int lane = threadIdx.x & 31;
+  const u64 p0 = c * P2_CH + (u64)lane * P2_BPL;
+  L.p0 = p0;
+  if (p0 + P2_BPL <= n && ((reinterpret_cast<uintptr_t>(in + p0) & 15) == 0)) {
+    const uint4 a = __ldcs(reinterpret_cast<const uint4 *>(in + p0));
+    const uint4 b = __ldcs(reinterpret_cast<const uint4 *>(in + p0) + 1);
+    L.w[0] = a.x; L.w[1] = a.y; L.w[2] = a.z; L.w[3] = a.w;
+    L.w[4] = b.x; L.w[5] = b.y; L.w[6] = b.z; L.w[7] = b.w;
+  } else {
 #pragma unroll
-    for (int k = 0; k < P2_BPT; ++k) {
-      const u64 g = g0 + k;
-      sz[k] = 0;
-      if (g < nseg) {
-        const u64 a = S.seg_start[g];
-        const u64 st = a & ~RUNBIT;
-        const u64 en = (g + 1 < nseg) ? (S.seg_start[g + 1] & ~RUNBIT) : n;
-        sz[k] = seg_size(en - st, (a & RUNBIT) != 0);
+    for (int q = 0; q < 8; ++q) {
+      uint32_t x = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const u64 i = p0 + 4 * q + k;
+        x |= (uint32_t)(i < n ? __ldg(in + i) : 1) << (8 * k);
       }
-      sum += sz[k];
+      L.w[q] = x;
     }
-    u64 tot;
-    const u64 ex = block_excl_scan<P2_NT, u64>(sum, ws, tot);
-    if (threadIdx.x < 32) {
-      const u64 p = lookback_exclusive(S.st_out, t, tot);
-      if (threadIdx.x == 0) s_pre = p;
-    }
-    __syncthreads();
-    u64 o = s_pre + ex;
-#pragma unroll
-    for (int k = 0; k < P2_BPT; ++k) {
-      if (g0 + k < nseg) S.seg_out[g0 + k] = o;
-      o += sz[k];
-    }
-    if (t + 1 == ntiles && threadIdx.x == 0) ctl->payload_len = s_pre + tot;
   }
+  uint32_t zb = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) zb |= zero_nibble(L.w[q]) << (4 * q);
+  // neighbours: 2 bytes before (previous lane), 1 after (next lane)
+  const uint32_t prevw = __shfl_up_sync(CSZI_FULL, L.w[7], 1);
+  const uint32_t nextw = __shfl_down_sync(CSZI_FULL, L.w[0], 1);
+  uint32_t zlo, zhi;
+  if (lane == 0) {
+    const uint32_t b2 = (p0 >= 2) ? __ldg(in + p0 - 2) : 1u;
+    const uint32_t b1 = (p0 >= 1) ? __ldg(in + p0 - 1) : 1u;
+    zlo = (b2 == 0 ? 1u : 0u) | (b1 == 0 ? 2u : 0u);
+  } else {
+    zlo = zero_nibble(prevw) >> 2;  // bytes 2, 3 of the previous lane
+  }
+  if (lane == 31) {
+    const u64 pn = p0 + P2_BPL;
+    zhi = (pn < n && __ldg(in + pn) == 0) ? 1u : 0u;
+  } else {
+    zhi = zero_nibble(nextw) & 1u;
+  }
+  // bit i <-> position p0 - 2 + i
+  const u64 Zb = (u64)zlo | ((u64)zb << 2) | ((u64)zhi << 34);
+  const u64 Z = Zb & ((Zb << 1) | (Zb >> 1));
+  const u64 S = Z ^ (Z << 1);
+  L.valid = (p0 >= n) ? 0u : (n - p0 >= 32 ? 0xffffffffu : ((1u << (n - p0)) - 1u));
+  L.zmask = (uint32_t)(Z >> 2) & L.valid;
+  L.smask = ((uint32_t)(S >> 2) | (p0 == 0 ? 1u : 0u)) & L.valid;
+}
+
+// heads and output bytes of a lane whose carried-in segment started at
+// cs (< p0); positions before `from` are excluded.
+DEV uint32_t p2_heads(const P2Lane &L, u64 cs) {
+  uint32_t heads = L.smask;
+  const uint32_t kh = (uint32_t)((128 - ((L.p0 - cs) & 127)) & 127);
+  const uint32_t fsl = L.smask ? (uint32_t)(__ffs(L.smask) - 1) : 32u;
+  if (kh < fsl) heads |= (1u << kh);  // kh < 32 here
+  return heads & L.valid;
+}
+
+__global__ void __launch_bounds__(P2_NT) k_p2_summary(const uint8_t *__restrict__ in,
+                                                      const u64 *Np, P2EncScratch S) {
+  const int lane = threadIdx.x & 31;
+  const u64 n = *Np;
+  const u64 nch = (n + P2_CH - 1) / P2_CH;
+  const u64 stride = (u64)gridDim.x * P2_NW;
+  for (u64 c = (u64)blockIdx.x * P2_NW + (threadIdx.x >> 5); c < nch; c += stride) {
+    P2Lane L;
+    p2_lane(in, n, c, L);
+    const u64 mylast = L.smask ? L.p0 + (31 - __clz(L.smask)) + 1 : 0;
+    u64 incl = warp_incl_max(mylast);
+    u64 cs1 = __shfl_up_sync(CSZI_FULL, incl, 1);
+    if (lane == 0) cs1 = 0;
+    const u64 last1 = __shfl_sync(CSZI_FULL, incl, 31);
+    const uint32_t myfirst = L.smask ? lane * P2_BPL + (__ffs(L.smask) - 1) : P2_NONE;
+    uint32_t fs = myfirst;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) fs = min(fs, __shfl_xor_sync(CSZI_FULL, fs, o));
+    uint32_t cnt;
+    const uint32_t lit = ~L.zmask & L.valid;
+    if (cs1) {
+      cnt = __popc(lit) + __popc(p2_heads(L, cs1 - 1));
+    } else if (L.smask) {
+      const uint32_t from = ~((1u << (__ffs(L.smask) - 1)) - 1u);
+      cnt = __popc(lit & from) + __popc(L.smask);
+    } else {
+      cnt = 0;
+    }
+    cnt = warp_sum(cnt);
+    if (lane == 0) {
+      S.last1[c] = last1;
+      S.fs[c] = fs;
+      S.rest[c] = cnt;
+      S.lit0[c] = (L.valid & ~L.zmask & 1u) ? 1 : 0;
+    }
+  }
+}
+
+constexpr int P2S_NT = 256, P2S_IPT = 8, P2S_TILE = P2S_NT * P2S_IPT;
+__global__ void __launch_bounds__(P2S_NT) k_p2_scan(const u64 *Np, P2EncScratch S,
+                                                    cszi_ctl *ctl) {
+  __shared__ u64 ws[P2S_NT / 32 + 1];
+  __shared__ u64 s_t, s_pmax, s_psum;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u64 n = *Np;
+  const u64 nch = (n + P2_CH - 1) / P2_CH;
+  const u64 ntiles = (nch + P2S_TILE - 1) / P2S_TILE;
+  if (threadIdx.x == 0) s_t = atomicAdd(S.ticket, 1u);
+  __syncthreads();
+  const u64 t = s_t;
+  if (t >= ntiles) {
+    if (t == 0 && threadIdx.x == 0) ctl->payload_len = 0;  // n == 0
+    return;
+  }
+  const u64 c0 = t * P2S_TILE + (u64)threadIdx.x * P2S_IPT;
+  // max-scan of last1 (inclusive within the thread's items)
+  u64 lm = 0;
+#pragma unroll
+  for (int i = 0; i < P2S_IPT; ++i)
+    if (c0 + i < nch) lm = max(lm, S.last1[c0 + i]);
+  u64 incl = warp_incl_max(lm);
+  if (lane == 31) ws[warp] = incl;
+  __syncthreads();
+  u64 tile_max = 0, wpre = 0;
+#pragma unroll
+  for (int w = 0; w < P2S_NT / 32; ++w) {
+    if (w < warp) wpre = max(wpre, ws[w]);
+    tile_max = max(tile_max, ws[w]);
+  }
+  u64 ex = __shfl_up_sync(CSZI_FULL, incl, 1);
+  if (lane == 0) ex = 0;
+  ex = max(ex, wpre);
+  if (warp == 0) {
+    const u64 pm = lookback_exclusive<true>(S.st_max, t, tile_max);
+    if (lane == 0) s_pmax = pm;
+  }
+  __syncthreads();
+  u64 run = max(ex, s_pmax);  // last start + 1 before item c0
+  u64 cnt[P2S_IPT];
+  u64 sum = 0;
+#pragma unroll
+  for (int i = 0; i < P2S_IPT; ++i) {
+    const u64 c = c0 + i;
+    cnt[i] = 0;
+    if (c < nch) {
+      const uint32_t fs = S.fs[c];
+      const u64 len = min((u64)P2_CH, n - c * P2_CH);
+      const u64 l0 = (fs == P2_NONE) ? len : fs;
+      u64 k = S.rest[c];
+      if (l0 > 0) {  // run >= 1: position 0 starts a segment
+        const u64 d = c * P2_CH - (run - 1);
+        k += (S.lit0[c] ? l0 : 0) + ((d + l0 - 1) / 128 - (d - 1) / 128);
+      }
+      S.prev1[c] = run;
+      run = max(run, S.last1[c]);
+      cnt[i] = k;
+      sum += k;
+    }
+  }
+  __syncthreads();
+  u64 tot;
+  const u64 so = block_excl_scan<P2S_NT, u64>(sum, ws, tot);
+  if (warp == 0) {
+    const u64 ps = lookback_exclusive<false>(S.st_sum, t, tot);
+    if (lane == 0) s_psum = ps;
+  }
+  __syncthreads();
+  u64 o = s_psum + so;
+#pragma unroll
+  for (int i = 0; i < P2S_IPT; ++i) {
+    if (c0 + i < nch) S.out_off[c0 + i] = o;
+    o += cnt[i];
+  }
+  if (t + 1 == ntiles && threadIdx.x == 0) ctl->payload_len = s_psum + tot;
 }
 
 __global__ void __launch_bounds__(P2_NT) k_p2_emit(const uint8_t *__restrict__ in, const u64 *Np,
                                                    P2EncScratch S, uint8_t *__restrict__ out) {
-  __shared__ u64 ws[P2_NT / 32 + 1];
+  __shared__ uint8_t obuf[P2_NW][P2_OB];
+  __shared__ uint32_t ibuf[P2_NW][P2_CH / 4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint8_t *ob = obuf[warp];
+  uint32_t *iw = ibuf[warp] + lane * (P2_BPL / 4);
+  const uint8_t *ib = reinterpret_cast<const uint8_t *>(iw);
   const u64 n = *Np;
-  const u64 nseg = (n == 0) ? 0 : *S.nseg;
-  const u64 ntiles = (n + P2_TILE - 1) / P2_TILE;
-  for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const u64 i0 = t * P2_TILE + (u64)threadIdx.x * P2_BPT;
-    uint32_t runmask;
-    const uint32_t starts = classify(in, n, i0, runmask);
-    u64 tot;
-    const u64 ex = block_excl_scan<P2_NT, u64>((u64)__popc(starts), ws, tot);
-    long long g = (long long)(S.tile_base[t] + ex) - 1;  // segment of byte i0-1
-    u64 sst = 0, len = 0, O = 0;
-    bool run = false;
-    long long cur = -2;
-#pragma unroll 1
-    for (int k = 0; k < P2_BPT; ++k) {
-      const u64 i = i0 + k;
-      if (i >= n) break;
-      if ((starts >> k) & 1u) g++;
-      if (g != cur) {
-        cur = g;
-        const u64 a = S.seg_start[g];
-        sst = a & ~RUNBIT;
-        run = (a & RUNBIT) != 0;
-        const u64 en = ((u64)g + 1 < nseg) ? (S.seg_start[g + 1] & ~RUNBIT) : n;
-        len = en - sst;
-        O = S.seg_out[g];
-      }
-      const u64 j = i - sst;
-      const u64 jm = j & 127;
-      if (run) {
-        if (jm == 0) out[O + j / 128] = (uint8_t)(127 + min((u64)128, len - j));
+  const u64 nch = (n + P2_CH - 1) / P2_CH;
+  const u64 stride = (u64)gridDim.x * P2_NW;
+  for (u64 c = (u64)blockIdx.x * P2_NW + warp; c < nch; c += stride) {
+    const u64 prev1 = S.prev1[c];
+    const u64 O = S.out_off[c];
+    const uint32_t fsn = (c + 1 < nch) ? S.fs[c + 1] : P2_NONE;
+    P2Lane L;
+    p2_lane(in, n, c, L);
+    const u64 mylast = L.smask ? L.p0 + (31 - __clz(L.smask)) + 1 : 0;
+    u64 incl = warp_incl_max(mylast);
+    u64 cs1 = __shfl_up_sync(CSZI_FULL, incl, 1);
+    if (lane == 0) cs1 = 0;
+    cs1 = max(cs1, prev1);  // >= 1
+    const uint32_t heads = p2_heads(L, cs1 - 1);
+    const uint32_t lit = ~L.zmask & L.valid;
+#pragma unroll
+    for (int q = 0; q < P2_BPL / 4; ++q) iw[q] = L.w[q];
+    const uint32_t cnt = __popc(lit) + __popc(heads);
+    const uint32_t incl_cnt = warp_incl_scan(cnt);
+    const uint32_t tot = __shfl_sync(CSZI_FULL, incl_cnt, 31);
+    uint32_t o = incl_cnt - cnt;
+    // first start after this lane: suffix minimum over later lanes, then the
+    // next chunk's first start
+    u64 nxt = L.smask ? L.p0 + (__ffs(L.smask) - 1) : ~0ull;
+    if (lane == 31) {
+      const u64 fn = (fsn == P2_NONE) ? ~0ull : (c + 1) * P2_CH + fsn;
+      nxt = min(nxt, fn);
+    }
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const u64 x = __shfl_down_sync(CSZI_FULL, nxt, d);
+      if (lane + d < 32) nxt = min(nxt, x);
+    }
+    u64 after = __shfl_down_sync(CSZI_FULL, nxt, 1);
+    if (lane == 31) after = (fsn == P2_NONE) ? ~0ull : (c + 1) * P2_CH + fsn;
+    for (uint32_t m = lit | heads; m; m &= m - 1) {
+      const int k = __ffs(m) - 1;
+      const u64 p = L.p0 + k;
+      const uint32_t byte = ib[k];
+      const bool z = (L.zmask >> k) & 1u;
+      if ((heads >> k) & 1u) {
+        const uint32_t later = L.smask & ~((2u << k) - 1u);  // k = 31: (2u << 31) == 0
+        const u64 ns = later ? L.p0 + (__ffs(later) - 1) : after;
+        u64 len = min((u64)128, n - p);
+        if (ns != ~0ull) len = min(len, ns - p);
+        if (z) {
+          ob[o++] = (uint8_t)(127 + len);
+        } else {
+          ob[o++] = (uint8_t)(len - 1);
+          ob[o++] = (uint8_t)byte;
+        }
       } else {
-        const u64 c = j / 128;
-        out[O + c * 129 + 1 + jm] = __ldg(in + i);
-        if (jm == 0) out[O + c * 129] = (uint8_t)(min((u64)128, len - j) - 1);
+        ob[o++] = (uint8_t)byte;
       }
     }
-    __syncthreads();
+    __syncwarp();
+    for (uint32_t i = lane; i < tot; i += 32) out[O + i] = ob[i];
+    __syncwarp();
   }
 }
 
 u64 p2enc_scratch_bytes(u64 n) {
-  const u64 nt = (n + P2_TILE - 1) / P2_TILE + 2;
-  return nt * 8 * 3 + (n + 2) * 8 * 2 + nt * 8 + 256;
+  const u64 nc = (n + P2_CH - 1) / P2_CH + 2;
+  const u64 nt = (nc + P2S_TILE - 1) / P2S_TILE + 2;
+  return nc * (8 + 4 + 4 + 1 + 8 + 8) + nt * 16 + 256;
 }
 
 // in: device bytes; Np: device pointer to the byte count (<= cap_n)
 int launch_pass2_encode(const uint8_t *in, const u64 *Np, u64 cap_n, uint8_t *out,
                         void *scratch, cszi_ctl *ctl, cudaStream_t st) {
-  const u64 nt = (cap_n + P2_TILE - 1) / P2_TILE + 2;
+  const u64 nc = (cap_n + P2_CH - 1) / P2_CH + 2;
+  const u64 ntm = (nc + P2S_TILE - 1) / P2S_TILE;
+  const u64 nt = ntm + 2;
   unsigned char *p = reinterpret_cast<unsigned char *>(scratch);
   P2EncScratch S;
-  S.st_seg = reinterpret_cast<u64 *>(p);
-  S.st_out = S.st_seg + nt;
-  S.tickets = reinterpret_cast<uint32_t *>(S.st_out + nt);
-  S.nseg = reinterpret_cast<u64 *>(S.tickets + 4);
-  S.tile_base = S.nseg + 2;
-  S.seg_start = S.tile_base + nt;
-  S.seg_out = S.seg_start + cap_n + 2;
-  cudaMemsetAsync(p, 0, (size_t)(nt * 16 + 16 + 16), st);
-  int dev = 0, sms = 148;
+  S.st_max = reinterpret_cast<u64 *>(p);  // zeroed: st_max, st_sum, ticket
+  S.st_sum = S.st_max + nt;
+  S.ticket = reinterpret_cast<uint32_t *>(S.st_sum + nt);
+  S.last1 = reinterpret_cast<u64 *>(S.ticket + 4);
+  S.prev1 = S.last1 + nc;
+  S.out_off = S.prev1 + nc;
+  S.fs = reinterpret_cast<uint32_t *>(S.out_off + nc);
+  S.rest = S.fs + nc;
+  S.lit0 = reinterpret_cast<uint8_t *>(S.rest + nc);
+  cudaMemsetAsync(p, 0, (size_t)(nt * 16 + 16), st);
+  int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  u64 grid = (u64)sms * 4;
-  const u64 tiles_max = (cap_n + P2_TILE - 1) / P2_TILE;
-  if (grid > tiles_max) grid = tiles_max;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_p2_emit, P2_NT, 0);
+  if (per_sm < 1) per_sm = 1;
+  u64 grid = (u64)sms * per_sm;
+  const u64 wb = (nc + P2_NW - 1) / P2_NW;
+  if (grid > wb) grid = wb;
   if (grid < 1) grid = 1;
-  k_p2_segments<<<(unsigned)grid, P2_NT, 0, st>>>(in, Np, S);
-  note_launch();
-  k_p2_sizes<<<(unsigned)grid, P2_NT, 0, st>>>(Np, S, ctl);
-  note_launch();
+  k_p2_summary<<<(unsigned)grid, P2_NT, 0, st>>>(in, Np, S);
+  k_p2_scan<<<(unsigned)(ntm < 1 ? 1 : ntm), P2S_NT, 0, st>>>(Np, S, ctl);
   k_p2_emit<<<(unsigned)grid, P2_NT, 0, st>>>(in, Np, S, out);
-  note_launch();
+  note_launch(3);
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 

@@ -35,6 +35,27 @@ def test_pass2_known_answers_and_random():
             assert P.pass2_decode(enc) == data
 
 
+def test_pass2_runs_across_tiles():
+    """Zero runs / literal stretches of random lengths straddling the 4 KiB
+    encoder tiles and the 128-byte chunk limit, vs the oracle."""
+    rng = np.random.default_rng(11)
+    for mean_run, mean_lit in ((3, 2), (150, 40), (700, 300), (5000, 129)):
+        parts = []
+        total = 0
+        while total < 60000:
+            r = int(rng.geometric(1.0 / mean_run))
+            lit = rng.integers(1, 256, int(rng.geometric(1.0 / mean_lit))).astype(np.uint8)
+            lit[rng.random(lit.size) < 0.1] = 0  # isolated zeros stay literal
+            parts += [np.zeros(r, np.uint8), lit]
+            total += r + lit.size
+        data = np.concatenate(parts).tobytes()
+        for cut in (len(data), 4096 * 3 + 1, 4096 * 2, 4095, 128 * 7 + 2):
+            d = data[:cut]
+            enc = P.pass2_encode(d)
+            assert enc == O.pass2_encode(d), (mean_run, mean_lit, cut)
+            assert P.pass2_decode(enc) == d
+
+
 def test_pass2_registry():
     P.register_pass2_codec(9, lambda d: bytes(b ^ 0x55 for b in d),
                            lambda d: bytes(b ^ 0x55 for b in d))
