@@ -689,6 +689,10 @@ uint64_t slab_anchor_count(const cszi_geom *g) {
   return (uint64_t)c;
 }
 
+}  // namespace cszi
+#include "tile3.cuh"
+namespace cszi {
+
 // ---------------------------------------------------------------------------
 // host-side launchers
 // ---------------------------------------------------------------------------
@@ -831,6 +835,8 @@ static int launch_recon_fast(const uint16_t *sym, const float *anchors, const u6
 
 int launch_predict(const float *x, const cszi_geom *g, int32_t radius, const cszi_ctl *ctl,
                    uint16_t *sym, u64 *hist, bool exact, cudaStream_t st) {
+  if (g->rank == 3 && layout_is<fast::L3>(g) && !getenv("CSZI_OLD_PREDICT"))
+    return t3::launch_predict_t3(x, g, radius, ctl, sym, hist, exact, st);
   if (g->rank == 3 && layout_is<fast::L3>(g))
     return launch_predict_fast<fast::L3, 128>(x, g, radius, ctl, sym, hist, exact, st);
   if (g->rank == 2 && layout_is<fast::L2>(g))
@@ -857,6 +863,8 @@ int launch_reconstruct(const uint16_t *sym, const float *anchors, const u64 *oid
     lc.order[a] = order[a];
     lc.variant[a] = variant[a];
   }
+  if (g->rank == 3 && layout_is<fast::L3>(g) && nlev == 3 && !getenv("CSZI_OLD_PREDICT"))
+    return t3::launch_recon_t3(sym, anchors, oidx, oval, nout, nout_dev, g, radius, lc, y, st);
   if (g->rank == 3 && layout_is<fast::L3>(g))
     return launch_recon_fast<fast::L3, 128>(sym, anchors, oidx, oval, nout, nout_dev, g, radius,
                                             lc, y, st);

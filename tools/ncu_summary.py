@@ -24,6 +24,20 @@ if len(rr) > 2:
                 "smsp__inst_executed_pipe_xu.sum"):
         if key in hh:
             print(f"{key:40s} {vv[hh.index(key)]} {rr[1][hh.index(key)]}")
+    # warp stall breakdown (cycles per issued instruction, by reason)
+    st = []
+    for i, k in enumerate(hh):
+        if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
+            try:
+                st.append((float(vv[i]), k[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]))
+            except ValueError:
+                pass
+    if st:
+        print("stalls/issue: " + ", ".join(f"{n} {v:.2f}" for v, n in sorted(st, reverse=True)[:10]))
+    for key in ("smsp__inst_executed.sum", "sm__inst_executed_pipe_fp64.sum", "smsp__inst_executed_op_shared_ld.sum",
+                "smsp__inst_executed_op_shared_st.sum", "sm__sass_inst_executed_op_shared_ld.sum"):
+        if key in hh:
+            print(f"{key:40s} {vv[hh.index(key)]}")
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 agg = collections.Counter(); stall = collections.Counter(); txt = {}
