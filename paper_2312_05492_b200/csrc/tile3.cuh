@@ -70,6 +70,7 @@ struct Geo {
   int nzl;           // planes held by the input buffer (slab incl. halo)
   int z0;            // global z of local plane 0
   int nt[3];         // tiles per axis (axis 0 over the owned planes)
+  int ni[3];         // interior tiles per axis (closing plane inside the grid)
   int R;
   int hist_smem;
   int tma;           // 1: tensor map valid
@@ -226,28 +227,37 @@ __device__ __noinline__ QS fix_point(uint32_t a, uint32_t st, int cs, double wo,
 }
 
 // Fast quantiser; returns false when undecided (then call quant_slow).
-//  * t' = r * RN(1/e2) lies within 3 ulp of RN(r / e2); unless t' is within
-//    2^-20 of a half-integer, rint(t') == trunc(t + copysign(.5, t)).
+//  * t' = r * RN(1/e2) lies within 3 ulp (< 2^-36 for |t| < 2^13) of
+//    RN(r / e2).  m = RN(t' + 1.5 * 2^34) has ulp 2^-18, so for |t'| < 2^13
+//    the low word of m is F = round(t' * 2^18) as an int32 (the high word
+//    tells whether t' was in range; outside it |q| >= 2^13 >= R: outlier).
+//    Unless t' * 2^18 lies within 1.5 units of a half-integer boundary,
+//    rint(t) == (F + 2^17) >> 18 == trunc(t + copysign(.5, t)).
 //  * y = RN(pred + RN(e2 q)); rec = RN32(y).  |rec - y| <= 2^-24 |y| +
 //    2^-150, so |dy| <= leb (1 - 2^-40) - 2^-23 |y| - 2^-148 with
 //    dy = RN(y - o) implies RN(f64(rec) - o) <= leb: the guard is false.
 //    (lebs is capped at 2^100 so that such a y never overflows float32.)
 // big (|q| >= R) points are outliers whatever the guard says.
-DEV bool quant_fast(double pred, float o32, const Lv &L, double Rd, int R, float &recon,
-                    uint32_t &sym) {
+constexpr double MAGIC34 = 25769803776.0;  // 1.5 * 2^34
+DEV bool quant_fast(double pred, float o32, const Lv &L, int R, float &recon, uint32_t &sym) {
   const double o = (double)o32;
   const double r = dsub(o, pred);
   const double t = dmul(r, L.inv);
-  const double m = dadd(t, MAGIC);
-  const double rq = dsub(m, MAGIC);
-  const bool near_ok = fabs(dsub(t, rq)) <= 0.49999904632568359375;
-  const bool big = fabs(rq) >= Rd;
-  const double y = dadd(pred, dmul(L.e2, rq));
+  const double m = dadd(t, MAGIC34);
+  const int F = __double2loint(m);
+  const int hi = __double2hiint(m);
+  const bool in_range = (hi + (int)((uint32_t)F >> 31)) == 0x42180000;
+  const int u = F + 0x20000;
+  const int q = u >> 18;
+  const bool near_ok = ((u + 2) & 0x3FFFF) >= 4;
+  const bool big = !in_range || q >= R || q <= -R;
+  const double qd = dsub(__hiloint2double(0x43300000, q ^ (int)0x80000000), 4503601774854144.0);
+  const double y = dadd(pred, dmul(L.e2, qd));
   const double dy = dsub(y, o);
   const bool safe = fabs(dy) <= __fma_rn(fabs(y), -0x1p-23, L.lebs);
   recon = big ? o32 : __double2float_rn(y);
-  sym = big ? 0u : (uint32_t)(__double2loint(m) + R);
-  return near_ok && (big || safe);
+  sym = big ? 0u : (uint32_t)(q + R);
+  return big ? (!in_range || near_ok) : (near_ok && safe);
 }
 
 struct Out {  // decompress outlier list
@@ -325,9 +335,9 @@ DEV double chain4(double w0, double w1, double w2, double w3, double a, double b
 
 // interior lines: compile-time case pattern; edge tiles: case from the true
 // extent (warp-uniform), weights from c_w.  cs < 0: interior.
-template <int NP>
+template <int NP, bool BND>
 DEV double pred_k(int k, int cs, double wo, double wi, double a, double b, double c, double d) {
-  if (cs < 0) {
+  if (!BND) {
     if (NP == 1) return p_lin(b, c);
     if (k == 0) return p_p3(b, c, d);
     if (k == NP - 1) return p_m3(a, b, c);
@@ -341,11 +351,10 @@ DEV bool anchor_coord(int c, int e) { return (c & 7) == 0 || c == e - 1; }
 
 // D = x: lane walks rows (z, y) of the pass lattice.  S = 1, 2: 8 quads +
 // x = 32 in 16-byte accesses; S = 4: 9 scalars.
-template <int S, int MODE>
+template <int S, int MODE, bool BND>
 DEV void walk_x(const Tile &T, int stz, int sty, double wo, double wi, const Lv &L, int R,
                 bool exact, const Out &O) {
   const int lane = threadIdx.x & 31;
-  const bool BND = T.bnd;
   const int ez = BND ? min(CZ, T.e[0]) : CZ, ey = BND ? min(CY, T.e[1]) : CY;
   const int ex = BND ? min(CX, T.e[2]) : CX;
   const int cz = (ez - 1) / stz + 1, cy = (ey - 1) / sty + 1;
@@ -421,10 +430,10 @@ DEV void walk_x(const Tile &T, int stz, int sty, double wo, double wi, const Lv 
         cs = case_of(pd, S, TX, T.e[2]);
         if (row_anchor && pd == T.e[2] - 1) keep |= 1u << k;
       }
-      const double pr = pred_k<NP>(k, cs, wo, wi, k > 0 ? ev[k - 1] : 0.0, ev[k], ev[k + 1],
+      const double pr = pred_k<NP, BND>(k, cs, wo, wi, k > 0 ? ev[k - 1] : 0.0, ev[k], ev[k + 1],
                                    k + 2 <= NP ? ev[k + 2] : 0.0);
       if (MODE == 0) {
-        if (!quant_fast(pr, pt[k], L, Rd, R, rec[k], code[k])) fail |= 1u << k;
+        if (!quant_fast(pr, pt[k], L, R, rec[k], code[k])) fail |= 1u << k;
       } else {
         rec[k] = dequant(pr, sy[k], L, R);
         if (sy[k] == 0xFFFFu) fail |= 1u << k;
@@ -485,11 +494,10 @@ DEV void walk_x(const Tile &T, int stz, int sty, double wo, double wi, const Lv 
 // 8 -> x = 4j on even quads only.  Quad 8 (x = 32..35) carries one real
 // line (x = 32); its other elements compute on staged data and are never
 // stored as codes (nor are elements beyond the grid on edge tiles).
-template <int S, int D, int STX, int MODE>
+template <int S, int D, int STX, int MODE, bool BND>
 DEV void walk_col(const Tile &T, int sta, double wo, double wi, const Lv &L, int R, bool exact,
                   const Out &O) {
   const int lane = threadIdx.x & 31;
-  const bool BND = T.bnd;
   constexpr uint32_t PD4 = 4u * ((D == 0) ? PZ : PX);
   constexpr int NE = (STX == 1) ? 4 : (STX == 2) ? 2 : 1;  // x-lines per quad
   constexpr int QS_ = (STX == 8) ? 2 : 1;                   // quad step
@@ -571,10 +579,10 @@ DEV void walk_col(const Tile &T, int sta, double wo, double wi, const Lv &L, int
       }
 #pragma unroll
       for (int e = 0; e < NE; ++e) {
-        const double pr = pred_k<NP>(k, cs, wo, wi, k > 0 ? ev[e][k - 1] : 0.0, ev[e][k],
+        const double pr = pred_k<NP, BND>(k, cs, wo, wi, k > 0 ? ev[e][k - 1] : 0.0, ev[e][k],
                                      ev[e][k + 1], k + 2 <= NP ? ev[e][k + 2] : 0.0);
         if (MODE == 0) {
-          if (!quant_fast(pr, pt[e][k], L, Rd, R, rec[e][k], code[e][k]))
+          if (!quant_fast(pr, pt[e][k], L, R, rec[e][k], code[e][k]))
             fail |= 1u << (e * NP + k);
         } else {
           rec[e][k] = dequant(pr, sy[e][k], L, R);
@@ -643,38 +651,38 @@ DEV void walk_col(const Tile &T, int sta, double wo, double wi, const Lv &L, int
   }
 }
 
-template <int MODE>
+template <int MODE, bool BND>
 DEV void run_pass(const Tile &T, int s, int D, int passed, bool nak, const Lv &L, int R,
                   bool exact, const Out &O) {
   const double wo = nak ? NAK_O : NAT_O, wi = nak ? NAK_I : NAT_I;
   const int stz = (passed & 1) ? s : 2 * s, sty = (passed & 2) ? s : 2 * s;
   const int stx = (passed & 4) ? s : 2 * s;
   if (s == 1) {
-    if (D == 2) walk_x<1, MODE>(T, stz, sty, wo, wi, L, R, exact, O);
+    if (D == 2) walk_x<1, MODE, BND>(T, stz, sty, wo, wi, L, R, exact, O);
     else if (D == 0) {
-      if (stx == 1) walk_col<1, 0, 1, MODE>(T, sty, wo, wi, L, R, exact, O);
-      else walk_col<1, 0, 2, MODE>(T, sty, wo, wi, L, R, exact, O);
+      if (stx == 1) walk_col<1, 0, 1, MODE, BND>(T, sty, wo, wi, L, R, exact, O);
+      else walk_col<1, 0, 2, MODE, BND>(T, sty, wo, wi, L, R, exact, O);
     } else {
-      if (stx == 1) walk_col<1, 1, 1, MODE>(T, stz, wo, wi, L, R, exact, O);
-      else walk_col<1, 1, 2, MODE>(T, stz, wo, wi, L, R, exact, O);
+      if (stx == 1) walk_col<1, 1, 1, MODE, BND>(T, stz, wo, wi, L, R, exact, O);
+      else walk_col<1, 1, 2, MODE, BND>(T, stz, wo, wi, L, R, exact, O);
     }
   } else if (s == 2) {
-    if (D == 2) walk_x<2, MODE>(T, stz, sty, wo, wi, L, R, exact, O);
+    if (D == 2) walk_x<2, MODE, BND>(T, stz, sty, wo, wi, L, R, exact, O);
     else if (D == 0) {
-      if (stx == 2) walk_col<2, 0, 2, MODE>(T, sty, wo, wi, L, R, exact, O);
-      else walk_col<2, 0, 4, MODE>(T, sty, wo, wi, L, R, exact, O);
+      if (stx == 2) walk_col<2, 0, 2, MODE, BND>(T, sty, wo, wi, L, R, exact, O);
+      else walk_col<2, 0, 4, MODE, BND>(T, sty, wo, wi, L, R, exact, O);
     } else {
-      if (stx == 2) walk_col<2, 1, 2, MODE>(T, stz, wo, wi, L, R, exact, O);
-      else walk_col<2, 1, 4, MODE>(T, stz, wo, wi, L, R, exact, O);
+      if (stx == 2) walk_col<2, 1, 2, MODE, BND>(T, stz, wo, wi, L, R, exact, O);
+      else walk_col<2, 1, 4, MODE, BND>(T, stz, wo, wi, L, R, exact, O);
     }
   } else {
-    if (D == 2) walk_x<4, MODE>(T, stz, sty, wo, wi, L, R, exact, O);
+    if (D == 2) walk_x<4, MODE, BND>(T, stz, sty, wo, wi, L, R, exact, O);
     else if (D == 0) {
-      if (stx == 4) walk_col<4, 0, 4, MODE>(T, sty, wo, wi, L, R, exact, O);
-      else walk_col<4, 0, 8, MODE>(T, sty, wo, wi, L, R, exact, O);
+      if (stx == 4) walk_col<4, 0, 4, MODE, BND>(T, sty, wo, wi, L, R, exact, O);
+      else walk_col<4, 0, 8, MODE, BND>(T, sty, wo, wi, L, R, exact, O);
     } else {
-      if (stx == 4) walk_col<4, 1, 4, MODE>(T, stz, wo, wi, L, R, exact, O);
-      else walk_col<4, 1, 8, MODE>(T, stz, wo, wi, L, R, exact, O);
+      if (stx == 4) walk_col<4, 1, 4, MODE, BND>(T, stz, wo, wi, L, R, exact, O);
+      else walk_col<4, 1, 8, MODE, BND>(T, stz, wo, wi, L, R, exact, O);
     }
   }
 }
@@ -685,7 +693,7 @@ struct Cfg {  // tuned configuration (per-CTA / per-warp copy)
   int nak[3];
 };
 
-template <int MODE>
+template <int MODE, bool BND>
 DEV void run_levels(const Tile &T, const Cfg &C, int R, bool exact, const Out &O) {
 #pragma unroll 1
   for (int lv = 0; lv < 3; ++lv) {
@@ -695,29 +703,65 @@ DEV void run_levels(const Tile &T, const Cfg &C, int R, bool exact, const Out &O
 #pragma unroll 1
     for (int i = 0; i < 3; ++i) {
       const int D = C.order[i];
-      run_pass<MODE>(T, s, D, passed, C.nak[D] != 0, L, R, exact, O);
+      run_pass<MODE, BND>(T, s, D, passed, C.nak[D] != 0, L, R, exact, O);
       passed |= 1 << D;
       __syncwarp();
     }
   }
 }
 
+// Interior tiles (closing plane inside the grid on every axis) form the box
+// ni[0] x ni[1] x ni[2]; edge tiles are the shell around it (z beyond, then
+// y beyond, then x beyond).  t indexes one set, x fastest.
+template <bool BND>
+DEV int tile_count(const Geo &G) {
+  const int ni = G.ni[0] * G.ni[1] * G.ni[2];
+  return BND ? G.nt[0] * G.nt[1] * G.nt[2] - ni : ni;
+}
+template <bool BND>
 DEV void tile_origin(const Geo &G, int t, int o[3]) {
-  const int tx = t % G.nt[2];
-  const int r = t / G.nt[2];
-  const int ty = r % G.nt[1];
-  const int tz = r / G.nt[1];
+  int tz, ty, tx;
+  if (!BND) {
+    tx = t % G.ni[2];
+    const int r = t / G.ni[2];
+    ty = r % G.ni[1];
+    tz = r / G.ni[1];
+  } else {
+    const int a = (G.nt[0] - G.ni[0]) * G.nt[1] * G.nt[2];
+    const int b = G.ni[0] * (G.nt[1] - G.ni[1]) * G.nt[2];
+    if (t < a) {
+      tx = t % G.nt[2];
+      const int r = t / G.nt[2];
+      ty = r % G.nt[1];
+      tz = G.ni[0] + r / G.nt[1];
+    } else if (t < a + b) {
+      const int u = t - a;
+      tx = u % G.nt[2];
+      const int r = u / G.nt[2];
+      const int w = G.nt[1] - G.ni[1];
+      ty = G.ni[1] + r % w;
+      tz = r / w;
+    } else {
+      const int u = t - a - b;
+      const int w = G.nt[2] - G.ni[2];
+      tx = G.ni[2] + u % w;
+      const int r = u / w;
+      ty = r % G.ni[1];
+      tz = r / G.ni[1];
+    }
+  }
   o[0] = G.z0 + tz * TZ;
   o[1] = ty * TY;
   o[2] = tx * TX;
 }
 
+template <bool BND>
 DEV void tile_init(Tile &T, const Geo &G, const int o[3]) {
   for (int a = 0; a < 3; ++a) {
     T.o[a] = o[a];
     T.e[a] = G.ext[a] - o[a];
   }
-  T.bnd = !(o[0] + TZ <= G.ext[0] - 1 && o[1] + TY <= G.ext[1] - 1 && o[2] + TX <= G.ext[2] - 1);
+  T.bnd = BND;
   T.gs0 = (int64_t)G.ext[1] * G.ext[2];
   T.gs1 = G.ext[2];
 }
@@ -785,6 +829,7 @@ DEV void sched_done(unsigned int *q) {
 // issued as soon as the passes release the staging buffer, so it overlaps
 // the epilogue (code store / histogram, or the float store).
 // ---------------------------------------------------------------------------
+template <bool BND>
 __global__ void __launch_bounds__(NT, 3)
     k_t3_predict(const __grid_constant__ CUtensorMap tm, const float *__restrict__ x, Geo G,
                  const cszi_ctl *__restrict__ ctl, uint16_t *__restrict__ sym,
@@ -799,14 +844,14 @@ __global__ void __launch_bounds__(NT, 3)
   uint32_t *hs = reinterpret_cast<uint32_t *>(sm + NW * P_WARP);
   const uint32_t buf = smem_u32(sm + warp * P_WARP);
   const uint32_t codes = buf + BUF_BYTES;
-  const int ntiles = G.nt[0] * G.nt[1] * G.nt[2];
+  const int ntiles = tile_count<BND>(G);
   unsigned int *q = g_t3_sched + 2 * slot;
   int t = next_tile(q);
   if (lane == 0) {
     mbar_init(&mbar[warp]);
     if (t < ntiles && G.tma) {
       int o[3];
-      tile_origin(G, t, o);
+      tile_origin<BND>(G, t, o);
       mbar_expect(&mbar[warp], (uint32_t)BUF_BYTES);
       tma_load3(sm + warp * P_WARP, &tm, o[2], o[1], o[0] - G.z0, &mbar[warp]);
     }
@@ -832,12 +877,12 @@ __global__ void __launch_bounds__(NT, 3)
   uint32_t zeros = 0, phase = 0;
   while (t < ntiles) {
     int o[3];
-    tile_origin(G, t, o);
+    tile_origin<BND>(G, t, o);
     Tile T;
     T.buf = buf;
     T.codes = codes;
     T.syms = 0;
-    tile_init(T, G, o);
+    tile_init<BND>(T, G, o);
     // codes default to R (anchors: code 0, predictor.py:414)
     for (int i = lane; i < NCODE / 8; i += 32) sts_u4(codes + 16u * i, make_uint4(rr, rr, rr, rr));
     if (G.tma) {
@@ -847,12 +892,12 @@ __global__ void __launch_bounds__(NT, 3)
       stage_manual_f32(buf, x, G, o);
     }
     __syncwarp();
-    run_levels<0>(T, C, R, exact, O);
+    run_levels<0, BND>(T, C, R, exact, O);
     // staging buffer free: prefetch the next tile
     const int tn = next_tile(q);
     if (lane == 0 && tn < ntiles && G.tma) {
       int on[3];
-      tile_origin(G, tn, on);
+      tile_origin<BND>(G, tn, on);
       fence_proxy_async();
       mbar_expect(&mbar[warp], (uint32_t)BUF_BYTES);
       tma_load3(sm + warp * P_WARP, &tm, on[2], on[1], on[0] - G.z0, &mbar[warp]);
@@ -918,6 +963,7 @@ __global__ void __launch_bounds__(NT, 3)
       if (hs[i]) atomicAdd(&hist[i], (u64)hs[i]);
 }
 
+template <bool BND>
 __global__ void __launch_bounds__(NT, 3)
     k_t3_reconstruct(const __grid_constant__ CUtensorMap tm, const uint16_t *__restrict__ sym,
                      const float *__restrict__ anchors, const u64 *out_idx,
@@ -931,14 +977,14 @@ __global__ void __launch_bounds__(NT, 3)
   unsigned char *sm = align128(t3_smem);
   const uint32_t syms = smem_u32(sm + warp * R_WARP);
   const uint32_t buf = syms + SYM_BYTES;
-  const int ntiles = G.nt[0] * G.nt[1] * G.nt[2];
+  const int ntiles = tile_count<BND>(G);
   unsigned int *q = g_t3_sched + 2 * slot;
   int t = next_tile(q);
   if (lane == 0) {
     mbar_init(&mbar[warp]);
     if (t < ntiles && G.tma) {
       int o[3];
-      tile_origin(G, t, o);
+      tile_origin<BND>(G, t, o);
       mbar_expect(&mbar[warp], (uint32_t)(NSYM * 2));
       tma_load3(sm + warp * R_WARP, &tm, o[2], o[1], o[0] - G.z0, &mbar[warp]);
     }
@@ -960,15 +1006,15 @@ __global__ void __launch_bounds__(NT, 3)
   uint32_t phase = 0;
   while (t < ntiles) {
     int o[3];
-    tile_origin(G, t, o);
+    tile_origin<BND>(G, t, o);
     Tile T;
     T.buf = buf;
     T.codes = 0;
     T.syms = syms;
-    tile_init(T, G, o);
+    tile_init<BND>(T, G, o);
     // edge tiles: zero the buffer so that weight-0 terms of missing
     // neighbours read finite values (interior tiles read only computed ones)
-    if (T.bnd)
+    if (BND)
       for (int i = lane; i < NBUF / 4; i += 32) sts_f4(buf + 16u * i, make_float4(0.f, 0.f, 0.f, 0.f));
     __syncwarp();
     // seed the anchors of the closed tile (multiples of 8, plus ext - 1)
@@ -994,11 +1040,11 @@ __global__ void __launch_bounds__(NT, 3)
       stage_manual_u16(syms, sym, G, o);
     }
     __syncwarp();
-    run_levels<1>(T, C, R, false, O);
+    run_levels<1, BND>(T, C, R, false, O);
     const int tn = next_tile(q);
     if (lane == 0 && tn < ntiles && G.tma) {
       int on[3];
-      tile_origin(G, tn, on);
+      tile_origin<BND>(G, tn, on);
       fence_proxy_async();
       mbar_expect(&mbar[warp], (uint32_t)(NSYM * 2));
       tma_load3(sm + warp * R_WARP, &tm, on[2], on[1], on[0] - G.z0, &mbar[warp]);
@@ -1105,6 +1151,16 @@ static bool t3_geo(const cszi_geom *g, int32_t radius, Geo &G) {
   G.nt[0] = (int)((zown + TZ - 1) / TZ);
   G.nt[1] = (G.ext[1] + TY - 1) / TY;
   G.nt[2] = (G.ext[2] + TX - 1) / TX;
+  {
+    const int T3[3] = {TZ, TY, TX};
+    const int64_t first[3] = {G.z0, 0, 0};
+    for (int a = 0; a < 3; ++a) {
+      // tiles whose closing plane o + T <= ext - 1
+      const int64_t lim = (int64_t)G.ext[a] - 1 - first[a];
+      int64_t n = lim >= T3[a] ? lim / T3[a] : 0;
+      G.ni[a] = (int)(n < G.nt[a] ? n : G.nt[a]);
+    }
+  }
   if ((int64_t)G.nt[0] * G.nt[1] * G.nt[2] > (int64_t)NW * 0x7fffffff) return false;
   // flat indices of the outlier lookup and of planes are int64; the
   // in-kernel (z * gs0 + ...) products need ext[1] * ext[2] < 2^62: fine.
@@ -1128,13 +1184,24 @@ static int launch_predict_t3(const float *x, const cszi_geom *g, int32_t radius,
   G.tma = make_tmap(&tm, x, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, G.ext[2], G.ext[1], G.nzl, PX)
               ? 1
               : 0;
-  const int64_t ntiles = (int64_t)G.nt[0] * G.nt[1] * G.nt[2];
+  const int64_t nall = (int64_t)G.nt[0] * G.nt[1] * G.nt[2];
+  const int64_t nint = (int64_t)G.ni[0] * G.ni[1] * G.ni[2];
   const size_t smem =
       128 + (size_t)NW * P_WARP + (G.hist_smem ? sizeof(uint32_t) * 2 * radius : 0);
-  cudaFuncSetAttribute(k_t3_predict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const unsigned grid = persistent_grid((const void *)k_t3_predict, smem, ntiles);
-  k_t3_predict<<<grid, NT, smem, st>>>(tm, x, G, ctl, sym, hist, sched_slot());
-  note_launch();
+  if (nint > 0) {
+    cudaFuncSetAttribute(k_t3_predict<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    const unsigned grid = persistent_grid((const void *)k_t3_predict<false>, smem, nint);
+    k_t3_predict<false><<<grid, NT, smem, st>>>(tm, x, G, ctl, sym, hist, sched_slot());
+    note_launch();
+  }
+  if (nall > nint) {
+    cudaFuncSetAttribute(k_t3_predict<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    const unsigned grid = persistent_grid((const void *)k_t3_predict<true>, smem, nall - nint);
+    k_t3_predict<true><<<grid, NT, smem, st>>>(tm, x, G, ctl, sym, hist, sched_slot());
+    note_launch();
+  }
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
@@ -1147,14 +1214,26 @@ static int launch_recon_t3(const uint16_t *sym, const float *anchors, const u64 
   G.tma = make_tmap(&tm, sym, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, G.ext[2], G.ext[1], G.nzl, SP)
               ? 1
               : 0;
-  const int64_t ntiles = (int64_t)G.nt[0] * G.nt[1] * G.nt[2];
+  const int64_t nall = (int64_t)G.nt[0] * G.nt[1] * G.nt[2];
+  const int64_t nint = (int64_t)G.ni[0] * G.ni[1] * G.ni[2];
   const size_t smem = 128 + (size_t)NW * R_WARP;
-  cudaFuncSetAttribute(k_t3_reconstruct, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)smem);
-  const unsigned grid = persistent_grid((const void *)k_t3_reconstruct, smem, ntiles);
-  k_t3_reconstruct<<<grid, NT, smem, st>>>(
-      tm, sym, anchors, oidx, oval, nout, nout_dev, G, lc, y, sched_slot());
-  note_launch();
+  if (nint > 0) {
+    cudaFuncSetAttribute(k_t3_reconstruct<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    const unsigned grid = persistent_grid((const void *)k_t3_reconstruct<false>, smem, nint);
+    k_t3_reconstruct<false><<<grid, NT, smem, st>>>(tm, sym, anchors, oidx, oval, nout, nout_dev,
+                                                    G, lc, y, sched_slot());
+    note_launch();
+  }
+  if (nall > nint) {
+    cudaFuncSetAttribute(k_t3_reconstruct<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    const unsigned grid =
+        persistent_grid((const void *)k_t3_reconstruct<true>, smem, nall - nint);
+    k_t3_reconstruct<true><<<grid, NT, smem, st>>>(tm, sym, anchors, oidx, oval, nout, nout_dev,
+                                                   G, lc, y, sched_slot());
+    note_launch();
+  }
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
