@@ -227,37 +227,29 @@ __device__ __noinline__ QS fix_point(uint32_t a, uint32_t st, int cs, double wo,
 }
 
 // Fast quantiser; returns false when undecided (then call quant_slow).
-//  * t' = r * RN(1/e2) lies within 3 ulp (< 2^-36 for |t| < 2^13) of
-//    RN(r / e2).  m = RN(t' + 1.5 * 2^34) has ulp 2^-18, so for |t'| < 2^13
-//    the low word of m is F = round(t' * 2^18) as an int32 (the high word
-//    tells whether t' was in range; outside it |q| >= 2^13 >= R: outlier).
-//    Unless t' * 2^18 lies within 1.5 units of a half-integer boundary,
-//    rint(t) == (F + 2^17) >> 18 == trunc(t + copysign(.5, t)).
+//  * t' = r * RN(1/e2) lies within 3 ulp of RN(r / e2); unless t' is within
+//    2^-20 of a half-integer, rint(t') == trunc(t + copysign(.5, t)); the
+//    magic-number round leaves rint(t') in the low word of m.
 //  * y = RN(pred + RN(e2 q)); rec = RN32(y).  |rec - y| <= 2^-24 |y| +
 //    2^-150, so |dy| <= leb (1 - 2^-40) - 2^-23 |y| - 2^-148 with
 //    dy = RN(y - o) implies RN(f64(rec) - o) <= leb: the guard is false.
 //    (lebs is capped at 2^100 so that such a y never overflows float32.)
 // big (|q| >= R) points are outliers whatever the guard says.
-constexpr double MAGIC34 = 25769803776.0;  // 1.5 * 2^34
-DEV bool quant_fast(double pred, float o32, const Lv &L, int R, float &recon, uint32_t &sym) {
+DEV bool quant_fast(double pred, float o32, const Lv &L, double Rd, int R, float &recon,
+                    uint32_t &sym) {
   const double o = (double)o32;
   const double r = dsub(o, pred);
   const double t = dmul(r, L.inv);
-  const double m = dadd(t, MAGIC34);
-  const int F = __double2loint(m);
-  const int hi = __double2hiint(m);
-  const bool in_range = (hi + (int)((uint32_t)F >> 31)) == 0x42180000;
-  const int u = F + 0x20000;
-  const int q = u >> 18;
-  const bool near_ok = ((u + 2) & 0x3FFFF) >= 4;
-  const bool big = !in_range || q >= R || q <= -R;
-  const double qd = dsub(__hiloint2double(0x43300000, q ^ (int)0x80000000), 4503601774854144.0);
-  const double y = dadd(pred, dmul(L.e2, qd));
+  const double m = dadd(t, MAGIC);
+  const double rq = dsub(m, MAGIC);
+  const bool near_ok = fabs(dsub(t, rq)) <= 0.49999904632568359375;
+  const bool big = fabs(rq) >= Rd;
+  const double y = dadd(pred, dmul(L.e2, rq));
   const double dy = dsub(y, o);
   const bool safe = fabs(dy) <= __fma_rn(fabs(y), -0x1p-23, L.lebs);
   recon = big ? o32 : __double2float_rn(y);
-  sym = big ? 0u : (uint32_t)(q + R);
-  return big ? (!in_range || near_ok) : (near_ok && safe);
+  sym = big ? 0u : (uint32_t)(__double2loint(m) + R);
+  return near_ok && (big || safe);
 }
 
 struct Out {  // decompress outlier list
@@ -433,7 +425,7 @@ DEV void walk_x(const Tile &T, int stz, int sty, double wo, double wi, const Lv 
       const double pr = pred_k<NP, BND>(k, cs, wo, wi, k > 0 ? ev[k - 1] : 0.0, ev[k], ev[k + 1],
                                    k + 2 <= NP ? ev[k + 2] : 0.0);
       if (MODE == 0) {
-        if (!quant_fast(pr, pt[k], L, R, rec[k], code[k])) fail |= 1u << k;
+        if (!quant_fast(pr, pt[k], L, Rd, R, rec[k], code[k])) fail |= 1u << k;
       } else {
         rec[k] = dequant(pr, sy[k], L, R);
         if (sy[k] == 0xFFFFu) fail |= 1u << k;
@@ -582,7 +574,7 @@ DEV void walk_col(const Tile &T, int sta, double wo, double wi, const Lv &L, int
         const double pr = pred_k<NP, BND>(k, cs, wo, wi, k > 0 ? ev[e][k - 1] : 0.0, ev[e][k],
                                      ev[e][k + 1], k + 2 <= NP ? ev[e][k + 2] : 0.0);
         if (MODE == 0) {
-          if (!quant_fast(pr, pt[e][k], L, R, rec[e][k], code[e][k]))
+          if (!quant_fast(pr, pt[e][k], L, Rd, R, rec[e][k], code[e][k]))
             fail |= 1u << (e * NP + k);
         } else {
           rec[e][k] = dequant(pr, sy[e][k], L, R);
