@@ -747,13 +747,17 @@ DEV void tile_origin(const Geo &G, int t, int o[3]) {
   o[2] = tx * TX;
 }
 
-template <bool BND>
-DEV void tile_init(Tile &T, const Geo &G, const int o[3]) {
+DEV void tile_of(const Geo &G, int nint, int u, int o[3]) {
+  if (u < nint) tile_origin<false>(G, u, o);
+  else tile_origin<true>(G, u - nint, o);
+}
+
+DEV void tile_init(Tile &T, const Geo &G, const int o[3], bool bnd) {
   for (int a = 0; a < 3; ++a) {
     T.o[a] = o[a];
     T.e[a] = G.ext[a] - o[a];
   }
-  T.bnd = BND;
+  T.bnd = bnd;
   T.gs0 = (int64_t)G.ext[1] * G.ext[2];
   T.gs1 = G.ext[2];
 }
@@ -817,11 +821,11 @@ DEV void sched_done(unsigned int *q) {
 }
 
 // ---------------------------------------------------------------------------
-// kernels: persistent warps, one tile at a time; the next tile's TMA load is
+// kernels: persistent warps take tiles from one queue, interior tiles first
+// (their code has no edge logic), then the edge shell; one tile at a time; the next tile's TMA load is
 // issued as soon as the passes release the staging buffer, so it overlaps
 // the epilogue (code store / histogram, or the float store).
 // ---------------------------------------------------------------------------
-template <bool BND>
 __global__ void __launch_bounds__(NT, 3)
     k_t3_predict(const __grid_constant__ CUtensorMap tm, const float *__restrict__ x, Geo G,
                  const cszi_ctl *__restrict__ ctl, uint16_t *__restrict__ sym,
@@ -836,14 +840,15 @@ __global__ void __launch_bounds__(NT, 3)
   uint32_t *hs = reinterpret_cast<uint32_t *>(sm + NW * P_WARP);
   const uint32_t buf = smem_u32(sm + warp * P_WARP);
   const uint32_t codes = buf + BUF_BYTES;
-  const int ntiles = tile_count<BND>(G);
+  const int nint = tile_count<false>(G);
+  const int ntiles = nint + tile_count<true>(G);
   unsigned int *q = g_t3_sched + 2 * slot;
   int t = next_tile(q);
   if (lane == 0) {
     mbar_init(&mbar[warp]);
     if (t < ntiles && G.tma) {
       int o[3];
-      tile_origin<BND>(G, t, o);
+      tile_of(G, nint, t, o);
       mbar_expect(&mbar[warp], (uint32_t)BUF_BYTES);
       tma_load3(sm + warp * P_WARP, &tm, o[2], o[1], o[0] - G.z0, &mbar[warp]);
     }
@@ -869,12 +874,12 @@ __global__ void __launch_bounds__(NT, 3)
   uint32_t zeros = 0, phase = 0;
   while (t < ntiles) {
     int o[3];
-    tile_origin<BND>(G, t, o);
+    tile_of(G, nint, t, o);
     Tile T;
     T.buf = buf;
     T.codes = codes;
     T.syms = 0;
-    tile_init<BND>(T, G, o);
+    tile_init(T, G, o, t >= nint);
     // codes default to R (anchors: code 0, predictor.py:414)
     for (int i = lane; i < NCODE / 8; i += 32) sts_u4(codes + 16u * i, make_uint4(rr, rr, rr, rr));
     if (G.tma) {
@@ -884,12 +889,13 @@ __global__ void __launch_bounds__(NT, 3)
       stage_manual_f32(buf, x, G, o);
     }
     __syncwarp();
-    run_levels<0, BND>(T, C, R, exact, O);
+    if (T.bnd) run_levels<0, true>(T, C, R, exact, O);
+    else run_levels<0, false>(T, C, R, exact, O);
     // staging buffer free: prefetch the next tile
     const int tn = next_tile(q);
     if (lane == 0 && tn < ntiles && G.tma) {
       int on[3];
-      tile_origin<BND>(G, tn, on);
+      tile_of(G, nint, tn, on);
       fence_proxy_async();
       mbar_expect(&mbar[warp], (uint32_t)BUF_BYTES);
       tma_load3(sm + warp * P_WARP, &tm, on[2], on[1], on[0] - G.z0, &mbar[warp]);
@@ -955,7 +961,6 @@ __global__ void __launch_bounds__(NT, 3)
       if (hs[i]) atomicAdd(&hist[i], (u64)hs[i]);
 }
 
-template <bool BND>
 __global__ void __launch_bounds__(NT, 3)
     k_t3_reconstruct(const __grid_constant__ CUtensorMap tm, const uint16_t *__restrict__ sym,
                      const float *__restrict__ anchors, const u64 *out_idx,
@@ -969,14 +974,15 @@ __global__ void __launch_bounds__(NT, 3)
   unsigned char *sm = align128(t3_smem);
   const uint32_t syms = smem_u32(sm + warp * R_WARP);
   const uint32_t buf = syms + SYM_BYTES;
-  const int ntiles = tile_count<BND>(G);
+  const int nint = tile_count<false>(G);
+  const int ntiles = nint + tile_count<true>(G);
   unsigned int *q = g_t3_sched + 2 * slot;
   int t = next_tile(q);
   if (lane == 0) {
     mbar_init(&mbar[warp]);
     if (t < ntiles && G.tma) {
       int o[3];
-      tile_origin<BND>(G, t, o);
+      tile_of(G, nint, t, o);
       mbar_expect(&mbar[warp], (uint32_t)(NSYM * 2));
       tma_load3(sm + warp * R_WARP, &tm, o[2], o[1], o[0] - G.z0, &mbar[warp]);
     }
@@ -998,15 +1004,15 @@ __global__ void __launch_bounds__(NT, 3)
   uint32_t phase = 0;
   while (t < ntiles) {
     int o[3];
-    tile_origin<BND>(G, t, o);
+    tile_of(G, nint, t, o);
     Tile T;
     T.buf = buf;
     T.codes = 0;
     T.syms = syms;
-    tile_init<BND>(T, G, o);
+    tile_init(T, G, o, t >= nint);
     // edge tiles: zero the buffer so that weight-0 terms of missing
     // neighbours read finite values (interior tiles read only computed ones)
-    if (BND)
+    if (T.bnd)
       for (int i = lane; i < NBUF / 4; i += 32) sts_f4(buf + 16u * i, make_float4(0.f, 0.f, 0.f, 0.f));
     __syncwarp();
     // seed the anchors of the closed tile (multiples of 8, plus ext - 1)
@@ -1032,11 +1038,12 @@ __global__ void __launch_bounds__(NT, 3)
       stage_manual_u16(syms, sym, G, o);
     }
     __syncwarp();
-    run_levels<1, BND>(T, C, R, false, O);
+    if (T.bnd) run_levels<1, true>(T, C, R, false, O);
+    else run_levels<1, false>(T, C, R, false, O);
     const int tn = next_tile(q);
     if (lane == 0 && tn < ntiles && G.tma) {
       int on[3];
-      tile_origin<BND>(G, tn, on);
+      tile_of(G, nint, tn, on);
       fence_proxy_async();
       mbar_expect(&mbar[warp], (uint32_t)(NSYM * 2));
       tma_load3(sm + warp * R_WARP, &tm, on[2], on[1], on[0] - G.z0, &mbar[warp]);
@@ -1177,23 +1184,12 @@ static int launch_predict_t3(const float *x, const cszi_geom *g, int32_t radius,
               ? 1
               : 0;
   const int64_t nall = (int64_t)G.nt[0] * G.nt[1] * G.nt[2];
-  const int64_t nint = (int64_t)G.ni[0] * G.ni[1] * G.ni[2];
   const size_t smem =
       128 + (size_t)NW * P_WARP + (G.hist_smem ? sizeof(uint32_t) * 2 * radius : 0);
-  if (nint > 0) {
-    cudaFuncSetAttribute(k_t3_predict<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    const unsigned grid = persistent_grid((const void *)k_t3_predict<false>, smem, nint);
-    k_t3_predict<false><<<grid, NT, smem, st>>>(tm, x, G, ctl, sym, hist, sched_slot());
-    note_launch();
-  }
-  if (nall > nint) {
-    cudaFuncSetAttribute(k_t3_predict<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    const unsigned grid = persistent_grid((const void *)k_t3_predict<true>, smem, nall - nint);
-    k_t3_predict<true><<<grid, NT, smem, st>>>(tm, x, G, ctl, sym, hist, sched_slot());
-    note_launch();
-  }
+  cudaFuncSetAttribute(k_t3_predict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const unsigned grid = persistent_grid((const void *)k_t3_predict, smem, nall);
+  k_t3_predict<<<grid, NT, smem, st>>>(tm, x, G, ctl, sym, hist, sched_slot());
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
@@ -1207,25 +1203,13 @@ static int launch_recon_t3(const uint16_t *sym, const float *anchors, const u64 
               ? 1
               : 0;
   const int64_t nall = (int64_t)G.nt[0] * G.nt[1] * G.nt[2];
-  const int64_t nint = (int64_t)G.ni[0] * G.ni[1] * G.ni[2];
   const size_t smem = 128 + (size_t)NW * R_WARP;
-  if (nint > 0) {
-    cudaFuncSetAttribute(k_t3_reconstruct<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    const unsigned grid = persistent_grid((const void *)k_t3_reconstruct<false>, smem, nint);
-    k_t3_reconstruct<false><<<grid, NT, smem, st>>>(tm, sym, anchors, oidx, oval, nout, nout_dev,
-                                                    G, lc, y, sched_slot());
-    note_launch();
-  }
-  if (nall > nint) {
-    cudaFuncSetAttribute(k_t3_reconstruct<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    const unsigned grid =
-        persistent_grid((const void *)k_t3_reconstruct<true>, smem, nall - nint);
-    k_t3_reconstruct<true><<<grid, NT, smem, st>>>(tm, sym, anchors, oidx, oval, nout, nout_dev,
-                                                   G, lc, y, sched_slot());
-    note_launch();
-  }
+  cudaFuncSetAttribute(k_t3_reconstruct, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  const unsigned grid = persistent_grid((const void *)k_t3_reconstruct, smem, nall);
+  k_t3_reconstruct<<<grid, NT, smem, st>>>(tm, sym, anchors, oidx, oval, nout, nout_dev, G, lc,
+                                           y, sched_slot());
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
