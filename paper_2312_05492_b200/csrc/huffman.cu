@@ -574,14 +574,23 @@ struct DecSmem {
   u64 first_code[33];
   uint32_t first_index[33];
   uint32_t counts[33];
+  int zrun;       // 1: exactly one length-1 codeword; canonically it is "0"
+  uint32_t zsym;  // its symbol
 };
 
-DEV void load_dec_smem(DecSmem &T, const DecTables *G) {
+DEV void load_dec_smem(DecSmem &T, const DecTables *G, const uint16_t *sorted) {
   for (int i = threadIdx.x; i < 4096; i += blockDim.x) T.lut[i] = G->lut[i];
   for (int i = threadIdx.x; i < 33; i += blockDim.x) {
     T.first_code[i] = G->first_code[i];
     T.first_index[i] = G->first_index[i];
     T.counts[i] = G->counts[i];
+  }
+  if (threadIdx.x == 0) {
+    // canonical order (huffman.py:128-160): the first codeword is all
+    // zeros, so a single length-1 symbol owns "0" and a run of z zero bits
+    // is z copies of it -- counted / emitted per run instead of per bit
+    T.zrun = (G->counts[1] == 1 && G->first_code[1] == 0) ? 1 : 0;
+    T.zsym = T.zrun ? sorted[G->first_index[1]] : 0u;
   }
   __syncthreads();
 }
@@ -686,7 +695,7 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_spec(Stream s, const DecTables *
   const u64 j0 = (u64)blockIdx.x * DEC_NT;
   SmemStream ss;
   stage_words(sw, s, j0, ss);
-  load_dec_smem(T, G);  // ends with __syncthreads()
+  load_dec_smem(T, G, sorted);  // ends with __syncthreads()
   const u64 j = j0 + threadIdx.x;
   if (j >= M) return;
   SmemReader br;
@@ -695,9 +704,17 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_spec(Stream s, const DecTables *
   const u64 end = min((j + 1) * DEC_C, s.nb);
   uint32_t cnt = 0;
   uint8_t dead = 0;
+  const bool zr = T.zrun != 0;
   while (pos < end) {
+    const uint32_t w = br.peek(ss, pos);
+    if (zr && !(w >> 31)) {  // run of the "0" codeword
+      const u64 adv = min((u64)__clz(w), end - pos);
+      pos += adv;
+      cnt += (uint32_t)adv;
+      continue;
+    }
     uint32_t len;
-    decode_at(T, sorted, br.peek(ss, pos), len);
+    decode_at(T, sorted, w, len);
     if (len == 0 || pos + len > s.nb) {
       dead = 1;
       break;
@@ -721,7 +738,7 @@ __global__ void __launch_bounds__(256) k_dec_sync(Stream s, const DecTables *G,
                                                  const uint8_t *chg_prev, u64 *X, uint32_t *K,
                                                  uint8_t *D, uint8_t *chg, uint32_t *nchg) {
   __shared__ DecSmem T;
-  load_dec_smem(T, G);
+  load_dec_smem(T, G, sorted);
   const u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x;
   if (j >= M) return;
   u64 e;
@@ -758,8 +775,16 @@ __global__ void __launch_bounds__(256) k_dec_sync(Stream s, const DecTables *G,
       break;
     }
     if (!b_alive || a < b) {
+      const uint32_t w = ba.peek(s, a);
+      if (T.zrun && !(w >> 31)) {  // zero run: every bit is a boundary
+        u64 adv = min((u64)__clz(w), end - a);
+        if (b_alive && b > a) adv = min(adv, b - a);
+        a += adv;
+        ca += (uint32_t)adv;
+        continue;
+      }
       uint32_t len;
-      decode_at(T, sorted, ba.peek(s, a), len);
+      decode_at(T, sorted, w, len);
       if (len == 0 || a + len > s.nb) {
         xo = a;
         ko = ca;
@@ -773,8 +798,15 @@ __global__ void __launch_bounds__(256) k_dec_sync(Stream s, const DecTables *G,
         b_alive = false;
         continue;
       }
+      const uint32_t w = bb.peek(s, b);
+      if (T.zrun && !(w >> 31)) {
+        const u64 adv = min(min((u64)__clz(w), end - b), a - b > 0 ? a - b : (u64)1);
+        b += adv;
+        cb += (uint32_t)adv;
+        continue;
+      }
       uint32_t len;
-      decode_at(T, sorted, bb.peek(s, b), len);
+      decode_at(T, sorted, w, len);
       if (len == 0 || b + len > s.nb) {
         b_alive = false;
         continue;
@@ -815,7 +847,7 @@ __global__ void __launch_bounds__(256) k_dec_table(Stream s, const DecTables *G,
                                                   const uint16_t *sorted, u64 M, int lmax,
                                                   uint8_t *tab, uint32_t *ktab, uint8_t *dtab) {
   __shared__ DecSmem T;
-  load_dec_smem(T, G);
+  load_dec_smem(T, G, sorted);
   const u64 w = blockIdx.x * (u64)blockDim.x + threadIdx.x;
   if (w >= M * (u64)lmax) return;
   const u64 j = w / lmax;
@@ -860,8 +892,8 @@ constexpr int DEC_K = 32;
 template <typename OutT>
 __global__ void __launch_bounds__(DEC_NT) k_dec_write(Stream s, const DecTables *G,
                                                      const uint16_t *sorted, u64 M, const u64 *X,
-                                                     const u64 *off, u64 n, int R,
-                                                     OutT *__restrict__ out) {
+                                                     const u64 *off, const uint32_t *cnts,
+                                                     u64 n, int R, OutT *__restrict__ out) {
   __shared__ DecSmem T;
   __shared__ uint32_t sw[DEC_SW];
   constexpr int K = (sizeof(OutT) == 2) ? DEC_K : DEC_K / 2;
@@ -869,7 +901,7 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_write(Stream s, const DecTables 
   const u64 j0 = (u64)blockIdx.x * DEC_NT;
   SmemStream ss;
   stage_words(sw, s, j0, ss);
-  load_dec_smem(T, G);
+  load_dec_smem(T, G, sorted);
   const u64 j = j0 + threadIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   u64 k = (j < M) ? off[j] : n;
@@ -878,12 +910,58 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_write(Stream s, const DecTables 
   bool active = j < M && k < n;
   SmemReader br;
   br.init();
+  if (T.zrun) {
+    // Sparse path: the chunk's output range [k, k1) is first filled with
+    // the run symbol in 16-byte stores, then only the other symbols are
+    // stored (program order makes them win).  Runs cost O(1) each.
+    if (!active) return;
+    const u64 k1 = min(k + cnts[j], n);
+    const OutT zv = (sizeof(OutT) == 4) ? (OutT)((int32_t)T.zsym - R) : (OutT)T.zsym;
+    constexpr int PER = 16 / sizeof(OutT);
+    u64 f = k;
+    for (; f < k1 && (f % PER); ++f) out[f] = zv;
+    uint4 zz;
+    {
+      OutT tmp[PER];
+#pragma unroll
+      for (int i = 0; i < PER; ++i) tmp[i] = zv;
+      zz = *reinterpret_cast<const uint4 *>(tmp);
+    }
+    for (; f + PER <= k1; f += PER) __stcs(reinterpret_cast<uint4 *>(out + f), zz);
+    for (; f < k1; ++f) out[f] = zv;
+    while (pos < end && k < k1) {
+      const uint32_t w = br.peek(ss, pos);
+      if (!(w >> 31)) {
+        const u64 adv = min(min((u64)__clz(w), end - pos), k1 - k);
+        pos += adv;
+        k += adv;
+        continue;
+      }
+      uint32_t len;
+      const uint32_t sym = decode_at(T, sorted, w, len);
+      if (len == 0 || pos + len > s.nb) break;  // dead chain: reported by k_dec_check
+      pos += len;
+      out[k++] = (sizeof(OutT) == 4) ? (OutT)((int32_t)sym - R) : (OutT)sym;
+    }
+    return;
+  }
   while (__any_sync(CSZI_FULL, active)) {
     int cnt = 0;
     if (active) {
       while (cnt < K && pos < end && k + cnt < n) {
+        const uint32_t w = br.peek(ss, pos);
+        if (T.zrun && !(w >> 31)) {  // run of the "0" codeword
+          u64 adv = min((u64)__clz(w), end - pos);
+          adv = min(adv, (u64)(K - cnt));
+          adv = min(adv, n - k - cnt);
+          const OutT zv = (sizeof(OutT) == 4) ? (OutT)((int32_t)T.zsym - R) : (OutT)T.zsym;
+          for (int i = 0; i < (int)adv; ++i) ob[warp][lane][cnt + i] = zv;
+          cnt += (int)adv;
+          pos += adv;
+          continue;
+        }
         uint32_t len;
-        const uint32_t sym = decode_at(T, sorted, br.peek(ss, pos), len);
+        const uint32_t sym = decode_at(T, sorted, w, len);
         if (len == 0 || pos + len > s.nb) {
           pos = end;  // dead chain: truncation is reported by k_dec_check
           break;
@@ -1141,10 +1219,10 @@ int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *de
   k_dec_check<<<1, 1, 0, st>>>(off, K, first_dead, total, n, ctl);
   note_launch();
   if (out_kind == 0)
-    k_dec_write<uint16_t><<<dblocks, DEC_NT, 0, st>>>(s, G, sorted, M, X0, off, n, R,
+    k_dec_write<uint16_t><<<dblocks, DEC_NT, 0, st>>>(s, G, sorted, M, X0, off, K, n, R,
                                                       reinterpret_cast<uint16_t *>(out));
   else
-    k_dec_write<int32_t><<<dblocks, DEC_NT, 0, st>>>(s, G, sorted, M, X0, off, n, R,
+    k_dec_write<int32_t><<<dblocks, DEC_NT, 0, st>>>(s, G, sorted, M, X0, off, K, n, R,
                                                      reinterpret_cast<int32_t *>(out));
   note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
