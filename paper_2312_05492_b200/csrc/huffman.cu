@@ -570,7 +570,7 @@ __global__ void __launch_bounds__(ENC_NT, 3) k_enc_pack(const void *__restrict__
 constexpr u64 DEC_C = 1024;  // bits per chunk (32 words)
 
 struct DecSmem {
-  uint32_t lut[4096];
+  const uint32_t *lut;  // global, read through L1 (16 KB, hot)
   u64 first_code[33];
   uint32_t first_index[33];
   uint32_t counts[33];
@@ -579,7 +579,7 @@ struct DecSmem {
 };
 
 DEV void load_dec_smem(DecSmem &T, const DecTables *G, const uint16_t *sorted) {
-  for (int i = threadIdx.x; i < 4096; i += blockDim.x) T.lut[i] = G->lut[i];
+  if (threadIdx.x == 0) T.lut = G->lut;
   for (int i = threadIdx.x; i < 33; i += blockDim.x) {
     T.first_code[i] = G->first_code[i];
     T.first_index[i] = G->first_index[i];
@@ -626,7 +626,7 @@ struct BitReader {
 // and sets len (0 if no codeword of length <= 32 matches; the caller also
 // treats pos + len > nb as exhaustion) — _kernels.py:74-91.
 DEV uint32_t decode_at(const DecSmem &T, const uint16_t *sorted, uint32_t win, uint32_t &len) {
-  const uint32_t e = T.lut[win >> 20];
+  const uint32_t e = __ldg(T.lut + (win >> 20));
   if (e >> 16) {
     len = e >> 16;
     return e & 0xffffu;
@@ -911,24 +911,39 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_write(Stream s, const DecTables 
   SmemReader br;
   br.init();
   if (T.zrun) {
-    // Sparse path: the chunk's output range [k, k1) is first filled with
-    // the run symbol in 16-byte stores, then only the other symbols are
-    // stored (program order makes them win).  Runs cost O(1) each.
-    if (!active) return;
-    const u64 k1 = min(k + cnts[j], n);
+    // Sparse path: the warp's 32 chunks own the contiguous output range
+    // [k(lane 0), k1(lane 31)); the warp fills it with the run symbol in
+    // coalesced 16-byte stores, then each lane stores only the other
+    // symbols of its chunk (after __syncwarp, so they win).  Runs cost O(1).
+    const u64 k1 = active ? min(k + cnts[j], n) : k;
     const OutT zv = (sizeof(OutT) == 4) ? (OutT)((int32_t)T.zsym - R) : (OutT)T.zsym;
     constexpr int PER = 16 / sizeof(OutT);
-    u64 f = k;
-    for (; f < k1 && (f % PER); ++f) out[f] = zv;
-    uint4 zz;
     {
-      OutT tmp[PER];
+      u64 wa = active ? k : ~0ull, wb = active ? k1 : 0;
 #pragma unroll
-      for (int i = 0; i < PER; ++i) tmp[i] = zv;
-      zz = *reinterpret_cast<const uint4 *>(tmp);
+      for (int o = 16; o > 0; o >>= 1) {
+        wa = min(wa, __shfl_xor_sync(CSZI_FULL, wa, o));
+        wb = max(wb, __shfl_xor_sync(CSZI_FULL, wb, o));
+      }
+      if (wa < wb) {
+        uint4 zz;
+        OutT tmp[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) tmp[i] = zv;
+        memcpy(&zz, tmp, 16);
+        const u64 va = (wa + PER - 1) / PER, vb = wb / PER;  // whole vectors
+        if (va <= vb) {
+          for (u64 f = wa + lane; f < va * PER; f += 32) out[f] = zv;
+          for (u64 v = va + lane; v < vb; v += 32)
+            __stcs(reinterpret_cast<uint4 *>(out) + v, zz);
+          for (u64 f = vb * PER + lane; f < wb; f += 32) out[f] = zv;
+        } else {
+          for (u64 f = wa + lane; f < wb; f += 32) out[f] = zv;
+        }
+      }
     }
-    for (; f + PER <= k1; f += PER) __stcs(reinterpret_cast<uint4 *>(out + f), zz);
-    for (; f < k1; ++f) out[f] = zv;
+    __syncwarp();
+    if (!active) return;
     while (pos < end && k < k1) {
       const uint32_t w = br.peek(ss, pos);
       if (!(w >> 31)) {

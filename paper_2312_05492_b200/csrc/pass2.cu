@@ -422,52 +422,127 @@ __global__ void k_p2d_counts(u64 M, const uint8_t *E, const uint32_t *ctab, uint
   cnt[j] = c & ~OVR;
 }
 
-__global__ void __launch_bounds__(256) k_p2d_expand(const uint8_t *__restrict__ in, u64 n,
-                                                    const uint8_t *E, const u64 *off,
-                                                    uint8_t *__restrict__ out, u64 cap,
-                                                    cszi_ctl *ctl) {
-  __shared__ uint16_t ctrl[P2D_C];
-  __shared__ uint32_t cout_[P2D_C];
-  __shared__ int nctrl;
-  __shared__ u64 ws[9];
-  const u64 c0 = (u64)blockIdx.x * P2D_C;
-  const u64 cend = min(c0 + P2D_C, n);
-  if (threadIdx.x == 0) {
-    int k = 0;
-    u64 p = c0 + E[blockIdx.x];
-    while (p < cend) {
-      const uint32_t b = in[p];
-      ctrl[k] = (uint16_t)(p - c0);
-      const uint32_t o = b < 128 ? b + 1 : b - 127;
-      cout_[k] = o;
-      k++;
-      p += (b < 128) ? b + 2 : 1;
-    }
-    nctrl = k;
+// Expand: one warp per chunk.  The chunk's output range [off, off + cnt)
+// is zero-filled with coalesced 16-byte stores; the control chain is then
+// walked 32 bytes at a time: lane l holds byte l of the window, the chain
+// positions inside the window come from pointer jumping over the lanes
+// (5 shuffle rounds for the 1..16-step successors, 5 OR-reductions to mark
+// the positions reachable from the window's entry), a warp scan gives each
+// control its output offset, and only literal payload bytes are stored
+// (consecutive lanes -> consecutive output bytes).  A literal payload that
+// runs past the window (or past the chunk, <= 128 bytes) is carried.
+constexpr int P2X_WPB = 8;  // warps (chunks) per block
+__global__ void __launch_bounds__(P2X_WPB * 32) k_p2d_expand(const uint8_t *__restrict__ in,
+                                                            u64 n, const uint8_t *E,
+                                                            const u64 *off,
+                                                            const uint32_t *cnt,
+                                                            uint8_t *__restrict__ out, u64 cap,
+                                                            u64 M, cszi_ctl *ctl) {
+  const int lane = threadIdx.x & 31;
+  const u64 j = (u64)blockIdx.x * P2X_WPB + (threadIdx.x >> 5);
+  if (j >= M) return;
+  const u64 c0 = j * P2D_C;
+  const u64 cend = min(c0 + P2D_C, n);  // controls start below cend
+  u64 obase = off[j];
+  const u64 oend = obase + cnt[j];
+  if (oend > cap) {
+    if (lane == 0) atomicOr(&ctl->flags, (uint32_t)CSZI_F_CAPACITY);
+    return;
   }
-  __syncthreads();
-  const int nc = nctrl;
-  u64 carry = off[blockIdx.x];
-  for (int base = 0; base < nc; base += blockDim.x) {
-    const int k = base + threadIdx.x;
-    const u64 o = (k < nc) ? cout_[k] : 0;
-    u64 tot;
-    const u64 ex = block_excl_scan<256, u64>(o, ws, tot);
-    if (k < nc) {
-      const u64 dst = carry + ex;
-      const u64 src = c0 + ctrl[k];
-      const uint32_t b = in[src];
-      if (dst + o > cap) {
-        atomicOr(&ctl->flags, (uint32_t)CSZI_F_CAPACITY);
-      } else if (b < 128) {
-        const u64 avail = (src + 1 < n) ? n - (src + 1) : 0;
-        const u64 m = min((u64)o, avail);  // overrun already flagged Corrupt
-        for (u64 q = 0; q < m; ++q) out[dst + q] = in[src + 1 + q];
-      } else {
-        for (u64 q = 0; q < o; ++q) out[dst + q] = 0;
+  {  // zero fill
+    const u64 va = (obase + 15) / 16, vb = oend / 16;
+    if (va <= vb) {
+      for (u64 f = obase + lane; f < va * 16; f += 32) out[f] = 0;
+      for (u64 v = va + lane; v < vb; v += 32)
+        __stcs(reinterpret_cast<uint4 *>(out) + v, make_uint4(0, 0, 0, 0));
+      for (u64 f = vb * 16 + lane; f < oend; f += 32) out[f] = 0;
+    } else {
+      for (u64 f = obase + lane; f < oend; f += 32) out[f] = 0;
+    }
+  }
+  __syncwarp();
+  int cur = E[j];                 // next control, relative to the window start
+  u64 lit_lo = 0, lit_hi = 0;     // carried literal payload [lo, hi) (absolute)
+  u64 lit_dst = 0;                // output position of lit_lo
+  const u64 wend = min(c0 + P2D_C + 130, n);
+  for (u64 w0 = c0; w0 < wend; w0 += 32) {
+    if (cur >= 32 && lit_hi <= w0) {  // entry beyond this window and no payload:
+      cur -= 32;                     // (the previous chunk's spill) skip it
+      continue;
+    }
+    const u64 i = w0 + lane;
+    const uint32_t b = (i < n) ? (uint32_t)__ldg(in + i) : 0u;
+    const bool can_ctrl = i < cend;
+    // successor of a control at this lane (32 = leaves the window)
+    int nx = can_ctrl ? lane + (b < 128 ? (int)b + 2 : 1) : 32;
+    if (nx > 32) nx = 32;
+    int J[5];
+    J[0] = nx;
+#pragma unroll
+    for (int r = 1; r < 5; ++r) {
+      const int t = __shfl_sync(CSZI_FULL, J[r - 1], J[r - 1] & 31);
+      J[r] = (J[r - 1] < 32) ? t : 32;
+    }
+    uint32_t on = 0;
+    if (cur < 32) {
+      on = 1u << cur;
+#pragma unroll
+      for (int r = 4; r >= 0; --r) {
+        const uint32_t c = ((on >> lane) & 1u) && J[r] < 32 ? (1u << J[r]) : 0u;
+        on |= __reduce_or_sync(CSZI_FULL, c);
+      }
+      on &= __ballot_sync(CSZI_FULL, can_ctrl);
+    }
+    const bool is_ctrl = (on >> lane) & 1u;
+    const uint32_t o = is_ctrl ? (b < 128 ? b + 1 : b - 127) : 0u;
+    // exclusive scan of output counts
+    uint32_t inc = o;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(CSZI_FULL, inc, d);
+      if (lane >= d) inc += t;
+    }
+    const uint32_t excl = inc - o;
+    const uint32_t wtot = __shfl_sync(CSZI_FULL, inc, 31);
+    // literal payload bytes: governed by the last control before the lane
+    const uint32_t before = on & ((1u << lane) - 1u);
+    u64 dst = ~0ull;
+    const int cl = before ? 31 - __clz(before) : 0;
+    const uint32_t bcl = __shfl_sync(CSZI_FULL, b, cl);
+    const uint32_t excl_cl = __shfl_sync(CSZI_FULL, excl, cl);
+    if (!is_ctrl && i < n) {
+      if (before) {
+        if (bcl < 128 && (uint32_t)(lane - cl) <= bcl + 1u)
+          dst = obase + excl_cl + (u64)(lane - cl - 1);
+      } else if (i >= lit_lo && i < lit_hi) {
+        dst = lit_dst + (i - lit_lo);
       }
     }
-    carry += tot;
+    if (dst != ~0ull && dst < oend) out[dst] = (uint8_t)b;
+    // carry: the window's last control
+    u64 nabs;  // absolute position of the next control
+    if (on) {
+      const int L = 31 - __clz(on);
+      const uint32_t bL = __shfl_sync(CSZI_FULL, b, L);
+      const uint32_t exL = __shfl_sync(CSZI_FULL, excl, L);
+      if (bL < 128) {
+        lit_lo = w0 + L + 1;
+        lit_hi = w0 + L + 2 + bL;
+        lit_dst = obase + exL;
+      } else {
+        lit_lo = lit_hi = 0;
+      }
+      nabs = w0 + L + (bL < 128 ? bL + 2 : 1);
+    } else {
+      nabs = (cur >= (1 << 20)) ? cend : w0 + cur;
+    }
+    obase += wtot;
+    if (nabs >= cend) {  // the chain left the chunk: finish the carried payload
+      if (lit_hi <= w0 + 32) break;
+      cur = 1 << 20;     // no more controls; keep storing payload bytes
+    } else {
+      cur = (int)(nabs - (w0 + 32));
+    }
   }
 }
 
@@ -506,7 +581,11 @@ int launch_pass2_decode(const uint8_t *in, u64 n, uint8_t *out, u64 cap, void *s
   k_p2d_counts<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(M, E, ctab, cnt, ctl);
   note_launch();
   launch_excl_scan_u32(cnt, M, off, reinterpret_cast<u64 *>(&ctl->raw_len), scan_ws, st);
-  if (expand) { k_p2d_expand<<<(unsigned)M, 256, 0, st>>>(in, n, E, off, out, cap, ctl); note_launch(); }
+  if (expand) {
+    k_p2d_expand<<<(unsigned)((M + P2X_WPB - 1) / P2X_WPB), P2X_WPB * 32, 0, st>>>(
+        in, n, E, off, cnt, out, cap, M, ctl);
+    note_launch();
+  }
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 

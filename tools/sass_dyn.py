@@ -1,7 +1,7 @@
 """Join ncu per-SASS-instruction counts (--page source --print-source sass
 CSV) with nvdisasm -gi inline chains: dynamic instruction counts per source
 function.  Usage: sass_dyn.py ncu_sass.csv nvdisasm_dump kernel_substr src.cuh fn..."""
-import bisect, collections, csv, re, sys
+import bisect, collections, csv, os, re, sys
 csvf, dump, kern, src = sys.argv[1:5]
 want = sys.argv[5:]
 # static attribution: offset -> function
@@ -44,7 +44,7 @@ for r in rows:
         sec = r[1]; base = None; continue
     if r[0] == 'Address':
         hdr = r; continue
-    if sec is None or kern.split('_')[-1] not in sec: continue
+    if sec is None or os.environ.get('SEC', kern) not in sec: continue
     a = int(r[0], 16)
     if base is None: base = a
     off = a - base
