@@ -333,6 +333,7 @@ template <> struct EncSyms<0> {
 };
 template <> struct EncSyms<1> {
   uint32_t s[ENC_SPT];
+  uint32_t w[ENC_SPT / 2];  // unused (MODE 0 fast path only)
   DEV uint32_t get(int j) const { return s[j]; }
   DEV void load(const void *src, u64 n, int R, int nbins, u64 base, bool &unknown) {
     const int32_t *cp = reinterpret_cast<const int32_t *>(src) + base;
@@ -363,16 +364,23 @@ DEV void enc_load_lut(uint2 *lut, const uint8_t *lengths, const uint32_t *words,
 
 template <int MODE>
 DEV uint32_t enc_bits(const EncSyms<MODE> &sy, const uint2 *lut, int nbins, bool &unknown,
-                      uint32_t &outmask) {
+                      uint32_t &outmask, uint32_t zz2) {
   uint32_t nbits = 0;
   outmask = 0;
 #pragma unroll
-  for (int j = 0; j < ENC_SPT; ++j) {
-    const uint32_t s = sy.get(j);
-    const uint32_t l = lut[s].y;
-    unknown |= (l == 0) && (s != (uint32_t)nbins);
-    nbits += l;
-    if (MODE == 0) outmask |= (uint32_t)(s == 0) << j;
+  for (int j = 0; j < ENC_SPT; j += 2) {
+    if (MODE == 0 && sy.w[j >> 1] == zz2) {  // two 1-bit "0" codewords
+      nbits += 2;
+      continue;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t s = sy.get(j + h);
+      const uint32_t l = lut[s].y;
+      unknown |= (l == 0) && (s != (uint32_t)nbins);
+      nbits += l;
+      if (MODE == 0) outmask |= (uint32_t)(s == 0) << (j + h);
+    }
   }
   return nbits;
 }
@@ -391,6 +399,8 @@ __global__ void __launch_bounds__(ENC_NT) k_enc_count(const void *__restrict__ s
     const int sI = (MODE == 0 && i == 0) ? R : i;
     lut[i] = (i == nbins) ? 0u : ((uint32_t)lengths[sI] | ((MODE == 0 && i == 0) ? 0x10000u : 0u));
   }
+  const uint32_t zz2 = (MODE == 0 && lengths[R] == 1) ? ((uint32_t)R | ((uint32_t)R << 16))
+                                                     : 0xffffffffu;
   __syncthreads();
   bool unknown = false;
   const u64 stride = (u64)gridDim.x * ENC_NW;
@@ -403,12 +413,19 @@ __global__ void __launch_bounds__(ENC_NT) k_enc_count(const void *__restrict__ s
     if (cn < nch) nx.load(src, n, R, nbins, cn * ENC_CH + (u64)lane * ENC_SPT, unknown);
     uint32_t acc = 0;
 #pragma unroll
-    for (int j = 0; j < ENC_SPT; ++j) {
-      const uint32_t e = lut[sy.get(j)];
-      // MODE 1: a symbol inside the code range without a codeword; MODE 0
-      // symbols come from the predictor whose histogram built the codebook
-      if (MODE == 1) unknown |= (e == 0) && (sy.get(j) != (uint32_t)nbins);
-      acc += e;
+    for (int j = 0; j < ENC_SPT; j += 2) {
+      if (MODE == 0 && sy.w[j >> 1] == zz2) {  // two 1-bit "0" codewords
+        acc += 2;
+        continue;
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t e = lut[sy.get(j + h)];
+        // MODE 1: a symbol inside the code range without a codeword; MODE 0
+        // symbols come from the predictor whose histogram built the codebook
+        if (MODE == 1) unknown |= (e == 0) && (sy.get(j + h) != (uint32_t)nbins);
+        acc += e;
+      }
     }
     acc = warp_sum(acc);
     if (lane == 0) {
@@ -484,6 +501,10 @@ __global__ void __launch_bounds__(ENC_NT, 3) k_enc_pack(const void *__restrict__
   uint32_t *stage = reinterpret_cast<uint32_t *>(lut + nbins + 2) + warp * ENC_SW;
   enc_load_lut<MODE>(lut, lengths, words, R);
   for (int i = lane; i < ENC_SW; i += 32) stage[i] = 0u;
+  // R coded as the 1-bit "0" (the usual case): pairs of R take the fast path
+  const uint32_t zz2 = (MODE == 0 && lengths[R] == 1 && words[R] == 0)
+                           ? ((uint32_t)R | ((uint32_t)R << 16))
+                           : 0xffffffffu;
   __syncthreads();
   bool unknown = false;  // reported by k_enc_count
   bool cap_hit = false;
@@ -498,25 +519,46 @@ __global__ void __launch_bounds__(ENC_NT, 3) k_enc_pack(const void *__restrict__
     const u64 tb = S.bit_off[c];
     const u64 ob = (MODE == 0) ? S.out_off[c] : 0;
     uint32_t outmask;
-    const uint32_t nbits = enc_bits<MODE>(sy, lut, nbins, unknown, outmask);
+    const uint32_t nbits = enc_bits<MODE>(sy, lut, nbins, unknown, outmask, zz2);
     const uint32_t incl = warp_incl_scan(nbits);
     const uint32_t bexcl = incl - nbits;
     const uint32_t tot_bits = __shfl_sync(CSZI_FULL, incl, 31);
-    {  // pack at chunk-relative bit offsets
+    {  // pack at chunk-relative bit offsets (staging words start zeroed, so
+       // all-zero words need no store)
       uint32_t w = bexcl >> 5;
       uint32_t nb = bexcl & 31;
       u64 acc = 0;
 #pragma unroll
-      for (int j = 0; j < ENC_SPT; ++j) {
-        const uint2 e = lut[sy.get(j)];
-        acc = (acc << e.y) | (u64)e.x;
-        nb += e.y;
+      for (int j = 0; j < ENC_SPT; j += 2) {
+        if (MODE == 0 && sy.w[j >> 1] == zz2) {
+          acc <<= 2;
+          nb += 2;
+        } else {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint2 e = lut[sy.get(j + h)];
+            acc = (acc << e.y) | (u64)e.x;
+            nb += e.y;
+            if (nb >= 32) {
+              nb -= 32;
+              const uint32_t v = (uint32_t)(acc >> nb);
+              if (v) atomicOr(&stage[w], v);
+              w++;
+            }
+          }
+          continue;
+        }
         if (nb >= 32) {
           nb -= 32;
-          atomicOr(&stage[w++], (uint32_t)(acc >> nb));
+          const uint32_t v = (uint32_t)(acc >> nb);
+          if (v) atomicOr(&stage[w], v);
+          w++;
         }
       }
-      if (nb > 0) atomicOr(&stage[w], (uint32_t)(acc << (32 - nb)));
+      if (nb > 0) {
+        const uint32_t v = (uint32_t)(acc << (32 - nb));
+        if (v) atomicOr(&stage[w], v);
+      }
     }
     if (MODE == 0 && __any_sync(CSZI_FULL, outmask != 0)) {
       const uint32_t no = (uint32_t)__popc(outmask);

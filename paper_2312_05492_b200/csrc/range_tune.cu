@@ -35,21 +35,43 @@ __global__ void __launch_bounds__(256) k_range(const float *__restrict__ x, uint
   const bool aligned = ((uintptr_t)x & 15) == 0;
   u64 done = 0;
   if (aligned) {
+    // two float4 per iteration in flight; keys of non-finite values enter the
+    // min/max too (the caller raises NonFiniteValue before using the range),
+    // so the exact first index is only computed on the rare bad vector
     const u64 n4 = n / 4;
     const float4 *x4 = reinterpret_cast<const float4 *>(x);
-    for (u64 i = tid; i < n4; i += nthr) {
-      const float4 v = __ldcs(x4 + i);  // streamed: read once
+    constexpr uint32_t EXP = 0x7f800000u;
+    u64 i = tid;
+    for (; i + nthr < n4; i += 2 * nthr) {
+      const float4 va = __ldcs(x4 + i);
+      const float4 vb = __ldcs(x4 + i + nthr);
+      const uint32_t b[8] = {__float_as_uint(va.x), __float_as_uint(va.y), __float_as_uint(va.z),
+                             __float_as_uint(va.w), __float_as_uint(vb.x), __float_as_uint(vb.y),
+                             __float_as_uint(vb.z), __float_as_uint(vb.w)};
+      bool nf = false;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        nf |= (b[j] & EXP) == EXP;
+        const uint32_t k = b[j] ^ ((uint32_t)((int32_t)b[j] >> 31) | 0x80000000u);
+        kmin = min(kmin, k);
+        kmax = max(kmax, k);
+      }
+      if (nf) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if ((b[j] & EXP) == EXP) bad = min(bad, 4 * (j < 4 ? i : i + nthr) + (j & 3));
+      }
+    }
+    for (; i < n4; i += nthr) {
+      const float4 v = __ldcs(x4 + i);
       const float a[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const uint32_t b = __float_as_uint(a[j]);
-        if ((b & 0x7f800000u) == 0x7f800000u) {
-          bad = min(bad, 4 * i + j);
-        } else {
-          const uint32_t k = float_key(a[j]);
-          kmin = min(kmin, k);
-          kmax = max(kmax, k);
-        }
+        if ((b & EXP) == EXP) bad = min(bad, 4 * i + j);
+        const uint32_t k = float_key(a[j]);
+        kmin = min(kmin, k);
+        kmax = max(kmax, k);
       }
     }
     done = n4 * 4;
