@@ -358,7 +358,7 @@ def run_ours(args, rank, world, local):
         "archive_bytes": blob_len,
         "roofline": {
             "bound": "hbm",
-            "kernel": "k_predict (fused G-Interp predict+quantize+histogram)",
+            "kernel": "t3::k_t3_predict (warp-per-tile fused G-Interp predict+quantize+histogram)",
             "achieved": round(achieved, 2),
             "peak": peak,
             "peak_kind": peak_kind,
