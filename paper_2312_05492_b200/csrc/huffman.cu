@@ -293,6 +293,7 @@ constexpr int ENC_CH = 32 * ENC_SPT;
 constexpr int ENC_SW = ENC_CH + 2;  // staged words per warp (max 32 bits per symbol)
 
 struct EncScratch {
+  uint16_t *lane_pre;  // per chunk, per lane: bit offset of the lane inside the chunk
   uint32_t *ch_bits;
   uint32_t *ch_out;
   u64 *bit_off;
@@ -427,10 +428,13 @@ __global__ void __launch_bounds__(ENC_NT) k_enc_count(const void *__restrict__ s
         acc += e;
       }
     }
-    acc = warp_sum(acc);
-    if (lane == 0) {
-      S.ch_bits[c] = acc & 0xffffu;
-      S.ch_out[c] = acc >> 16;
+    // lane offsets inside the chunk (bits < 2^15 per chunk: u16) for the
+    // sparse packer, chunk totals for the scan
+    const uint32_t incl = warp_incl_scan(acc);
+    if (MODE == 0) S.lane_pre[c * 32 + lane] = (uint16_t)((incl - acc) & 0xffffu);
+    if (lane == 31) {
+      S.ch_bits[c] = incl & 0xffffu;
+      S.ch_out[c] = incl >> 16;
     }
     sy = nx;
     c = cn;
@@ -486,6 +490,111 @@ __global__ void __launch_bounds__(PS_NT) k_scan_pair(EncScratch S, u64 nch, int 
   }
 }
 
+// Sparse stream (MODE 0): R owns the 1-bit "0" codeword and at most n/8
+// symbols are not R (every other codeword has >= 2 bits, so bits - n bounds
+// their count).  The stream is then zeroed and only the codewords holding
+// 1-bits are ORed in at their offsets (k_enc_sparse); otherwise k_enc_pack
+// packs every chunk.  Both kernels evaluate the same predicate on device.
+DEV bool enc_sparse(const uint8_t *lengths, const uint32_t *words, int R, u64 n,
+                    const cszi_ctl *ctl) {
+  const u64 bits = ctl->bits;
+  return lengths[R] == 1 && words[R] == 0 && bits >= n && (bits - n) <= n / 8;
+}
+
+__global__ void k_enc_zero(const uint8_t *lengths, const uint32_t *words, int R, u64 n,
+                           uint32_t *out, u64 cap_words, const cszi_ctl *ctl) {
+  if (!enc_sparse(lengths, words, R, n, ctl)) return;
+  u64 nw = (ctl->bits + 31) / 32 + 1;
+  if (nw > cap_words) nw = cap_words;
+  uint4 *o4 = reinterpret_cast<uint4 *>(out);
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nw / 4;
+       i += (u64)gridDim.x * blockDim.x)
+    o4[i] = make_uint4(0, 0, 0, 0);
+  for (u64 i = (nw / 4) * 4 + blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nw;
+       i += (u64)gridDim.x * blockDim.x)
+    out[i] = 0u;
+}
+
+// OR one codeword (word, len) into the zeroed MSB-first stream at bit pos.
+DEV void sp_put(uint32_t *out, u64 cap_words, u64 pos, uint32_t word, uint32_t len,
+                bool &cap_hit) {
+  const u64 w = pos >> 5;
+  const uint32_t off = (uint32_t)(pos & 31);
+  if (w + 1 >= cap_words) {
+    cap_hit = true;
+  } else if (off + len <= 32) {
+    atomicOr(out + w, bswap32(word << (32 - off - len)));
+  } else {
+    const uint32_t sh = off + len - 32;  // bits spilling into word w + 1
+    atomicOr(out + w, bswap32(word >> sh));
+    atomicOr(out + w + 1, bswap32(word << (32 - sh)));
+  }
+}
+
+__global__ void __launch_bounds__(ENC_NT, 3) k_enc_sparse(const uint16_t *__restrict__ src, u64 n,
+                                                          int R, const uint8_t *__restrict__ lengths,
+                                                          const uint32_t *__restrict__ words,
+                                                          uint32_t *__restrict__ out, u64 cap_words,
+                                                          const float *__restrict__ xval,
+                                                          u64 *o_idx, float *o_val, u64 o_cap,
+                                                          EncScratch S, u64 nch, u64 idx_offset,
+                                                          cszi_ctl *ctl) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  if (!enc_sparse(lengths, words, R, n, ctl)) return;
+  const int nbins = 2 * R;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint2 *lut = reinterpret_cast<uint2 *>(sm_raw);
+  enc_load_lut<0>(lut, lengths, words, R);
+  const uint32_t zz2 = (uint32_t)R | ((uint32_t)R << 16);
+  __syncthreads();
+  bool unknown = false, cap_hit = false;
+  const u64 stride = (u64)gridDim.x * ENC_NW;
+  u64 c = (u64)blockIdx.x * ENC_NW + warp;
+  EncSyms<0> sy;
+  if (c < nch) sy.load(src, n, R, nbins, c * ENC_CH + (u64)lane * ENC_SPT, unknown);
+  while (c < nch) {
+    const u64 cn = c + stride;
+    EncSyms<0> nx;
+    if (cn < nch) nx.load(src, n, R, nbins, cn * ENC_CH + (u64)lane * ENC_SPT, unknown);
+    const u64 ob = S.out_off[c];
+    u64 pos = S.bit_off[c] + S.lane_pre[c * 32 + lane];
+    uint32_t outmask = 0;
+#pragma unroll
+    for (int j = 0; j < ENC_SPT; j += 2) {
+      if (sy.w[j >> 1] == zz2) {
+        pos += 2;
+        continue;
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t s = sy.get(j + h);
+        const uint2 e = lut[s];
+        outmask |= (uint32_t)(s == 0) << (j + h);
+        if (e.x) sp_put(out, cap_words, pos, e.x, e.y, cap_hit);
+        pos += e.y;
+      }
+    }
+    if (__any_sync(CSZI_FULL, outmask != 0)) {
+      const uint32_t no = (uint32_t)__popc(outmask);
+      u64 k = ob + (warp_incl_scan(no) - no);
+      const u64 base = c * ENC_CH + (u64)lane * ENC_SPT;
+      for (uint32_t mm = outmask; mm; mm &= mm - 1) {
+        const u64 gi = base + (__ffs(mm) - 1);
+        if (k < o_cap) {
+          o_idx[k] = gi + idx_offset;
+          o_val[k] = xval[gi];
+        } else {
+          cap_hit = true;
+        }
+        k++;
+      }
+    }
+    sy = nx;
+    c = cn;
+  }
+  if (cap_hit) atomicOr(&ctl->flags, (uint32_t)CSZI_F_CAPACITY);
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(ENC_NT, 3) k_enc_pack(const void *__restrict__ src, u64 n, int R,
                                                        const uint8_t *__restrict__ lengths,
@@ -495,6 +604,7 @@ __global__ void __launch_bounds__(ENC_NT, 3) k_enc_pack(const void *__restrict__
                                                        float *o_val, u64 o_cap, EncScratch S,
                                                        u64 nch, u64 idx_offset, cszi_ctl *ctl) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
+  if (MODE == 0 && enc_sparse(lengths, words, R, n, ctl)) return;  // k_enc_sparse's case
   const int nbins = 2 * R;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint2 *lut = reinterpret_cast<uint2 *>(sm_raw);
@@ -1132,7 +1242,7 @@ int launch_pack_outliers(const u64 *idx, const float *val, u64 k, uint8_t *out,
 u64 enc_scratch_bytes(u64 n) {
   const u64 nc = (n + ENC_CH - 1) / ENC_CH + 2;
   const u64 nt = (nc + PS_TILE - 1) / PS_TILE + 2;
-  return nc * (4 + 4 + 8 + 8) + nt * 16 + 64;
+  return nc * (4 + 4 + 8 + 8 + 2 * 32) + nt * 16 + 64;
 }
 
 // mode 0: uint16 symbols with outlier sentinel; mode 1: int32 codes
@@ -1154,6 +1264,7 @@ int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *length
   S.out_off = S.bit_off + nc;
   S.ch_bits = reinterpret_cast<uint32_t *>(S.out_off + nc);
   S.ch_out = S.ch_bits + nc;
+  S.lane_pre = reinterpret_cast<uint16_t *>(S.ch_out + nc);
   cudaMemsetAsync(p, 0, (size_t)(nt * 16 + 16), st);
   const int nbins = 2 * R;
   int dev = 0, sms = 148, per_sm = 1;
@@ -1178,6 +1289,19 @@ int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *length
                                                xval, o_idx, o_val, o_cap, S, nch, idx_offset,
                                                ctl);
   note_launch(3);
+  if (mode == 0) {
+    // sparse alternative (each kernel checks the same device-side predicate)
+    k_enc_zero<<<(unsigned)(sms * 4), 256, 0, st>>>(lengths, words, R, n, out, cap_bytes / 4, ctl);
+    const size_t smem_s = sizeof(uint2) * (nbins + 2) + 16;
+    cudaFuncSetAttribute(k_enc_sparse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_enc_sparse, ENC_NT, smem_s);
+    blocks = (u64)sms * (per_sm < 1 ? 1 : per_sm);
+    if (blocks > wblocks) blocks = wblocks;
+    k_enc_sparse<<<(unsigned)blocks, ENC_NT, smem_s, st>>>(
+        reinterpret_cast<const uint16_t *>(src), n, R, lengths, words, out, cap_bytes / 4, xval,
+        o_idx, o_val, o_cap, S, nch, idx_offset, ctl);
+    note_launch(2);
+  }
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
