@@ -809,6 +809,12 @@ DEV int next_tile(unsigned int *q) {
   if ((threadIdx.x & 31) == 0) t = (int)atomicAdd(q, 1u);
   return __shfl_sync(CSZI_FULL, t, 0);
 }
+// split form: the ticket is requested when a tile starts and read after its
+// passes, so the atomic's round trip hides under the tile's work
+DEV unsigned int ticket_issue(unsigned int *q) {
+  return ((threadIdx.x & 31) == 0) ? atomicAdd(q, 1u) : 0u;
+}
+DEV int ticket_read(unsigned int raw) { return (int)__shfl_sync(CSZI_FULL, raw, 0); }
 DEV void sched_done(unsigned int *q) {
   if ((threadIdx.x & 31) == 0) {
     __threadfence();
@@ -889,10 +895,11 @@ __global__ void __launch_bounds__(NT, 3)
       stage_manual_f32(buf, x, G, o);
     }
     __syncwarp();
+    const unsigned int raw = ticket_issue(q);
     if (T.bnd) run_levels<0, true>(T, C, R, exact, O);
     else run_levels<0, false>(T, C, R, exact, O);
     // staging buffer free: prefetch the next tile
-    const int tn = next_tile(q);
+    const int tn = ticket_read(raw);
     if (lane == 0 && tn < ntiles && G.tma) {
       int on[3];
       tile_of(G, nint, tn, on);
@@ -1038,9 +1045,10 @@ __global__ void __launch_bounds__(NT, 3)
       stage_manual_u16(syms, sym, G, o);
     }
     __syncwarp();
+    const unsigned int raw = ticket_issue(q);
     if (T.bnd) run_levels<1, true>(T, C, R, false, O);
     else run_levels<1, false>(T, C, R, false, O);
-    const int tn = next_tile(q);
+    const int tn = ticket_read(raw);
     if (lane == 0 && tn < ntiles && G.tma) {
       int on[3];
       tile_of(G, nint, tn, on);
