@@ -291,8 +291,15 @@ def to_device_u8(data) -> "object":
         if data.dtype != t.uint8:
             data = data.view(t.uint8)
         return data.contiguous().cuda()
-    arr = np.frombuffer(bytes(data), dtype=np.uint8) if not isinstance(data, np.ndarray) else data
+    if isinstance(data, np.ndarray):
+        arr = np.ascontiguousarray(data).view(np.uint8).reshape(-1)
+    else:
+        # bytearray keeps the buffer writable (torch.from_numpy rejects
+        # read-only memory with a warning); one host copy of the payload
+        arr = np.frombuffer(bytearray(data), dtype=np.uint8)
     out = t.empty(max(arr.size, 1), dtype=t.uint8, device="cuda")
     if arr.size:
-        out[: arr.size].copy_(t.from_numpy(np.ascontiguousarray(arr)), non_blocking=False)
+        if not arr.flags.writeable:
+            arr = arr.copy()
+        out[: arr.size].copy_(t.from_numpy(arr), non_blocking=False)
     return out[: arr.size] if arr.size else out[:0]
