@@ -1023,7 +1023,14 @@ __global__ void __launch_bounds__(NT, 3)
       for (int i = lane; i < NBUF / 4; i += 32) sts_f4(buf + 16u * i, make_float4(0.f, 0.f, 0.f, 0.f));
     __syncwarp();
     // seed the anchors of the closed tile (multiples of 8, plus ext - 1)
-    {
+    if (!T.bnd) {
+      // interior: z, y in {0, 8}, x in {0, 8, 16, 24, 32}; no closing anchors
+      if (lane < 20) {
+        const int iz = lane / 10, iy = (lane / 5) & 1, ix = lane % 5;
+        const int64_t kz = o[0] / 8 + iz, ky = o[1] / 8 + iy, kx = o[2] / 8 + ix;
+        sts_f(bufa(T, 8 * iz, 8 * iy, 8 * ix), __ldg(anchors + (kz * G.na1 + ky) * G.na2 + kx));
+      }
+    } else {
       int az[3], ay[3], ax[6];
       const int nz = anchor_axis_local<CZ, 8>(T.e[0], az);
       const int ny = anchor_axis_local<CY, 8>(T.e[1], ay);
