@@ -679,6 +679,15 @@ DEV void run_pass(const Tile &T, int s, int D, int passed, bool nak, const Lv &L
   }
 }
 
+#ifdef T3_PROF
+// per-phase cycle counters (tools/microbench/t3_phases.py; build with
+// make EXTRA=-DT3_PROF OUT=...): [0] setup [1] TMA wait [2] passes
+// [3] epilogue [4] tiles [6 + 3 lv + i] interior pass (lv, i)
+__device__ unsigned long long g_t3_prof[16];
+#define T3P_CLOCK(v) const long long v = clock64()
+#else
+#define T3P_CLOCK(v)
+#endif
 struct Cfg {  // tuned configuration (per-CTA / per-warp copy)
   Lv lv[3];
   int order[3];
@@ -695,9 +704,14 @@ DEV void run_levels(const Tile &T, const Cfg &C, int R, bool exact, const Out &O
 #pragma unroll 1
     for (int i = 0; i < 3; ++i) {
       const int D = C.order[i];
+      T3P_CLOCK(q0);
       run_pass<MODE, BND>(T, s, D, passed, C.nak[D] != 0, L, R, exact, O);
       passed |= 1 << D;
       __syncwarp();
+#ifdef T3_PROF
+      if (MODE == 0 && !BND && (threadIdx.x & 31) == 0)
+        atomicAdd(&g_t3_prof[6 + lv * 3 + i], (unsigned long long)(clock64() - q0));
+#endif
     }
   }
 }
@@ -878,7 +892,11 @@ __global__ void __launch_bounds__(NT, 3)
   const int64_t pz = (int64_t)G.ext[1] * G.ext[2];
   const int py = G.ext[2];
   uint32_t zeros = 0, phase = 0;
+#ifdef T3_PROF
+  unsigned long long pc[5] = {0, 0, 0, 0, 0};
+#endif
   while (t < ntiles) {
+    T3P_CLOCK(c0);
     int o[3];
     tile_of(G, nint, t, o);
     Tile T;
@@ -888,6 +906,7 @@ __global__ void __launch_bounds__(NT, 3)
     tile_init(T, G, o, t >= nint);
     // codes default to R (anchors: code 0, predictor.py:414)
     for (int i = lane; i < NCODE / 8; i += 32) sts_u4(codes + 16u * i, make_uint4(rr, rr, rr, rr));
+    T3P_CLOCK(c1);
     if (G.tma) {
       mbar_wait(&mbar[warp], phase);
       phase ^= 1;
@@ -895,9 +914,11 @@ __global__ void __launch_bounds__(NT, 3)
       stage_manual_f32(buf, x, G, o);
     }
     __syncwarp();
+    T3P_CLOCK(c2);
     const unsigned int raw = ticket_issue(q);
     if (T.bnd) run_levels<0, true>(T, C, R, exact, O);
     else run_levels<0, false>(T, C, R, exact, O);
+    T3P_CLOCK(c3);
     // staging buffer free: prefetch the next tile
     const int tn = ticket_read(raw);
     if (lane == 0 && tn < ntiles && G.tma) {
@@ -952,8 +973,19 @@ __global__ void __launch_bounds__(NT, 3)
       }
     }
     __syncwarp();  // codes read before the next tile resets them
+#ifdef T3_PROF
+    pc[0] += c1 - c0;
+    pc[1] += c2 - c1;
+    pc[2] += c3 - c2;
+    pc[3] += clock64() - c3;
+    pc[4] += 1;
+#endif
     t = tn;
   }
+#ifdef T3_PROF
+  if (lane == 0)
+    for (int i = 0; i < 5; ++i) atomicAdd(&g_t3_prof[i], pc[i]);
+#endif
   sched_done(q);
   zeros = warp_sum(zeros);
   if (lane == 0) zero_ws[warp] = zeros;
@@ -1230,3 +1262,12 @@ static int launch_recon_t3(const uint16_t *sym, const float *anchors, const u64 
 
 }  // namespace t3
 }  // namespace cszi
+
+#ifdef T3_PROF
+extern "C" int cszi_t3_prof(unsigned long long *out) {  // read and reset
+  cudaMemcpyFromSymbol(out, cszi::t3::g_t3_prof, sizeof(unsigned long long) * 16);
+  const unsigned long long z[16] = {0};
+  cudaMemcpyToSymbol(cszi::t3::g_t3_prof, z, sizeof(z));
+  return 0;
+}
+#endif
