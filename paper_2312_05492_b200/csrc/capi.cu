@@ -69,7 +69,7 @@ __global__ void k_ctl_reset_outputs(cszi_ctl *ctl) {
 // outlier section (archive.py:184-189: u64 count + packed (u64, f32)).
 __global__ void k_assemble(uint8_t *raw, u64 head, const uint8_t *bits, const u64 *oidx,
                            const float *oval, u64 raw_cap, u64 bits_cap, u64 o_cap,
-                           cszi_ctl *ctl, int is_payload) {
+                           cszi_ctl *ctl, int is_payload, int bits_in_place) {
   const u64 nbits = ctl->bits;
   const u64 k = ctl->n_outliers;
   const u64 nbytes = (nbits + 7) / 8;
@@ -82,7 +82,8 @@ __global__ void k_assemble(uint8_t *raw, u64 head, const uint8_t *bits, const u6
   const u64 nthr = (u64)gridDim.x * blockDim.x;
   // bitstream: 16-byte chunks where possible
   uint8_t *dst = raw + head;
-  for (u64 i = tid; i < nbytes; i += nthr) dst[i] = bits[i];
+  if (!bits_in_place)
+    for (u64 i = tid; i < nbytes; i += nthr) dst[i] = bits[i];
   uint8_t *os = raw + head + nbytes;
   if (tid < 8) os[tid] = (uint8_t)(k >> (8 * tid));
   for (u64 r = tid; r < k; r += nthr) {
@@ -310,12 +311,17 @@ int cszi_compress(const float *x, const cszi_geom *g, const cszi_params *p,
   CK(launch_gather_anchors(x, g, reinterpret_cast<float *>(raw), st));
   uint8_t *lengths = raw + 4 * na;  // the codebook section is the length table
   CK(launch_codebook(W.hist, (int)nbins, lengths, W.words, ctl, st));
-  CK(launch_encode(0, W.sym, n, R, lengths, W.words, W.bits, caps->bits_cap, x, W.oidx, W.oval,
-                   caps->outlier_cap, W.enc_scratch, ctl, st, 0));
   const u64 head = 4 * na + nbins;
+  // the bitstream is packed straight into its section when the section is
+  // word-aligned (R even); otherwise into W.bits and copied by k_assemble
+  const bool in_place = ((reinterpret_cast<uintptr_t>(raw) + head) & 3) == 0;
+  uint32_t *bits_out = in_place ? reinterpret_cast<uint32_t *>(raw + head) : W.bits;
+  CK(launch_encode(0, W.sym, n, R, lengths, W.words, bits_out, caps->bits_cap, x, W.oidx, W.oval,
+                   caps->outlier_cap, W.enc_scratch, ctl, st, 0));
   k_assemble<<<grid_for(n / 16), 256, 0, st>>>(raw, head, reinterpret_cast<uint8_t *>(W.bits),
                                                 W.oidx, W.oval, raw_cap, caps->bits_cap,
-                                                caps->outlier_cap, ctl, pass2 ? 0 : 1);
+                                                caps->outlier_cap, ctl, pass2 ? 0 : 1,
+                                                in_place ? 1 : 0);
   note_launch();
   if (pass2) CK(launch_pass2_encode(raw, reinterpret_cast<const u64 *>(&ctl->raw_len), raw_cap, payload, W.p2_scratch, ctl, st));
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;

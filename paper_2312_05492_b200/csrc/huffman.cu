@@ -506,13 +506,15 @@ __global__ void k_enc_zero(const uint8_t *lengths, const uint32_t *words, int R,
   if (!enc_sparse(lengths, words, R, n, ctl)) return;
   u64 nw = (ctl->bits + 31) / 32 + 1;
   if (nw > cap_words) nw = cap_words;
-  uint4 *o4 = reinterpret_cast<uint4 *>(out);
-  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nw / 4;
-       i += (u64)gridDim.x * blockDim.x)
-    o4[i] = make_uint4(0, 0, 0, 0);
-  for (u64 i = (nw / 4) * 4 + blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nw;
-       i += (u64)gridDim.x * blockDim.x)
-    out[i] = 0u;
+  // words up to the first 16-byte boundary, then 16-byte stores
+  const u64 lead = min((u64)(((16 - (reinterpret_cast<uintptr_t>(out) & 15)) & 15) / 4), nw);
+  const u64 tid = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+  const u64 nthr = (u64)gridDim.x * blockDim.x;
+  if (tid < lead) out[tid] = 0u;
+  uint4 *o4 = reinterpret_cast<uint4 *>(out + lead);
+  const u64 nv = (nw - lead) / 4;
+  for (u64 i = tid; i < nv; i += nthr) o4[i] = make_uint4(0, 0, 0, 0);
+  for (u64 i = lead + nv * 4 + tid; i < nw; i += nthr) out[i] = 0u;
 }
 
 // OR one codeword (word, len) into the zeroed MSB-first stream at bit pos.

@@ -66,6 +66,7 @@ def test_outlier_heavy_and_exact_paths():
     blob = _round_trip_equals_oracle(data, 1e-6)  # most points are outliers
     assert len(P.parse_archive(blob).outliers) > 8
     _round_trip_equals_oracle(data, 1e-3, mode="abs", quant_radius=4)  # |q| >= R often
+    _round_trip_equals_oracle(data, 1e-3, quant_radius=7)  # odd R: bitstream not word-aligned
     g = P.Grid(P.Dims(data.shape), data)
     a = P.compress_device(g, 1e-4, exact=True).to_bytes()
     assert a == O.compress(data, 1e-4)
