@@ -35,3 +35,16 @@ for name, fn in [("H2D pinned", lambda: pin.to('cuda', non_blocking=True)),
         r = fn()
     torch.cuda.synchronize(); t1 = time.perf_counter()
     print(f"{name} {1e3*(t1-t0)/N:.2f} ms")
+
+# the bench's e2e loop pattern (events on the current stream, result kept alive)
+ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+for steps in (10, 50):
+    torch.cuda.synchronize()
+    ev0.record()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        back = P.decompress(blob)
+    ev1.record()
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    print(f"bench-pattern decompress x{steps}: events {ev0.elapsed_time(ev1)/steps:.2f} ms, wall {1e3*(t1-t0)/steps:.2f} ms")
