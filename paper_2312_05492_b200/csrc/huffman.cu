@@ -721,7 +721,7 @@ __global__ void __launch_bounds__(ENC_NT, 3) k_enc_pack(const void *__restrict__
 // ---------------------------------------------------------------------------
 // decode: self-synchronising chunked decode of one stream
 // ---------------------------------------------------------------------------
-constexpr u64 DEC_C = 1024;  // bits per chunk (32 words)
+constexpr u64 DEC_C = 256;  // bits per chunk (8 words)
 
 struct DecSmem {
   const uint32_t *lut;  // global, read through L1 (16 KB, hot)
