@@ -363,7 +363,7 @@ int launch_pass2_encode(const uint8_t *in, const u64 *Np, u64 cap_n, uint8_t *ou
 // ---------------------------------------------------------------------------
 // decode
 // ---------------------------------------------------------------------------
-constexpr int P2D_C = 2048;
+constexpr int P2D_C = 1024;
 constexpr int P2D_D = 129;           // entry offsets 0..128
 constexpr int P2D_P = P2D_C + 130;   // local positions incl. spill
 constexpr uint32_t OVR = 0x80000000u;
