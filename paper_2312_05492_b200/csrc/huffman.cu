@@ -840,6 +840,9 @@ struct SmemReader {
   }
 };
 
+// canonical (huffman.py:128-160): a single length-1 codeword is "0"
+DEV bool zrun_tables(const DecTables *G) { return G->counts[1] == 1 && G->first_code[1] == 0; }
+
 // Phase 1: speculative decode of chunk j from its first bit.
 __global__ void __launch_bounds__(DEC_NT) k_dec_spec(Stream s, const DecTables *G,
                                                     const uint16_t *sorted, u64 M, u64 *spec_exit,
@@ -1048,6 +1051,7 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_write(Stream s, const DecTables 
                                                      const uint16_t *sorted, u64 M, const u64 *X,
                                                      const u64 *off, const uint32_t *cnts,
                                                      u64 n, int R, OutT *__restrict__ out) {
+  if (zrun_tables(G)) return;  // zero-run streams: k_dec_write_zr
   __shared__ DecSmem T;
   __shared__ uint32_t sw[DEC_SW];
   constexpr int K = (sizeof(OutT) == 2) ? DEC_K : DEC_K / 2;
@@ -1064,7 +1068,70 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_write(Stream s, const DecTables 
   bool active = j < M && k < n;
   SmemReader br;
   br.init();
-  if (T.zrun) {
+  if (T.zrun) return;  // zero-run streams: k_dec_write_zr
+  while (__any_sync(CSZI_FULL, active)) {
+    int cnt = 0;
+    if (active) {
+      while (cnt < K && pos < end && k + cnt < n) {
+        const uint32_t w = br.peek(ss, pos);
+        if (T.zrun && !(w >> 31)) {  // run of the "0" codeword
+          u64 adv = min((u64)__clz(w), end - pos);
+          adv = min(adv, (u64)(K - cnt));
+          adv = min(adv, n - k - cnt);
+          const OutT zv = (sizeof(OutT) == 4) ? (OutT)((int32_t)T.zsym - R) : (OutT)T.zsym;
+          for (int i = 0; i < (int)adv; ++i) ob[warp][lane][cnt + i] = zv;
+          cnt += (int)adv;
+          pos += adv;
+          continue;
+        }
+        uint32_t len;
+        const uint32_t sym = decode_at(T, sorted, w, len);
+        if (len == 0 || pos + len > s.nb) {
+          pos = end;  // dead chain: truncation is reported by k_dec_check
+          break;
+        }
+        pos += len;
+        ob[warp][lane][cnt++] = (sizeof(OutT) == 4) ? (OutT)((int32_t)sym - R) : (OutT)sym;
+      }
+    }
+    __syncwarp();
+    for (int i = 0; i < 32; ++i) {
+      const int ci = __shfl_sync(CSZI_FULL, cnt, i);
+      const u64 ki = __shfl_sync(CSZI_FULL, k, i);
+      if (lane < ci) out[ki + lane] = ob[warp][i][lane];
+    }
+    __syncwarp();
+    k += cnt;
+    active = active && cnt == K && pos < end && k < n;
+  }
+}
+
+// Zero-run streams: the warp fills its chunks' output range with the run
+// symbol (coalesced), then each lane stores only its chunk's other symbols.
+// Separate from k_dec_write so that neither the staging buffer nor the
+// registers of the dense path limit its occupancy.
+template <typename OutT>
+__global__ void __launch_bounds__(DEC_NT) k_dec_write_zr(Stream s, const DecTables *G,
+                                                        const uint16_t *sorted, u64 M,
+                                                        const u64 *X, const u64 *off,
+                                                        const uint32_t *cnts, u64 n, int R,
+                                                        OutT *__restrict__ out) {
+  if (!zrun_tables(G)) return;  // k_dec_write handles other streams
+  __shared__ DecSmem T;
+  __shared__ uint32_t sw[DEC_SW];
+  const u64 j0 = (u64)blockIdx.x * DEC_NT;
+  SmemStream ss;
+  stage_words(sw, s, j0, ss);
+  load_dec_smem(T, G, sorted);
+  const u64 j = j0 + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  u64 k = (j < M) ? off[j] : n;
+  u64 pos = (j < M) ? ((j == 0) ? 0 : X[j - 1]) : 0;
+  const u64 end = (j < M) ? min((j + 1) * DEC_C, s.nb) : 0;
+  const bool active = j < M && k < n;
+  SmemReader br;
+  br.init();
+  {
     // Sparse path: the warp's 32 chunks own the contiguous output range
     // [k(lane 0), k1(lane 31)); the warp fills it with the run symbol in
     // coalesced 16-byte stores, then each lane stores only the other
@@ -1113,41 +1180,6 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_write(Stream s, const DecTables 
       out[k++] = (sizeof(OutT) == 4) ? (OutT)((int32_t)sym - R) : (OutT)sym;
     }
     return;
-  }
-  while (__any_sync(CSZI_FULL, active)) {
-    int cnt = 0;
-    if (active) {
-      while (cnt < K && pos < end && k + cnt < n) {
-        const uint32_t w = br.peek(ss, pos);
-        if (T.zrun && !(w >> 31)) {  // run of the "0" codeword
-          u64 adv = min((u64)__clz(w), end - pos);
-          adv = min(adv, (u64)(K - cnt));
-          adv = min(adv, n - k - cnt);
-          const OutT zv = (sizeof(OutT) == 4) ? (OutT)((int32_t)T.zsym - R) : (OutT)T.zsym;
-          for (int i = 0; i < (int)adv; ++i) ob[warp][lane][cnt + i] = zv;
-          cnt += (int)adv;
-          pos += adv;
-          continue;
-        }
-        uint32_t len;
-        const uint32_t sym = decode_at(T, sorted, w, len);
-        if (len == 0 || pos + len > s.nb) {
-          pos = end;  // dead chain: truncation is reported by k_dec_check
-          break;
-        }
-        pos += len;
-        ob[warp][lane][cnt++] = (sizeof(OutT) == 4) ? (OutT)((int32_t)sym - R) : (OutT)sym;
-      }
-    }
-    __syncwarp();
-    for (int i = 0; i < 32; ++i) {
-      const int ci = __shfl_sync(CSZI_FULL, cnt, i);
-      const u64 ki = __shfl_sync(CSZI_FULL, k, i);
-      if (lane < ci) out[ki + lane] = ob[warp][i][lane];
-    }
-    __syncwarp();
-    k += cnt;
-    active = active && cnt == K && pos < end && k < n;
   }
 }
 
@@ -1401,13 +1433,18 @@ int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *de
   note_launch();
   k_dec_check<<<1, 1, 0, st>>>(off, K, first_dead, total, n, ctl);
   note_launch();
-  if (out_kind == 0)
+  if (out_kind == 0) {
     k_dec_write<uint16_t><<<dblocks, DEC_NT, 0, st>>>(s, G, sorted, M, X0, off, K, n, R,
                                                       reinterpret_cast<uint16_t *>(out));
-  else
+    k_dec_write_zr<uint16_t><<<dblocks, DEC_NT, 0, st>>>(s, G, sorted, M, X0, off, K, n, R,
+                                                         reinterpret_cast<uint16_t *>(out));
+  } else {
     k_dec_write<int32_t><<<dblocks, DEC_NT, 0, st>>>(s, G, sorted, M, X0, off, K, n, R,
                                                      reinterpret_cast<int32_t *>(out));
-  note_launch();
+    k_dec_write_zr<int32_t><<<dblocks, DEC_NT, 0, st>>>(s, G, sorted, M, X0, off, K, n, R,
+                                                        reinterpret_cast<int32_t *>(out));
+  }
+  note_launch(2);
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
