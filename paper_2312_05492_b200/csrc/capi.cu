@@ -1,6 +1,7 @@
 // extern "C" entry points of libcszi.so (see include/cszi.h) and the
 // stream-ordered orchestration of the compress / decompress paths
 // (pipeline.py:66-204).  No exceptions cross the ABI; no host sync inside.
+#include <algorithm>
 #include <atomic>
 #include <cstring>
 
@@ -42,7 +43,7 @@ int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *length
 u64 dec_scratch_bytes(u64 nbytes, int table_mode);
 int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *dec_tables,
                   void *out, int out_kind, void *scratch, cszi_ctl *ctl, cudaStream_t st,
-                  int table_mode, int lmax);
+                  int table_mode, int lmax, u64 w0, u64 w1);
 u64 p2enc_scratch_bytes(u64 n);
 int launch_pass2_encode(const uint8_t *in, const u64 *Np, u64 cap_n, uint8_t *out,
                         void *scratch, cszi_ctl *ctl, cudaStream_t st);
@@ -134,13 +135,15 @@ __global__ void k_outliers_parse(const uint8_t *sec, u64 sec_len, u64 n, u64 *oi
     if (ix >= n) atomicOr(&ctl->flags, (uint32_t)CSZI_F_OUTLIER_INDEX);
   }
 }
-__global__ void k_outliers_mark(const u64 *oidx, const cszi_ctl *ctl, u64 n, uint16_t *sym) {
+// sym holds the window [w0, w1) of the symbol array ([0, n) for a grid)
+__global__ void k_outliers_mark(const u64 *oidx, const cszi_ctl *ctl, u64 n, uint16_t *sym,
+                                u64 w0, u64 w1) {
   if (ctl->flags & (CSZI_F_OUTLIER_COUNT | CSZI_F_OUTLIER_ORDER | CSZI_F_OUTLIER_INDEX)) return;
   const u64 k = ctl->n_outliers;
   for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < k;
        r += (u64)gridDim.x * blockDim.x) {
     const u64 ix = oidx[r];
-    if (ix < n) sym[ix] = 0xFFFFu;
+    if (ix < n && ix >= w0 && ix < w1) sym[ix - w0] = 0xFFFFu;
   }
 }
 
@@ -218,6 +221,20 @@ struct DecompressWS {
   void *dec_scratch;
 };
 
+// symbols a decompress needs: the whole grid, or for a z-slab shard
+// [z0, z1) its planes plus the closing halo plane: [z0, min(z1 + 1, nz))
+static u64 sym_window(const cszi_geom *g, u64 *w0) {
+  const u64 plane = (u64)g->ext[1] * g->ext[2];
+  if (g->slab[1] > g->slab[0]) {
+    const u64 z0 = (u64)g->slab[0];
+    const u64 z1 = std::min<u64>((u64)g->slab[1] + 1, (u64)g->ext[0]);
+    if (w0) *w0 = z0 * plane;
+    return (z1 - z0) * plane;
+  }
+  if (w0) *w0 = 0;
+  return grid_n(g);
+}
+
 static u64 layout_decompress(const cszi_geom *g, int32_t R, const u64 sec[4], u64 payload_len,
                              int table_mode, void *base, DecompressWS *W) {
   const u64 n = grid_n(g);
@@ -228,7 +245,7 @@ static u64 layout_decompress(const cszi_geom *g, int32_t R, const u64 sec[4], u6
   w.raw = c.take(raw + 64);
   w.p2_scratch = c.take(p2dec_scratch_bytes(payload_len));
   w.dec_tables = c.take(dec_tables_bytes(2 * R));
-  w.sym = reinterpret_cast<uint16_t *>(c.take(2 * n + 32));
+  w.sym = reinterpret_cast<uint16_t *>(c.take(2 * sym_window(g, nullptr) + 32));
   w.oidx = reinterpret_cast<u64 *>(c.take(8 * kmax));
   w.oval = reinterpret_cast<float *>(c.take(4 * kmax));
   w.dec_scratch = c.take(dec_scratch_bytes(sec[2], table_mode));
@@ -361,13 +378,15 @@ int cszi_decompress(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
   const uint8_t *bits = lengths + sec_len[1];
   const uint8_t *outl = bits + sec_len[2];
   CK(launch_canonical(lengths, (int)nbins, nullptr, W.dec_tables, ctl, st));
+  u64 w0 = 0;
+  const u64 wn = sym_window(g, &w0);  // z-slab shard: only its symbol window
   CK(launch_decode(bits, sec_len[2], n, radius, W.dec_tables, W.sym, 0, W.dec_scratch, ctl, st,
-                   table_mode, 32));
+                   table_mode, 32, w0, w0 + wn));
   const u64 kmax = sec_len[3] >= 8 ? (sec_len[3] - 8) / 12 : 0;
   k_outliers_parse<<<grid_for(kmax), 256, 0, st>>>(outl, sec_len[3], n, W.oidx, W.oval, W.sym,
                                                    ctl);
   note_launch();
-  k_outliers_mark<<<grid_for(kmax), 256, 0, st>>>(W.oidx, ctl, n, W.sym);
+  k_outliers_mark<<<grid_for(kmax), 256, 0, st>>>(W.oidx, ctl, n, W.sym, w0, w0 + wn);
   note_launch();
   // the anchor section is 4-byte aligned inside the decoded payload
   const float *anc = reinterpret_cast<const float *>(anchors);
@@ -490,7 +509,7 @@ int cszi_huff_decode_i32(const uint8_t *stream_bytes, uint64_t nbytes, uint64_t 
                          int32_t table_mode, int32_t lmax, void *workspace, cszi_ctl *ctl,
                          void *stream) {
   return launch_decode(stream_bytes, nbytes, n, radius, dec_tables, codes, 1, workspace, ctl,
-                       reinterpret_cast<cudaStream_t>(stream), table_mode, lmax);
+                       reinterpret_cast<cudaStream_t>(stream), table_mode, lmax, 0, n);
 }
 
 uint64_t cszi_pass2_encode_workspace_size(uint64_t n) { return p2enc_scratch_bytes(n) + 256; }

@@ -1046,11 +1046,15 @@ __global__ void k_dec_from_tab(u64 M, int lmax, const uint8_t *E, const uint32_t
 // every store instruction of a warp covers one contiguous 64-128 B span.
 constexpr int DEC_K = 32;
 
+// Both write kernels store symbol k at out[k - w0] for k in [w0, w1) only
+// (a z-slab's window of the stream; [0, n) for a whole grid); chunks
+// outside the window are not decoded.
 template <typename OutT>
 __global__ void __launch_bounds__(DEC_NT) k_dec_write(Stream s, const DecTables *G,
                                                      const uint16_t *sorted, u64 M, const u64 *X,
                                                      const u64 *off, const uint32_t *cnts,
-                                                     u64 n, int R, OutT *__restrict__ out) {
+                                                     u64 n, int R, OutT *__restrict__ out, u64 w0,
+                                                     u64 w1) {
   if (zrun_tables(G)) return;  // zero-run streams: k_dec_write_zr
   __shared__ DecSmem T;
   __shared__ uint32_t sw[DEC_SW];
@@ -1065,7 +1069,7 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_write(Stream s, const DecTables 
   u64 k = (j < M) ? off[j] : n;
   u64 pos = (j < M) ? ((j == 0) ? 0 : X[j - 1]) : 0;
   const u64 end = (j < M) ? min((j + 1) * DEC_C, s.nb) : 0;
-  bool active = j < M && k < n;
+  bool active = j < M && k < n && k < w1 && k + cnts[j] > w0;
   SmemReader br;
   br.init();
   if (T.zrun) return;  // zero-run streams: k_dec_write_zr
@@ -1098,11 +1102,11 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_write(Stream s, const DecTables 
     for (int i = 0; i < 32; ++i) {
       const int ci = __shfl_sync(CSZI_FULL, cnt, i);
       const u64 ki = __shfl_sync(CSZI_FULL, k, i);
-      if (lane < ci) out[ki + lane] = ob[warp][i][lane];
+      if (lane < ci && ki + lane >= w0 && ki + lane < w1) out[ki + lane - w0] = ob[warp][i][lane];
     }
     __syncwarp();
     k += cnt;
-    active = active && cnt == K && pos < end && k < n;
+    active = active && cnt == K && pos < end && k < n && k < w1;
   }
 }
 
@@ -1115,7 +1119,7 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_write_zr(Stream s, const DecTabl
                                                         const uint16_t *sorted, u64 M,
                                                         const u64 *X, const u64 *off,
                                                         const uint32_t *cnts, u64 n, int R,
-                                                        OutT *__restrict__ out) {
+                                                        OutT *__restrict__ out, u64 w0, u64 w1) {
   if (!zrun_tables(G)) return;  // k_dec_write handles other streams
   __shared__ DecSmem T;
   __shared__ uint32_t sw[DEC_SW];
@@ -1128,7 +1132,7 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_write_zr(Stream s, const DecTabl
   u64 k = (j < M) ? off[j] : n;
   u64 pos = (j < M) ? ((j == 0) ? 0 : X[j - 1]) : 0;
   const u64 end = (j < M) ? min((j + 1) * DEC_C, s.nb) : 0;
-  const bool active = j < M && k < n;
+  const bool active = j < M && k < n && k < w1 && k + cnts[j] > w0;
   SmemReader br;
   br.init();
   {
@@ -1136,30 +1140,32 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_write_zr(Stream s, const DecTabl
     // [k(lane 0), k1(lane 31)); the warp fills it with the run symbol in
     // coalesced 16-byte stores, then each lane stores only the other
     // symbols of its chunk (after __syncwarp, so they win).  Runs cost O(1).
-    const u64 k1 = active ? min(k + cnts[j], n) : k;
+    const u64 k1 = active ? min(min(k + cnts[j], n), w1) : k;
     const OutT zv = (sizeof(OutT) == 4) ? (OutT)((int32_t)T.zsym - R) : (OutT)T.zsym;
     constexpr int PER = 16 / sizeof(OutT);
     {
-      u64 wa = active ? k : ~0ull, wb = active ? k1 : 0;
+      u64 wa = active ? max(k, w0) : ~0ull, wb = active ? k1 : 0;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         wa = min(wa, __shfl_xor_sync(CSZI_FULL, wa, o));
         wb = max(wb, __shfl_xor_sync(CSZI_FULL, wb, o));
       }
-      if (wa < wb) {
+      if (wa < wb) {  // window coordinates (out is 16-byte aligned at w0 when PER | w0)
         uint4 zz;
         OutT tmp[PER];
 #pragma unroll
         for (int i = 0; i < PER; ++i) tmp[i] = zv;
         memcpy(&zz, tmp, 16);
-        const u64 va = (wa + PER - 1) / PER, vb = wb / PER;  // whole vectors
-        if (va <= vb) {
-          for (u64 f = wa + lane; f < va * PER; f += 32) out[f] = zv;
+        const u64 ra = wa - w0, rb = wb - w0;
+        const bool vec = (w0 % PER) == 0;
+        const u64 va = vec ? (ra + PER - 1) / PER : rb, vb = vec ? rb / PER : rb;
+        if (vec && va <= vb) {
+          for (u64 f = ra + lane; f < va * PER; f += 32) out[f] = zv;
           for (u64 v = va + lane; v < vb; v += 32)
             __stcs(reinterpret_cast<uint4 *>(out) + v, zz);
-          for (u64 f = vb * PER + lane; f < wb; f += 32) out[f] = zv;
+          for (u64 f = vb * PER + lane; f < rb; f += 32) out[f] = zv;
         } else {
-          for (u64 f = wa + lane; f < wb; f += 32) out[f] = zv;
+          for (u64 f = ra + lane; f < rb; f += 32) out[f] = zv;
         }
       }
     }
@@ -1177,7 +1183,8 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_write_zr(Stream s, const DecTabl
       const uint32_t sym = decode_at(T, sorted, w, len);
       if (len == 0 || pos + len > s.nb) break;  // dead chain: reported by k_dec_check
       pos += len;
-      out[k++] = (sizeof(OutT) == 4) ? (OutT)((int32_t)sym - R) : (OutT)sym;
+      if (k >= w0) out[k - w0] = (sizeof(OutT) == 4) ? (OutT)((int32_t)sym - R) : (OutT)sym;
+      ++k;
     }
     return;
   }
@@ -1366,7 +1373,7 @@ static unsigned char *carve(unsigned char *&p, u64 bytes) {
 // length), used when the speculative path reports non-convergence.
 int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *dec_tables,
                   void *out, int out_kind, void *scratch, cszi_ctl *ctl, cudaStream_t st,
-                  int table_mode, int lmax) {
+                  int table_mode, int lmax, u64 w0, u64 w1) {
   if (n == 0) return CSZI_OK;
   Stream s;
   const uintptr_t addr = reinterpret_cast<uintptr_t>(bytes);
@@ -1435,14 +1442,14 @@ int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *de
   note_launch();
   if (out_kind == 0) {
     k_dec_write<uint16_t><<<dblocks, DEC_NT, 0, st>>>(s, G, sorted, M, X0, off, K, n, R,
-                                                      reinterpret_cast<uint16_t *>(out));
-    k_dec_write_zr<uint16_t><<<dblocks, DEC_NT, 0, st>>>(s, G, sorted, M, X0, off, K, n, R,
-                                                         reinterpret_cast<uint16_t *>(out));
+                                                      reinterpret_cast<uint16_t *>(out), w0, w1);
+    k_dec_write_zr<uint16_t><<<dblocks, DEC_NT, 0, st>>>(
+        s, G, sorted, M, X0, off, K, n, R, reinterpret_cast<uint16_t *>(out), w0, w1);
   } else {
     k_dec_write<int32_t><<<dblocks, DEC_NT, 0, st>>>(s, G, sorted, M, X0, off, K, n, R,
-                                                     reinterpret_cast<int32_t *>(out));
-    k_dec_write_zr<int32_t><<<dblocks, DEC_NT, 0, st>>>(s, G, sorted, M, X0, off, K, n, R,
-                                                        reinterpret_cast<int32_t *>(out));
+                                                     reinterpret_cast<int32_t *>(out), w0, w1);
+    k_dec_write_zr<int32_t><<<dblocks, DEC_NT, 0, st>>>(
+        s, G, sorted, M, X0, off, K, n, R, reinterpret_cast<int32_t *>(out), w0, w1);
   }
   note_launch(2);
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;

@@ -387,3 +387,41 @@ def compress_simulated(x, world: int, eb: float, mode: str = "rel", pass2: bool 
         states.append(SlabState(x=x[z0:min(z1 + 1, nz)].contiguous(), extents=tuple(x.shape),
                                 z0=z0, z1=z1, eb=float(eb), mode=mode, radius=int(quant_radius)))
     return compress_slabs(states, SimComm(world), pass2=pass2)
+
+
+# ---------------------------------------------------------------------------
+# sharded decompress: every rank holds the archive, synchronises
+# the Huffman stream, decodes only its slab's symbol window and reconstructs
+# its planes.  No exchange: the archive is the shared input.
+# ---------------------------------------------------------------------------
+def decompress_slab(data, z0: int, z1: int):
+    """Planes [z0, z1) of a 3-D archive as a (z1 - z0, ny, nx) CUDA tensor."""
+    from .pipeline import decompress_device
+
+    return decompress_device(data, slab=(z0, z1))
+
+
+def decompress_sharded(data, nz: int = None, group=None):
+    """torch.distributed entry point: this rank's slab of the decompressed
+    field -> (z0, z1, tensor).  ``nz`` defaults to the archive's extent."""
+    import torch.distributed as dist
+
+    from .archive import HEADER_SIZE, unpack_header
+
+    if nz is None:
+        head = data[:HEADER_SIZE] if not isinstance(data, DeviceArchive) else data.header
+        nz = unpack_header(bytes(head), len(data)).extents[0]
+    z0, z1 = slab_bounds(nz, dist.get_world_size(group))[dist.get_rank(group)]
+    return z0, z1, decompress_slab(data, z0, z1)
+
+
+def decompress_simulated(data, world: int):
+    """All ``world`` slabs in this process, concatenated (GPU-count
+    determinism check on one device)."""
+    from .archive import HEADER_SIZE, unpack_header
+
+    t = _lib.torch()
+    head = data.header if isinstance(data, DeviceArchive) else bytes(data[:HEADER_SIZE])
+    nz = unpack_header(head, len(data)).extents[0]
+    parts = [decompress_slab(data, z0, z1) for z0, z1 in slab_bounds(nz, world) if z1 > z0]
+    return t.cat(parts, 0)

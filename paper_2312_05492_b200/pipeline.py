@@ -333,8 +333,14 @@ def _validate_only(h, d_payload, dev_pass2: bool, dims: Dims, host_err) -> None:
     raise host_err
 
 
-def decompress_device(data, threads: int = None) -> Grid:
-    """decompress() returning a Grid whose data stays in device memory."""
+def decompress_device(data, threads: int = None, slab=None):
+    """decompress() returning a Grid whose data stays in device memory.
+
+    Extension (multi-GPU): ``slab=(z0, z1)`` decodes only the
+    z-slab shard [z0, z1) of a 3-D default-layout archive -- the Huffman
+    stream is synchronised over its whole length but only the slab's symbol
+    window (plus the closing halo plane) is decoded -- and returns the
+    (z1 - z0, ny, nx) float32 CUDA tensor of those planes."""
     thread_count(threads)
     t = _lib.require_cuda()
     lib = _lib.load()
@@ -362,6 +368,16 @@ def decompress_device(data, threads: int = None) -> Grid:
     if host_err is not None:
         _validate_only(h, d_payload, dev_pass2, dims, host_err)
     geom = make_geom(h.extents, layout)
+    out_n = n
+    if slab is not None:
+        z0, z1 = (int(v) for v in slab)
+        if h.rank != 3 or layout.anchor_stride != 8 or layout.super_chunk_extents != (8, 8, 32):
+            raise NotImplementedError("slab decompress needs a 3-D default-layout archive")
+        nz = h.extents[0]
+        if not (0 <= z0 < z1 <= nz) or z0 % 8:
+            raise ValueError(f"slab [{z0}, {z1}) must start on an anchor plane inside [0, {nz})")
+        geom.slab[0], geom.slab[1] = z0, z1
+        out_n = (z1 - z0) * h.extents[1] * h.extents[2]
     plan = plan_levels(layout.anchor_stride, h.eb_abs, h.alpha)
     leb = (ctypes.c_double * _lib.MAX_LEVELS)(*[s.eb for s in plan.levels])
     pad = 3 - h.rank
@@ -369,7 +385,7 @@ def decompress_device(data, threads: int = None) -> Grid:
     order = (ctypes.c_int32 * 3)(*(tuple(pad + d for d in h.dim_order) + (0,) * pad))
     sec = (ctypes.c_uint64 * 4)(*h.sec_lens)
     R = h.quant_radius
-    y = t.empty(n, dtype=t.float32, device="cuda")
+    y = t.empty(out_n, dtype=t.float32, device="cuda")
     ctl = _lib.DeviceCtl()
     st = _lib.stream_ptr()
     plen = d_payload.numel()
@@ -387,6 +403,8 @@ def decompress_device(data, threads: int = None) -> Grid:
     _raise_device_flags(c, n)
     if c.flags & _lib.F_OUTLIER_INDEX:
         raise IndexError("outlier index out of bounds for the grid")
+    if slab is not None:
+        return y.view(slab[1] - slab[0], h.extents[1], h.extents[2])
     return Grid.wrap_device(dims, y)
 
 

@@ -37,3 +37,23 @@ def test_slab_sharding_modes_and_outliers():
         ref = O.compress(data, eb, mode=mode, pass2=p2)
         for world in (2, 4):
             assert compress_simulated(x, world, eb, mode=mode, pass2=p2).to_bytes() == ref
+
+
+@pytest.mark.parametrize("shape,world", [((64, 48, 64), 2), ((41, 30, 37), 4), ((100, 64, 96), 8),
+                                         ((17, 24, 40), 3)])
+def test_sharded_decompress_equals_whole(shape, world):
+    """Each slab decoded from the one archive (symbol window + halo plane)
+    matches the corresponding planes of the whole-grid decompression."""
+    import torch
+
+    from paper_2312_05492_b200.distributed import decompress_simulated
+
+    rng = np.random.default_rng(7)
+    data = noisy_field(rng, shape)
+    for eb in (1e-3, 1e-5):
+        blob = O.compress(data, eb)
+        whole = P.decompress_device(blob).tensor
+        parts = decompress_simulated(blob, world)
+        assert torch.equal(parts.view(-1), whole.reshape(-1))
+        arch = P.compress_device(P.Grid(P.Dims(shape), torch.from_numpy(data).cuda()), eb)
+        assert torch.equal(decompress_simulated(arch, world).view(-1), whole.reshape(-1))
