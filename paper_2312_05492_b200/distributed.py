@@ -227,7 +227,9 @@ class GpuSlabBackend:
         n = s.scratch["n_own"]
         ny, nx = s.extents[1], s.extents[2]
         cap = ((4 * n + 64) + 15) & ~15
-        bits = t.zeros(cap + 16, dtype=t.uint8, device="cuda")
+        # no zero fill (537 MB per 512-plane slab): the packers write or zero
+        # every word of the stream they use (k_enc_zero / k_scan_pair)
+        bits = t.empty(cap + 16, dtype=t.uint8, device="cuda")
         ocap = n + 16
         oidx = t.empty(ocap, dtype=t.int64, device="cuda")
         oval = t.empty(ocap, dtype=t.float32, device="cuda")
@@ -289,9 +291,10 @@ class GpuSlabBackend:
         k = sum(int(x.numel()) for x in oidx)
         head = a.numel() + lengths.numel()
         raw_len = head + nbytes + 8 + 12 * k
-        raw = t.zeros(raw_len + 16, dtype=t.uint8, device="cuda")
+        raw = t.empty(raw_len + 16, dtype=t.uint8, device="cuda")
         raw[: a.numel()] = a
         raw[a.numel(): head] = lengths
+        raw[head: head + nbytes + 8].zero_()  # the bit pieces are ORed in
         off = 0
         for piece, nb in zip(bit_pieces, nbits):
             if nb:
