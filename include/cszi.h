@@ -226,6 +226,14 @@ int cszi_encode_sym(const uint16_t *sym, uint64_t n, int32_t radius, const uint8
                     const uint32_t *words, const float *x, uint64_t idx_offset, uint8_t *out,
                     uint64_t cap_bytes, uint64_t *out_idx, float *out_val, uint64_t out_cap,
                     void *workspace, cszi_ctl *ctl, void *stream);
+/* The same with the stream packed from bit bit_base (0..31) of out's first
+ * word: a z-slab shard packs its piece at its global bit phase, so the root
+ * merges pieces with word copies (multi-GPU compress). */
+int cszi_encode_sym_at(const uint16_t *sym, uint64_t n, int32_t radius, const uint8_t *lengths,
+                       const uint32_t *words, const float *x, uint64_t idx_offset,
+                       uint32_t bit_base, uint8_t *out, uint64_t cap_bytes, uint64_t *out_idx,
+                       float *out_val, uint64_t out_cap, void *workspace, cszi_ctl *ctl,
+                       void *stream);
 
 /* dst (zeroed, bytes) |= nbits of src placed at bit offset dst_bit (MSB-first). */
 int cszi_concat_bits(uint8_t *dst, uint64_t dst_bit, const uint8_t *src, uint64_t nbits,

@@ -39,7 +39,7 @@ u64 enc_scratch_bytes(u64 n);
 int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *lengths,
                   const uint32_t *words, uint32_t *out, u64 cap_bytes, const float *xval,
                   u64 *o_idx, float *o_val, u64 o_cap, void *scratch, cszi_ctl *ctl,
-                  cudaStream_t st, u64 idx_offset);
+                  cudaStream_t st, u64 idx_offset, uint32_t bit_base = 0);
 u64 dec_scratch_bytes(u64 nbytes, int table_mode);
 int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *dec_tables,
                   void *out, int out_kind, void *scratch, cszi_ctl *ctl, cudaStream_t st,
@@ -425,14 +425,24 @@ uint64_t cszi_slab_anchor_count(const cszi_geom *g) { return slab_anchor_count(g
 
 uint64_t cszi_encode_sym_workspace_size(uint64_t n) { return enc_scratch_bytes(n) + 256; }
 
+int cszi_encode_sym_at(const uint16_t *sym, uint64_t n, int32_t radius, const uint8_t *lengths,
+                       const uint32_t *words, const float *x, uint64_t idx_offset,
+                       uint32_t bit_base, uint8_t *out, uint64_t cap_bytes, uint64_t *out_idx,
+                       float *out_val, uint64_t out_cap, void *workspace, cszi_ctl *ctl,
+                       void *stream) {
+  if ((reinterpret_cast<uintptr_t>(out) & 3) || bit_base > 31) return CSZI_E_INVALID_ARG;
+  return launch_encode(0, sym, n, radius, lengths, words, reinterpret_cast<uint32_t *>(out),
+                       cap_bytes, x, reinterpret_cast<u64 *>(out_idx), out_val, out_cap,
+                       workspace, ctl, reinterpret_cast<cudaStream_t>(stream), idx_offset,
+                       bit_base);
+}
+
 int cszi_encode_sym(const uint16_t *sym, uint64_t n, int32_t radius, const uint8_t *lengths,
                     const uint32_t *words, const float *x, uint64_t idx_offset, uint8_t *out,
                     uint64_t cap_bytes, uint64_t *out_idx, float *out_val, uint64_t out_cap,
                     void *workspace, cszi_ctl *ctl, void *stream) {
-  if (reinterpret_cast<uintptr_t>(out) & 3) return CSZI_E_INVALID_ARG;
-  return launch_encode(0, sym, n, radius, lengths, words, reinterpret_cast<uint32_t *>(out),
-                       cap_bytes, x, reinterpret_cast<u64 *>(out_idx), out_val, out_cap,
-                       workspace, ctl, reinterpret_cast<cudaStream_t>(stream), idx_offset);
+  return cszi_encode_sym_at(sym, n, radius, lengths, words, x, idx_offset, 0, out, cap_bytes,
+                            out_idx, out_val, out_cap, workspace, ctl, stream);
 }
 
 int cszi_concat_bits(uint8_t *dst, uint64_t dst_bit, const uint8_t *src, uint64_t nbits,

@@ -445,7 +445,8 @@ __global__ void __launch_bounds__(ENC_NT) k_enc_count(const void *__restrict__ s
 // exclusive prefixes of (bits, outliers) per chunk; totals -> ctl
 constexpr int PS_NT = 256, PS_IPT = 8, PS_TILE = PS_NT * PS_IPT;
 __global__ void __launch_bounds__(PS_NT) k_scan_pair(EncScratch S, u64 nch, int mode,
-                                                    uint32_t *out, u64 cap_words, cszi_ctl *ctl) {
+                                                    uint32_t *out, u64 cap_words, cszi_ctl *ctl,
+                                                    uint32_t bit_base) {
   __shared__ u64 ws[PS_NT / 32 + 1];
   __shared__ u64 s_t, s_pb, s_po;
   if (threadIdx.x == 0) s_t = atomicAdd(S.ticket, 1u);
@@ -479,7 +480,8 @@ __global__ void __launch_bounds__(PS_NT) k_scan_pair(EncScratch S, u64 nch, int 
       S.bit_off[base + i] = rb;
       S.out_off[base + i] = ro;
       // a word holding an unaligned chunk boundary is ORed by both chunks
-      if ((rb & 31) && (rb >> 5) < cap_words) out[rb >> 5] = 0u;
+      const u64 ab = rb + bit_base;  // bit position in the output words
+      if ((ab & 31) && (ab >> 5) < cap_words) out[ab >> 5] = 0u;
     }
     rb += vb[i];
     ro += vo[i];
@@ -502,9 +504,9 @@ DEV bool enc_sparse(const uint8_t *lengths, const uint32_t *words, int R, u64 n,
 }
 
 __global__ void k_enc_zero(const uint8_t *lengths, const uint32_t *words, int R, u64 n,
-                           uint32_t *out, u64 cap_words, const cszi_ctl *ctl) {
+                           uint32_t *out, u64 cap_words, const cszi_ctl *ctl, uint32_t bit_base) {
   if (!enc_sparse(lengths, words, R, n, ctl)) return;
-  u64 nw = (ctl->bits + 31) / 32 + 1;
+  u64 nw = (ctl->bits + bit_base + 31) / 32 + 1;
   if (nw > cap_words) nw = cap_words;
   // words up to the first 16-byte boundary, then 16-byte stores
   const u64 lead = min((u64)(((16 - (reinterpret_cast<uintptr_t>(out) & 15)) & 15) / 4), nw);
@@ -540,7 +542,7 @@ __global__ void __launch_bounds__(ENC_NT, 3) k_enc_sparse(const uint16_t *__rest
                                                           const float *__restrict__ xval,
                                                           u64 *o_idx, float *o_val, u64 o_cap,
                                                           EncScratch S, u64 nch, u64 idx_offset,
-                                                          cszi_ctl *ctl) {
+                                                          cszi_ctl *ctl, uint32_t bit_base) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   if (!enc_sparse(lengths, words, R, n, ctl)) return;
   const int nbins = 2 * R;
@@ -559,7 +561,7 @@ __global__ void __launch_bounds__(ENC_NT, 3) k_enc_sparse(const uint16_t *__rest
     EncSyms<0> nx;
     if (cn < nch) nx.load(src, n, R, nbins, cn * ENC_CH + (u64)lane * ENC_SPT, unknown);
     const u64 ob = S.out_off[c];
-    u64 pos = S.bit_off[c] + S.lane_pre[c * 32 + lane];
+    u64 pos = S.bit_off[c] + bit_base + S.lane_pre[c * 32 + lane];
     uint32_t outmask = 0;
 #pragma unroll
     for (int j = 0; j < ENC_SPT; j += 2) {
@@ -604,7 +606,7 @@ __global__ void __launch_bounds__(ENC_NT, 3) k_enc_pack(const void *__restrict__
                                                        uint32_t *__restrict__ out, u64 cap_words,
                                                        const float *__restrict__ xval, u64 *o_idx,
                                                        float *o_val, u64 o_cap, EncScratch S,
-                                                       u64 nch, u64 idx_offset, cszi_ctl *ctl) {
+                                                       u64 nch, u64 idx_offset, cszi_ctl *ctl, uint32_t bit_base) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   if (MODE == 0 && enc_sparse(lengths, words, R, n, ctl)) return;  // k_enc_sparse's case
   const int nbins = 2 * R;
@@ -628,7 +630,7 @@ __global__ void __launch_bounds__(ENC_NT, 3) k_enc_pack(const void *__restrict__
     const u64 cn = c + stride;
     EncSyms<MODE> nx;
     if (cn < nch) nx.load(src, n, R, nbins, cn * ENC_CH + (u64)lane * ENC_SPT, unknown);
-    const u64 tb = S.bit_off[c];
+    const u64 tb = S.bit_off[c] + bit_base;
     const u64 ob = (MODE == 0) ? S.out_off[c] : 0;
     uint32_t outmask;
     const uint32_t nbits = enc_bits<MODE>(sy, lut, nbins, unknown, outmask, zz2);
@@ -1290,7 +1292,7 @@ u64 enc_scratch_bytes(u64 n) {
 int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *lengths,
                   const uint32_t *words, uint32_t *out, u64 cap_bytes, const float *xval,
                   u64 *o_idx, float *o_val, u64 o_cap, void *scratch, cszi_ctl *ctl,
-                  cudaStream_t st, u64 idx_offset) {
+                  cudaStream_t st, u64 idx_offset, uint32_t bit_base) {
   if (n == 0) return CSZI_OK;
   const u64 nch = (n + ENC_CH - 1) / ENC_CH;
   const u64 nc = nch + 2;
@@ -1322,17 +1324,18 @@ int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *length
   u64 blocks = (u64)sms * (per_sm < 1 ? 1 : per_sm);
   if (blocks > wblocks) blocks = wblocks;
   kc<<<(unsigned)blocks, ENC_NT, smem_c, st>>>(src, n, R, lengths, S, nch, ctl);
-  k_scan_pair<<<(unsigned)npt, PS_NT, 0, st>>>(S, nch, mode, out, cap_bytes / 4, ctl);
+  k_scan_pair<<<(unsigned)npt, PS_NT, 0, st>>>(S, nch, mode, out, cap_bytes / 4, ctl, bit_base);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, ENC_NT, smem_p);
   blocks = (u64)sms * (per_sm < 1 ? 1 : per_sm);
   if (blocks > wblocks) blocks = wblocks;
   kp<<<(unsigned)blocks, ENC_NT, smem_p, st>>>(src, n, R, lengths, words, out, cap_bytes / 4,
                                                xval, o_idx, o_val, o_cap, S, nch, idx_offset,
-                                               ctl);
+                                               ctl, bit_base);
   note_launch(3);
   if (mode == 0) {
     // sparse alternative (each kernel checks the same device-side predicate)
-    k_enc_zero<<<(unsigned)(sms * 4), 256, 0, st>>>(lengths, words, R, n, out, cap_bytes / 4, ctl);
+    k_enc_zero<<<(unsigned)(sms * 4), 256, 0, st>>>(lengths, words, R, n, out, cap_bytes / 4, ctl,
+                                                    bit_base);
     const size_t smem_s = sizeof(uint2) * (nbins + 2) + 16;
     cudaFuncSetAttribute(k_enc_sparse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_enc_sparse, ENC_NT, smem_s);
@@ -1340,7 +1343,7 @@ int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *length
     if (blocks > wblocks) blocks = wblocks;
     k_enc_sparse<<<(unsigned)blocks, ENC_NT, smem_s, st>>>(
         reinterpret_cast<const uint16_t *>(src), n, R, lengths, words, out, cap_bytes / 4, xval,
-        o_idx, o_val, o_cap, S, nch, idx_offset, ctl);
+        o_idx, o_val, o_cap, S, nch, idx_offset, ctl, bit_base);
     note_launch(2);
   }
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;

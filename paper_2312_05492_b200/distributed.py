@@ -221,9 +221,16 @@ class GpuSlabBackend:
         s.scratch["lengths"] = lengths
         s.scratch["words"] = words
 
-    def encode(self, s: SlabState):
+    def piece_bits(self, s: SlabState, hist_local):
+        """Bits of this slab's Huffman piece: sum over symbols of count x length
+        (outliers and anchors are counted as R, which is how they are coded)."""
+        lengths = s.scratch["lengths"].to(hist_local.dtype)
+        return (hist_local.reshape(-1) * lengths).sum().reshape(1)
+
+    def encode(self, s: SlabState, bit_base: int = 0):
         t = _lib.torch()
         lib = _lib.load()
+        s.scratch["bit_base"] = int(bit_base)
         n = s.scratch["n_own"]
         ny, nx = s.extents[1], s.extents[2]
         cap = ((4 * n + 64) + 15) & ~15
@@ -236,11 +243,11 @@ class GpuSlabBackend:
         ws = _lib.WS.get(int(lib.cszi_encode_sym_workspace_size(max(n, 1))), "enc_slab")
         ctl = s.scratch["ctl"]
         if n:
-            _lib.check(lib.cszi_encode_sym(
+            _lib.check(lib.cszi_encode_sym_at(
                 _lib.ptr(s.scratch["sym"]), n, s.radius, _lib.ptr(s.scratch["lengths"]),
-                _lib.ptr(s.scratch["words"]), _lib.ptr(s.x), s.z0 * ny * nx, _lib.ptr(bits), cap,
-                _lib.ptr(oidx), _lib.ptr(oval), ocap, _lib.ptr(ws), ctl.ptr, _lib.stream_ptr()),
-                "encode")
+                _lib.ptr(s.scratch["words"]), _lib.ptr(s.x), s.z0 * ny * nx, int(bit_base),
+                _lib.ptr(bits), cap, _lib.ptr(oidx), _lib.ptr(oval), ocap, _lib.ptr(ws), ctl.ptr,
+                _lib.stream_ptr()), "encode")
         s.scratch.update(bits=bits, oidx=oidx, oval=oval)
         return t.cat([_ctl_field(ctl, "bits", t.int64), _ctl_field(ctl, "n_outliers", t.int64)])
 
@@ -260,7 +267,8 @@ class GpuSlabBackend:
     def pieces(self, s: SlabState, counts):
         """Variable-length payload pieces of this slab (device tensors)."""
         nbits, nout = int(counts[0]), int(counts[1])
-        bits = s.scratch["bits"][: (nbits + 7) // 8]
+        nw = (s.scratch.get("bit_base", 0) + nbits + 31) // 32  # whole words, phase-packed
+        bits = s.scratch["bits"][: 4 * nw]
         return bits, s.scratch["oidx"][:nout], s.scratch["oval"][:nout]
 
     def assemble(self, s0: SlabState, anchors, bit_pieces, nbits, oidx, oval, pass2: bool,
@@ -294,13 +302,25 @@ class GpuSlabBackend:
         raw = t.empty(raw_len + 16, dtype=t.uint8, device="cuda")
         raw[: a.numel()] = a
         raw[a.numel(): head] = lengths
-        raw[head: head + nbytes + 8].zero_()  # the bit pieces are ORed in
+        raw[head: head + 4 * ((total_bits + 31) // 32 + 1)].zero_()  # the bit pieces are ORed in
         off = 0
-        for piece, nb in zip(bit_pieces, nbits):
-            if nb:
-                _lib.check(lib.cszi_concat_bits(_lib.ptr(raw[head:]), off, _lib.ptr(piece), nb, st),
-                           "concat_bits")
-            off += nb
+        if (raw.data_ptr() + head) % 4 == 0:
+            # pieces were packed at their global bit phase: OR whole words
+            nwt = (total_bits + 31) // 32 + 1
+            rw = raw[head: head + 4 * nwt].view(t.int32)
+            for piece, nb in zip(bit_pieces, nbits):
+                if nb:
+                    w0 = off // 32
+                    pw = piece.view(t.int32)
+                    rw[w0: w0 + pw.numel()].bitwise_or_(pw)
+                off += nb
+        else:  # odd R: the section is not word-aligned; shift the pieces back
+            for piece, nb in zip(bit_pieces, nbits):
+                if nb:
+                    ph = off % 32
+                    _lib.check(lib.cszi_concat_bits(_lib.ptr(raw[head:]), off - ph,
+                                                    _lib.ptr(piece), ph + nb, st), "concat_bits")
+                off += nb
         idx = t.cat([x.reshape(-1) for x in oidx]) if k else t.zeros(1, dtype=t.int64, device="cuda")
         val = t.cat([x.reshape(-1) for x in oval]) if k else t.zeros(1, dtype=t.float32, device="cuda")
         _lib.check(lib.cszi_pack_outliers(_lib.ptr(idx), _lib.ptr(val), k,
@@ -346,11 +366,23 @@ def compress_slabs(states: list, comm, backend=None, pass2: bool = True):
         backend.tune(s, v, alpha)
     # (3) histogram -> shared codebook
     hists = [backend.predict(s) for s in states]
+    phased = hasattr(backend, "piece_bits")
+    local_h = [h.clone() for h in hists] if phased else None
     comm.allreduce(hists, "sum")
     for s, h in zip(states, hists):
         backend.codebook(s, h)
-    # (4) bit / outlier counts
-    counts = [backend.encode(s) for s in states]
+    # (4) bit / outlier counts.  A phase-packing backend first exchanges each
+    # slab's stream length (local histogram . code lengths, known before any
+    # packing) so every slab packs at its global bit phase and the root
+    # merges whole words instead of bit-shifting the pieces.
+    if phased:
+        pb = [backend.piece_bits(s, h) for s, h in zip(states, local_h)]
+        allpb = [int(v.reshape(-1)[0].item()) for v in comm.allgather(pb)[0]]
+        starts = [sum(allpb[:r]) for r in range(len(allpb))]
+        counts = [backend.encode(s, bit_base=starts[r] % 32)
+                  for s, r in zip(states, _local_ranks(comm, states))]
+    else:
+        counts = [backend.encode(s) for s in states]
     allc = comm.allgather(counts)[0]
     allc = [c.cpu().numpy() for c in allc]
     # (5) gather pieces to the root

@@ -57,3 +57,17 @@ def test_sharded_decompress_equals_whole(shape, world):
         assert torch.equal(parts.view(-1), whole.reshape(-1))
         arch = P.compress_device(P.Grid(P.Dims(shape), torch.from_numpy(data).cuda()), eb)
         assert torch.equal(decompress_simulated(arch, world).view(-1), whole.reshape(-1))
+
+
+def test_phase_packed_pieces_odd_radius():
+    """Odd R leaves the bitstream section unaligned: the root shifts the
+    phase-packed pieces instead of OR-ing words; bytes still match."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    data = noisy_field(rng, (40, 24, 48))
+    x = torch.from_numpy(data).cuda()
+    for R in (7, 512):
+        ref = O.compress(data, 1e-3, quant_radius=R)
+        for world in (2, 3, 5):
+            assert compress_simulated(x, world, 1e-3, quant_radius=R).to_bytes() == ref
