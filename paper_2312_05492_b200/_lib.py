@@ -15,7 +15,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcszi.so")
+LIB_PATH = os.environ.get("CSZI_LIB") or os.path.join(_HERE, "libcszi.so")  # override: A/B runs
 CSRC = os.path.join(_HERE, "csrc")
 
 MAX_LEVELS = 16

@@ -21,7 +21,8 @@ int launch_concat_bits(uint8_t *dst, u64 dst_bit, const uint8_t *src, u64 nbits,
 int launch_pack_outliers(const u64 *idx, const float *val, u64 k, uint8_t *out,
                          cudaStream_t st);
 int launch_predict(const float *x, const cszi_geom *g, int32_t radius, const cszi_ctl *ctl,
-                   uint16_t *sym, u64 *hist, bool exact, cudaStream_t st);
+                   uint16_t *sym, u64 *hist, bool exact, cudaStream_t st,
+                   uint32_t *nzmap = nullptr, bool *nz_done = nullptr);
 int launch_reconstruct(const uint16_t *sym, const float *anchors, const u64 *oidx,
                        const float *oval, u64 nout, const u64 *nout_dev, const cszi_geom *g,
                        int32_t radius,
@@ -39,7 +40,8 @@ u64 enc_scratch_bytes(u64 n);
 int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *lengths,
                   const uint32_t *words, uint32_t *out, u64 cap_bytes, const float *xval,
                   u64 *o_idx, float *o_val, u64 o_cap, void *scratch, cszi_ctl *ctl,
-                  cudaStream_t st, u64 idx_offset, uint32_t bit_base = 0);
+                  cudaStream_t st, u64 idx_offset, uint32_t bit_base = 0,
+                  const uint32_t *nzmap = nullptr, const u64 *hist = nullptr);
 u64 dec_scratch_bytes(u64 nbytes, int table_mode);
 int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *dec_tables,
                   void *out, int out_kind, void *scratch, cszi_ctl *ctl, cudaStream_t st,
@@ -182,6 +184,7 @@ static u64 raw_capacity(const cszi_geom *g, int32_t R, const cszi_caps *caps) {
 struct CompressWS {
   int32_t *samples;
   uint16_t *sym;
+  uint32_t *nzmap;  // non-R bit per symbol (t3 predictor -> sparse encoder)
   u64 *hist;
   uint32_t *words;
   uint32_t *bits;
@@ -199,6 +202,7 @@ static u64 layout_compress(const cszi_geom *g, int32_t R, const cszi_caps *caps,
   CompressWS w;
   w.samples = reinterpret_cast<int32_t *>(c.take(4 * CSZI_SAMPLE_WORDS));
   w.sym = reinterpret_cast<uint16_t *>(c.take(2 * n + 32));
+  w.nzmap = reinterpret_cast<uint32_t *>(c.take(n / 8 + 16));
   w.hist = reinterpret_cast<u64 *>(c.take(8 * 2 * (u64)R));
   w.words = reinterpret_cast<uint32_t *>(c.take(4 * 2 * (u64)R));
   w.bits = reinterpret_cast<uint32_t *>(c.take(caps->bits_cap + 16));
@@ -323,7 +327,8 @@ int cszi_compress(const float *x, const cszi_geom *g, const cszi_params *p,
   }
   CK(launch_tune(x, g, p, ctl, W.samples, st));
   cudaMemsetAsync(W.hist, 0, 8 * nbins, st);
-  CK(launch_predict(x, g, R, ctl, W.sym, W.hist, p->exact != 0, st));
+  bool nz = false;
+  CK(launch_predict(x, g, R, ctl, W.sym, W.hist, p->exact != 0, st, W.nzmap, &nz));
   uint8_t *raw = pass2 ? W.raw : payload;
   CK(launch_gather_anchors(x, g, reinterpret_cast<float *>(raw), st));
   uint8_t *lengths = raw + 4 * na;  // the codebook section is the length table
@@ -334,7 +339,8 @@ int cszi_compress(const float *x, const cszi_geom *g, const cszi_params *p,
   const bool in_place = ((reinterpret_cast<uintptr_t>(raw) + head) & 3) == 0;
   uint32_t *bits_out = in_place ? reinterpret_cast<uint32_t *>(raw + head) : W.bits;
   CK(launch_encode(0, W.sym, n, R, lengths, W.words, bits_out, caps->bits_cap, x, W.oidx, W.oval,
-                   caps->outlier_cap, W.enc_scratch, ctl, st, 0));
+                   caps->outlier_cap, W.enc_scratch, ctl, st, 0, 0, nz ? W.nzmap : nullptr,
+                   W.hist));
   k_assemble<<<grid_for(n / 16), 256, 0, st>>>(raw, head, reinterpret_cast<uint8_t *>(W.bits),
                                                 W.oidx, W.oval, raw_cap, caps->bits_cap,
                                                 caps->outlier_cap, ctl, pass2 ? 0 : 1,

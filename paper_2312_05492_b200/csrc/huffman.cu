@@ -301,6 +301,7 @@ struct EncScratch {
   u64 *st_bits;  // look-back status of the pair scan
   u64 *st_out;
   uint32_t *ticket;
+  uint32_t *nz_lane;  // bitmap path: per super-chunk and lane, packed exclusive prefixes
 };
 
 
@@ -386,13 +387,27 @@ DEV uint32_t enc_bits(const EncSyms<MODE> &sy, const uint2 *lut, int nbins, bool
   return nbits;
 }
 
+// Sparse stream (MODE 0): R owns the 1-bit "0" codeword and at most n/8
+// symbols are not R (every other codeword has >= 2 bits, so bits - n bounds
+// their count).  The stream is then zeroed and only the codewords holding
+// 1-bits are ORed in at their offsets (k_enc_sparse); otherwise k_enc_pack
+// packs every chunk.  Both kernels evaluate the same predicate on device.
+DEV bool enc_sparse(const uint8_t *lengths, const uint32_t *words, int R, u64 n,
+                    const cszi_ctl *ctl) {
+  const u64 bits = ctl->bits;
+  return lengths[R] == 1 && words[R] == 0 && bits >= n && (bits - n) <= n / 8;
+}
+
 // k_enc_count: lengths and outlier flags come from one u32 LUT entry
 // (length | outlier << 16) so a lane sums both with one add per symbol.
 template <int MODE>
 __global__ void __launch_bounds__(ENC_NT) k_enc_count(const void *__restrict__ src, u64 n, int R,
                                                      const uint8_t *__restrict__ lengths,
-                                                     EncScratch S, u64 nch, cszi_ctl *ctl) {
+                                                     EncScratch S, u64 nch, cszi_ctl *ctl,
+                                                     const uint32_t *skip_words) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
+  // the k_enc_nz_* kernels encode the sparse case (ctl->bits known beforehand)
+  if (skip_words && enc_sparse(lengths, skip_words, R, n, ctl)) return;
   uint32_t *lut = reinterpret_cast<uint32_t *>(sm_raw);
   const int nbins = 2 * R;
   const int lane = threadIdx.x & 31;
@@ -446,8 +461,12 @@ __global__ void __launch_bounds__(ENC_NT) k_enc_count(const void *__restrict__ s
 constexpr int PS_NT = 256, PS_IPT = 8, PS_TILE = PS_NT * PS_IPT;
 __global__ void __launch_bounds__(PS_NT) k_scan_pair(EncScratch S, u64 nch, int mode,
                                                     uint32_t *out, u64 cap_words, cszi_ctl *ctl,
-                                                    uint32_t bit_base) {
+                                                    uint32_t bit_base, const uint8_t *p_len,
+                                                    const uint32_t *p_words, int R, u64 n,
+                                                    int when) {
   __shared__ u64 ws[PS_NT / 32 + 1];
+  // when: 0 always, 1 dense streams only, 2 sparse streams only
+  if (when && enc_sparse(p_len, p_words, R, n, ctl) != (when == 2)) return;
   __shared__ u64 s_t, s_pb, s_po;
   if (threadIdx.x == 0) s_t = atomicAdd(S.ticket, 1u);
   __syncthreads();
@@ -490,17 +509,6 @@ __global__ void __launch_bounds__(PS_NT) k_scan_pair(EncScratch S, u64 nch, int 
     ctl->bits = s_pb + tb;
     if (mode == 0) ctl->n_outliers = s_po + to;
   }
-}
-
-// Sparse stream (MODE 0): R owns the 1-bit "0" codeword and at most n/8
-// symbols are not R (every other codeword has >= 2 bits, so bits - n bounds
-// their count).  The stream is then zeroed and only the codewords holding
-// 1-bits are ORed in at their offsets (k_enc_sparse); otherwise k_enc_pack
-// packs every chunk.  Both kernels evaluate the same predicate on device.
-DEV bool enc_sparse(const uint8_t *lengths, const uint32_t *words, int R, u64 n,
-                    const cszi_ctl *ctl) {
-  const u64 bits = ctl->bits;
-  return lengths[R] == 1 && words[R] == 0 && bits >= n && (bits - n) <= n / 8;
 }
 
 __global__ void k_enc_zero(const uint8_t *lengths, const uint32_t *words, int R, u64 n,
@@ -597,6 +605,204 @@ __global__ void __launch_bounds__(ENC_NT, 3) k_enc_sparse(const uint16_t *__rest
     c = cn;
   }
   if (cap_hit) atomicOr(&ctl->flags, (uint32_t)CSZI_F_CAPACITY);
+}
+
+// Bitmap-driven sparse encoder (MODE 0).  The predictor also wrote one bit
+// per symbol, set when the symbol is not R (outliers included), as u32 words
+// in symbol order (n % 32 == 0), and k_total_bits computed the stream length
+// from the histogram, so the sparse case is known before encoding.  Then R
+// is the 1-bit "0" and symbol J starts at bit J + (extra bits of the non-R
+// codewords before J).  One warp per 4096-symbol super-chunk, a lane per
+// 128 symbols (4 bitmap words): the lane reads only the 16-byte groups of
+// symbols under set bits -- about 5% of the groups on smooth fields -- so
+// runs of R cost one bitmap bit each.  k_enc_nz_count (extra bits and
+// outliers per super-chunk, lane prefixes) -> k_scan_pair over the
+// super-chunks -> k_enc_nz_emit.  (Tried: a single-pass decoupled look-back
+// over the 32k super-chunks -- 3x slower, the per-tile work is too small to
+// hide the walk; shared-memory position lists -- dense super-chunks at the
+// field's edges serialise one warp for ~100 us.)
+constexpr int NZ_SC = 4096;  // symbols per super-chunk (128 bitmap words)
+constexpr int NZ_FW = 4;     // warps per block
+
+__global__ void k_total_bits(const u64 *__restrict__ hist, const uint8_t *__restrict__ lengths,
+                             int nbins, cszi_ctl *ctl) {
+  __shared__ u64 ws[32];
+  u64 v = 0;
+  for (int i = threadIdx.x; i < nbins; i += blockDim.x) v += hist[i] * lengths[i];
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = (threadIdx.x < (blockDim.x >> 5)) ? ws[threadIdx.x] : 0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) ctl->bits = v;
+  }
+}
+
+// Super-chunk of the calling warp, last first: the densest super-chunks
+// (the far edge planes of the field, extrapolated) then start early instead
+// of forming the kernel's tail.
+DEV u64 nz_tile(u64 nsc) {
+  const u64 r = (u64)blockIdx.x * NZ_FW + (threadIdx.x >> 5);
+  return r < nsc ? nsc - 1 - r : nsc;
+}
+
+// The lane's 4 bitmap words of super-chunk t; returns the lane's set-bit count.
+DEV uint32_t nz_words(const uint32_t *__restrict__ nzmap, u64 n, u64 t, int lane,
+                      uint32_t wv[4]) {
+  const u64 nwords = n / 32, w0 = t * (NZ_SC / 32) + 4 * (u64)lane;
+  if (w0 + 4 <= nwords) {
+    const uint4 q = __ldcs(reinterpret_cast<const uint4 *>(nzmap + w0));
+    wv[0] = q.x, wv[1] = q.y, wv[2] = q.z, wv[3] = q.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) wv[i] = (w0 + i < nwords) ? nzmap[w0 + i] : 0u;
+  }
+  return __popc(wv[0]) + __popc(wv[1]) + __popc(wv[2]) + __popc(wv[3]);
+}
+
+// Calls f(j, symbol) for every set bit j (lane-local, increasing) of the
+// lane's 128 symbols at sp.  Per bitmap word the 16-byte groups holding set
+// bits are loaded together (one memory latency) and parked in the lane's
+// 64-byte shared-memory slot; the rolled loop over set bits reads them back
+// with one LDS each and keeps f to a single call site (an unrolled
+// per-symbol body overflows the instruction cache).
+template <class F>
+DEV void nz_visit(const uint16_t *__restrict__ sp, const uint32_t wv[4], uint4 *slot, F &&f) {
+  const uint16_t *s16 = reinterpret_cast<const uint16_t *>(slot);
+#pragma unroll 1
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t w = i == 0 ? wv[0] : i == 1 ? wv[1] : i == 2 ? wv[2] : wv[3];  // no local array
+    if (!w) continue;
+    uint4 q[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+      if ((w >> (8 * g)) & 0xffu) q[g] = __ldcs(reinterpret_cast<const uint4 *>(sp + 32 * i + 8 * g));
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+      if ((w >> (8 * g)) & 0xffu) slot[g] = q[g];
+#pragma unroll 1
+    for (uint32_t m = w; m; m &= m - 1) {
+      const uint32_t b = __ffs(m) - 1;
+      f(32 * i + b, (uint32_t)s16[b]);
+    }
+  }
+}
+
+// o_val[k] = x[o_idx[k] - idx_offset] for the outliers listed by k_enc_nz_emit
+__global__ void k_outlier_values(const u64 *__restrict__ o_idx, const float *__restrict__ xval,
+                                 float *__restrict__ o_val, u64 o_cap, u64 idx_offset,
+                                 const cszi_ctl *ctl) {
+  const u64 k = ctl->n_outliers < o_cap ? ctl->n_outliers : o_cap;
+  for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < k;
+       r += (u64)gridDim.x * blockDim.x)
+    o_val[r] = xval[o_idx[r] - idx_offset];
+}
+
+// Combining writer of one lane's codewords into the zeroed MSB-first
+// stream: bits of the same 32-bit word are merged in a register.  A lane's
+// range covers >= 128 bits, so only its first and last words can be shared
+// (with the neighbouring lanes): those are ORed in atomically, the words in
+// between are plain stores.
+struct WordOr {
+  uint32_t *out;
+  u64 cap_words;
+  u64 first;  // the lane's first word
+  u64 cur = ~0ull;
+  uint32_t acc = 0;
+  bool cap_hit = false;
+  DEV void put_word(u64 w, uint32_t v) {
+    if (w != cur) {
+      flush(false);
+      cur = w;
+    }
+    acc |= v;
+  }
+  DEV void flush(bool last) {
+    if (cur != ~0ull && acc) {
+      if (cur >= cap_words) cap_hit = true;
+      else if (last || cur == first) atomicOr(out + cur, bswap32(acc));
+      else out[cur] = bswap32(acc);
+    }
+    acc = 0;
+  }
+  DEV void put(u64 pos, uint32_t word, uint32_t len) {
+    const u64 w = pos >> 5;
+    const uint32_t off = (uint32_t)(pos & 31);
+    if (off + len <= 32) {
+      put_word(w, word << (32 - off - len));
+    } else {
+      const uint32_t sh = off + len - 32;
+      put_word(w, word >> sh);
+      put_word(w + 1, word << (32 - sh));
+    }
+  }
+};
+
+// per super-chunk: stream bits (R = 1 bit) and outliers -> S.ch_bits /
+// S.ch_out; per lane the exclusive prefixes (extra bits | outliers << 18)
+__global__ void __launch_bounds__(NZ_FW * 32) k_enc_nz_count(
+    const uint16_t *__restrict__ src, const uint32_t *__restrict__ nzmap, u64 n, int R,
+    const uint8_t *__restrict__ lengths, const uint32_t *__restrict__ words, EncScratch S,
+    u64 nsc, const cszi_ctl *ctl) {
+  const int lane = threadIdx.x & 31;
+  const u64 t = nz_tile(nsc);
+  if (t >= nsc) return;
+  uint32_t wv[4];
+  nz_words(nzmap, n, t, lane, wv);
+  if (!enc_sparse(lengths, words, R, n, ctl)) return;
+  __shared__ uint4 slots[NZ_FW * 32][4];
+  uint32_t ex = 0, o = 0;
+  nz_visit(src + t * NZ_SC + 128 * lane, wv, slots[threadIdx.x], [&](uint32_t, uint32_t s) {
+    ex += (uint32_t)__ldg(lengths + (s ? s : (uint32_t)R)) - 1u;  // outlier 0 is coded as R
+    o += s == 0;
+  });
+  // ex < 2^17 (128 symbols x 31 extra bits), o <= 128: one packed scan
+  const uint32_t v = ex | (o << 18);
+  const uint32_t incl = warp_incl_scan(v);
+  S.nz_lane[t * 32 + lane] = incl - v;
+  if (lane == 31) {
+    S.ch_bits[t] = (uint32_t)min((u64)NZ_SC, n - t * NZ_SC) + (incl & 0x3ffffu);
+    S.ch_out[t] = incl >> 18;
+  }
+}
+
+__global__ void __launch_bounds__(NZ_FW * 32) k_enc_nz_emit(
+    const uint16_t *__restrict__ src, const uint32_t *__restrict__ nzmap, u64 n, int R,
+    const uint8_t *__restrict__ lengths, const uint32_t *__restrict__ words,
+    uint32_t *__restrict__ out, u64 cap_words, const float *__restrict__ xval, u64 *o_idx,
+    float *o_val, u64 o_cap, EncScratch S, u64 nsc, u64 idx_offset, cszi_ctl *ctl,
+    uint32_t bit_base) {
+  const int lane = threadIdx.x & 31;
+  const u64 t = nz_tile(nsc);
+  if (t >= nsc) return;
+  uint32_t wv[4];
+  const uint32_t pc = nz_words(nzmap, n, t, lane, wv);
+  if (!enc_sparse(lengths, words, R, n, ctl)) return;
+  if (pc == 0) return;
+  const uint32_t lp = S.nz_lane[t * 32 + lane];
+  // bit_off counts whole symbols: lane-local symbol j starts at
+  // pos0 + j + (extra bits of the lane's codewords before it)
+  const u64 g0 = t * NZ_SC + 128 * (u64)lane;
+  const u64 pos0 = S.bit_off[t] + bit_base + 128 * (u64)lane + (lp & 0x3ffffu);
+  u64 ko = S.out_off[t] + (lp >> 18);
+  uint32_t extra = 0;
+  bool cap_hit = false;
+  WordOr wo{out, cap_words, pos0 >> 5};
+  __shared__ uint4 slots[NZ_FW * 32][4];
+  nz_visit(src + g0, wv, slots[threadIdx.x], [&](uint32_t j, uint32_t s) {
+    const uint32_t sI = s ? s : (uint32_t)R;
+    const uint32_t len = __ldg(lengths + sI), cw = __ldg(words + sI);
+    if (cw) wo.put(pos0 + j + extra, cw, len);
+    extra += len - 1;
+    if (s == 0) {  // values: k_outlier_values (a dependent load here stalls the lane)
+      if (ko < o_cap) o_idx[ko] = g0 + j + idx_offset;
+      else cap_hit = true;
+      ko++;
+    }
+  });
+  wo.flush(true);
+  if (cap_hit || wo.cap_hit) atomicOr(&ctl->flags, (uint32_t)CSZI_F_CAPACITY);
 }
 
 template <int MODE>
@@ -1285,15 +1491,18 @@ int launch_pack_outliers(const u64 *idx, const float *val, u64 k, uint8_t *out,
 u64 enc_scratch_bytes(u64 n) {
   const u64 nc = (n + ENC_CH - 1) / ENC_CH + 2;
   const u64 nt = (nc + PS_TILE - 1) / PS_TILE + 2;
-  return nc * (4 + 4 + 8 + 8 + 2 * 32) + nt * 16 + 64;
+  const u64 nsc = n / NZ_SC + 2;
+  return nc * (4 + 4 + 8 + 8 + 2 * 32) + nt * 16 + 64 + nsc * 4 * 32;
 }
 
 // mode 0: uint16 symbols with outlier sentinel; mode 1: int32 codes
 int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *lengths,
                   const uint32_t *words, uint32_t *out, u64 cap_bytes, const float *xval,
                   u64 *o_idx, float *o_val, u64 o_cap, void *scratch, cszi_ctl *ctl,
-                  cudaStream_t st, u64 idx_offset, uint32_t bit_base) {
+                  cudaStream_t st, u64 idx_offset, uint32_t bit_base,
+                  const uint32_t *nzmap, const u64 *hist) {
   if (n == 0) return CSZI_OK;
+  if (mode != 0 || (n & 31) || (reinterpret_cast<uintptr_t>(src) & 15)) nzmap = nullptr;
   const u64 nch = (n + ENC_CH - 1) / ENC_CH;
   const u64 nc = nch + 2;
   const u64 npt = (nch + PS_TILE - 1) / PS_TILE;
@@ -1308,6 +1517,7 @@ int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *length
   S.ch_bits = reinterpret_cast<uint32_t *>(S.out_off + nc);
   S.ch_out = S.ch_bits + nc;
   S.lane_pre = reinterpret_cast<uint16_t *>(S.ch_out + nc);
+  S.nz_lane = reinterpret_cast<uint32_t *>(S.lane_pre + 32 * nc);
   cudaMemsetAsync(p, 0, (size_t)(nt * 16 + 16), st);
   const int nbins = 2 * R;
   int dev = 0, sms = 148, per_sm = 1;
@@ -1323,8 +1533,18 @@ int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *length
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kc, ENC_NT, smem_c);
   u64 blocks = (u64)sms * (per_sm < 1 ? 1 : per_sm);
   if (blocks > wblocks) blocks = wblocks;
-  kc<<<(unsigned)blocks, ENC_NT, smem_c, st>>>(src, n, R, lengths, S, nch, ctl);
-  k_scan_pair<<<(unsigned)npt, PS_NT, 0, st>>>(S, nch, mode, out, cap_bytes / 4, ctl, bit_base);
+  // bitmap path: needs the bitmap and the histogram (stream length known
+  // up front); count / scan / pack over 1024-symbol chunks then run only
+  // for a dense stream, the k_enc_nz_* kernels only for a sparse one
+  const bool nzp = nzmap && hist;
+  if (nzp) {
+    k_total_bits<<<1, 1024, 0, st>>>(hist, lengths, nbins, ctl);
+    note_launch();
+  }
+  kc<<<(unsigned)blocks, ENC_NT, smem_c, st>>>(src, n, R, lengths, S, nch, ctl,
+                                               nzp ? words : nullptr);
+  k_scan_pair<<<(unsigned)npt, PS_NT, 0, st>>>(S, nch, mode, out, cap_bytes / 4, ctl, bit_base,
+                                                lengths, words, R, n, nzp ? 1 : 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, ENC_NT, smem_p);
   blocks = (u64)sms * (per_sm < 1 ? 1 : per_sm);
   if (blocks > wblocks) blocks = wblocks;
@@ -1336,14 +1556,30 @@ int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *length
     // sparse alternative (each kernel checks the same device-side predicate)
     k_enc_zero<<<(unsigned)(sms * 4), 256, 0, st>>>(lengths, words, R, n, out, cap_bytes / 4, ctl,
                                                     bit_base);
-    const size_t smem_s = sizeof(uint2) * (nbins + 2) + 16;
-    cudaFuncSetAttribute(k_enc_sparse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_enc_sparse, ENC_NT, smem_s);
-    blocks = (u64)sms * (per_sm < 1 ? 1 : per_sm);
-    if (blocks > wblocks) blocks = wblocks;
-    k_enc_sparse<<<(unsigned)blocks, ENC_NT, smem_s, st>>>(
-        reinterpret_cast<const uint16_t *>(src), n, R, lengths, words, out, cap_bytes / 4, xval,
-        o_idx, o_val, o_cap, S, nch, idx_offset, ctl, bit_base);
+    const auto *s16 = reinterpret_cast<const uint16_t *>(src);
+    if (nzp) {
+      const u64 nsc = (n + NZ_SC - 1) / NZ_SC;
+      const unsigned nb = (unsigned)((nsc + NZ_FW - 1) / NZ_FW);
+      k_enc_nz_count<<<nb, NZ_FW * 32, 0, st>>>(s16, nzmap, n, R, lengths, words, S, nsc, ctl);
+      k_scan_pair<<<(unsigned)((nsc + PS_TILE - 1) / PS_TILE), PS_NT, 0, st>>>(
+          S, nsc, mode, out, cap_bytes / 4, ctl, bit_base, lengths, words, R, n, 2);
+      k_enc_nz_emit<<<nb, NZ_FW * 32, 0, st>>>(s16, nzmap, n, R, lengths, words, out,
+                                               cap_bytes / 4, xval, o_idx, o_val, o_cap, S, nsc,
+                                               idx_offset, ctl, bit_base);
+      k_outlier_values<<<(unsigned)(sms * 8), 256, 0, st>>>(o_idx, xval, o_val, o_cap,
+                                                             idx_offset, ctl);
+      note_launch(3);
+    } else {
+      const size_t smem_s = sizeof(uint2) * (nbins + 2) + 16;
+      cudaFuncSetAttribute(k_enc_sparse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem_s);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_enc_sparse, ENC_NT, smem_s);
+      blocks = (u64)sms * (per_sm < 1 ? 1 : per_sm);
+      if (blocks > wblocks) blocks = wblocks;
+      k_enc_sparse<<<(unsigned)blocks, ENC_NT, smem_s, st>>>(
+          s16, n, R, lengths, words, out, cap_bytes / 4, xval, o_idx, o_val, o_cap, S, nch,
+          idx_offset, ctl, bit_base);
+    }
     note_launch(2);
   }
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;

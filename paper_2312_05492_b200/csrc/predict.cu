@@ -834,9 +834,11 @@ static int launch_recon_fast(const uint16_t *sym, const float *anchors, const u6
 }
 
 int launch_predict(const float *x, const cszi_geom *g, int32_t radius, const cszi_ctl *ctl,
-                   uint16_t *sym, u64 *hist, bool exact, cudaStream_t st) {
+                   uint16_t *sym, u64 *hist, bool exact, cudaStream_t st, uint32_t *nzmap,
+                   bool *nz_done) {
+  if (nz_done) *nz_done = false;
   if (g->rank == 3 && layout_is<fast::L3>(g) && !getenv("CSZI_OLD_PREDICT"))
-    return t3::launch_predict_t3(x, g, radius, ctl, sym, hist, exact, st);
+    return t3::launch_predict_t3(x, g, radius, ctl, sym, hist, exact, st, nzmap, nz_done);
   if (g->rank == 3 && layout_is<fast::L3>(g))
     return launch_predict_fast<fast::L3, 128>(x, g, radius, ctl, sym, hist, exact, st);
   if (g->rank == 2 && layout_is<fast::L2>(g))

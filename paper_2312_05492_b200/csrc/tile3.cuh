@@ -57,7 +57,8 @@ constexpr int NW = 4;                           // warps (tiles) per CTA
 constexpr int NT = NW * 32;
 // per-warp shared regions (128-byte aligned for the TMA destinations)
 constexpr int BUF_BYTES = NBUF * 4;                              // 11664
-constexpr int P_WARP = ((BUF_BYTES + NCODE * 2) + 127) & ~127;   // 16384
+constexpr int NZ_BYTES = TZ * TY * 4;  // non-R bitmap words of a tile's rows
+constexpr int P_WARP = ((BUF_BYTES + NCODE * 2 + NZ_BYTES) + 127) & ~127;   // 16640
 constexpr int SYM_BYTES = ((NSYM * 2) + 127) & ~127;             // 6528
 constexpr int R_WARP = ((SYM_BYTES + BUF_BYTES) + 127) & ~127;   // 18304
 
@@ -161,6 +162,11 @@ DEV void sts_f4(uint32_t a, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
                "f"(v.w)
                : "memory");
+}
+// bit 0: low code of a packed pair differs from R; bit 1: high code does
+DEV uint32_t ne_r2(uint32_t w, uint32_t rr) {
+  const uint32_t d = w ^ rr;
+  return (uint32_t)((d & 0xffffu) != 0u) | ((uint32_t)(d > 0xffffu) << 1);
 }
 DEV uint32_t lds_u16(uint32_t a) {
   unsigned short v;
@@ -849,7 +855,7 @@ DEV void sched_done(unsigned int *q) {
 __global__ void __launch_bounds__(NT, 3)
     k_t3_predict(const __grid_constant__ CUtensorMap tm, const float *__restrict__ x, Geo G,
                  const cszi_ctl *__restrict__ ctl, uint16_t *__restrict__ sym,
-                 u64 *__restrict__ hist, int slot) {
+                 u64 *__restrict__ hist, uint32_t *__restrict__ nzmap, int slot) {
   extern __shared__ __align__(128) unsigned char t3_smem[];
   __shared__ Cfg C;
   __shared__ uint64_t mbar[NW];
@@ -860,6 +866,7 @@ __global__ void __launch_bounds__(NT, 3)
   uint32_t *hs = reinterpret_cast<uint32_t *>(sm + NW * P_WARP);
   const uint32_t buf = smem_u32(sm + warp * P_WARP);
   const uint32_t codes = buf + BUF_BYTES;
+  uint32_t *nzs = reinterpret_cast<uint32_t *>(sm + warp * P_WARP + BUF_BYTES + NCODE * 2);
   const int nint = tile_count<false>(G);
   const int ntiles = nint + tile_count<true>(G);
   unsigned int *q = g_t3_sched + 2 * slot;
@@ -906,6 +913,10 @@ __global__ void __launch_bounds__(NT, 3)
     tile_init(T, G, o, t >= nint);
     // codes default to R (anchors: code 0, predictor.py:414)
     for (int i = lane; i < NCODE / 8; i += 32) sts_u4(codes + 16u * i, make_uint4(rr, rr, rr, rr));
+    if (nzmap) {
+      nzs[lane] = 0u;
+      nzs[lane + 32] = 0u;
+    }
     T3P_CLOCK(c1);
     if (G.tma) {
       mbar_wait(&mbar[warp], phase);
@@ -939,12 +950,19 @@ __global__ void __launch_bounds__(NT, 3)
         const uint32_t src = codea(T, z, y, 8 * c);
         const uint2 a = lds_u2(src);
         const uint2 b = lds_u2(src + 8);
-        __stcs(reinterpret_cast<uint4 *>(sym + gbase + z * pz + (int64_t)y * py + 8 * c),
-               make_uint4(a.x, a.y, b.x, b.y));
+        const int64_t g0 = gbase + z * pz + (int64_t)y * py;
+        __stcs(reinterpret_cast<uint4 *>(sym + g0 + 8 * c), make_uint4(a.x, a.y, b.x, b.y));
         if (((a.x ^ rr) | (a.y ^ rr) | (b.x ^ rr) | (b.y ^ rr)) == 0) {
           zeros += 8;
           continue;
         }
+        // non-R bit per code (outliers included) for the sparse encoder: the
+        // map is zeroed beforehand and only groups holding a non-R code (~5%
+        // on smooth fields) OR their byte into the row's word
+        if (nzmap)
+          atomicOr(&nzs[row], (ne_r2(a.x, rr) | (ne_r2(a.y, rr) << 2) | (ne_r2(b.x, rr) << 4) |
+                               (ne_r2(b.y, rr) << 6))
+                                  << (8 * c));
         const uint32_t w[4] = {a.x, a.y, b.x, b.y};
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
@@ -961,12 +979,25 @@ __global__ void __launch_bounds__(NT, 3)
           }
         }
       }
+      if (nzmap) {  // rows with a non-R code -> the zeroed global map
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int row = lane + 32 * h;
+          const uint32_t wd = nzs[row];
+          if (wd) nzmap[(gbase + (row >> 3) * pz + (int64_t)(row & 7) * py) >> 5] = wd;
+        }
+      }
     } else {
       for (int i = lane; i < O0 * O1 * O2; i += 32) {
         const int row = i / O2, xx = i - row * O2;
         const int z = row / O1, y = row - z * O1;
         const uint32_t sy = lds_u16(codea(T, z, y, xx));
         sym[gbase + z * pz + (int64_t)y * py + xx] = (uint16_t)sy;
+        if (nzmap) {  // O2 == 32 whenever nzmap is set: one row per iteration
+          const uint32_t wd = __ballot_sync(CSZI_FULL, sy != (uint32_t)R);
+          if (lane == 0 && wd) nzmap[(gbase + z * pz + (int64_t)y * py) >> 5] = wd;
+        }
         if (sy == (uint32_t)R || sy == 0) zeros++;
         else if (G.hist_smem) atomicAdd(&hs[sy], 1u);
         else atomicAdd(&hist[sy], 1ull);
@@ -1222,9 +1253,13 @@ static bool t3_geo(const cszi_geom *g, int32_t radius, Geo &G) {
 
 static int launch_predict_t3(const float *x, const cszi_geom *g, int32_t radius,
                              const cszi_ctl *ctl, uint16_t *sym, u64 *hist, bool exact,
-                             cudaStream_t st) {
+                             cudaStream_t st, uint32_t *nzmap, bool *nz_done) {
   Geo G;
   if (!t3_geo(g, radius, G)) return CSZI_E_UNSUPPORTED;
+  // the non-R bitmap needs every tile row to be one aligned 32-code word
+  if (G.ext[2] % 32 != 0 || getenv("CSZI_NO_NZ")) nzmap = nullptr;
+  if (nz_done) *nz_done = nzmap != nullptr;
+  if (nzmap) cudaMemsetAsync(nzmap, 0, (size_t)G.nzl * G.ext[1] * G.ext[2] / 8, st);
   G.exact = exact ? 1 : 0;
   CUtensorMap tm;
   G.tma = make_tmap(&tm, x, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, G.ext[2], G.ext[1], G.nzl, PX)
@@ -1235,7 +1270,7 @@ static int launch_predict_t3(const float *x, const cszi_geom *g, int32_t radius,
       128 + (size_t)NW * P_WARP + (G.hist_smem ? sizeof(uint32_t) * 2 * radius : 0);
   cudaFuncSetAttribute(k_t3_predict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const unsigned grid = persistent_grid((const void *)k_t3_predict, smem, nall);
-  k_t3_predict<<<grid, NT, smem, st>>>(tm, x, G, ctl, sym, hist, sched_slot());
+  k_t3_predict<<<grid, NT, smem, st>>>(tm, x, G, ctl, sym, hist, nzmap, sched_slot());
   note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
