@@ -179,6 +179,10 @@ int cszi_decompress(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
 
 /* ctl := initial state (range keys reset, counters and flags zero). */
 int cszi_ctl_init(cszi_ctl *ctl, void *stream);
+/* Stream-ordered copy of a device ctl into host memory (pinned for an
+ * asynchronous copy) followed by a stream synchronisation: the one host
+ * read-back of a compress / decompress call. */
+int cszi_ctl_fetch(const cszi_ctl *ctl, cszi_ctl *host, void *stream);
 
 /* value_range + finite scan (grid.py:60-62, :104-108) into ctl. */
 int cszi_range(const float *x, uint64_t n, cszi_ctl *ctl, void *stream);

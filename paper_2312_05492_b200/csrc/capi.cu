@@ -3,6 +3,9 @@
 // (pipeline.py:66-204).  No exceptions cross the ABI; no host sync inside.
 #include <algorithm>
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cstring>
 
 #include "common.cuh"
@@ -258,9 +261,7 @@ static u64 layout_decompress(const cszi_geom *g, int32_t R, const u64 sec[4], u6
 }
 
 static int grid_for(u64 work) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = sm_count();
   u64 b = (work + 255) / 256;
   if (b > (u64)sms * 8) b = (u64)sms * 8;
   if (b < 1) b = 1;
@@ -281,6 +282,47 @@ static int check_geom(const cszi_geom *g, int32_t R) {
   if (R < 2) return CSZI_E_INVALID_ARG;
   if (2 * (int64_t)R > 16384) return CSZI_E_UNSUPPORTED;  // uint16 symbols + codebook kernel
   return CSZI_OK;
+}
+
+static std::mutex g_cache_mu;
+static int g_sms[64];
+static std::map<std::pair<int, const void *>, size_t> g_smem_set;
+static std::map<std::tuple<int, const void *, int, size_t>, int> g_occ;
+
+int sm_count() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && g_sms[dev]) return g_sms[dev];
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (dev >= 0 && dev < 64) g_sms[dev] = sms;
+  return sms;
+}
+
+void ensure_smem(const void *fn, size_t smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  size_t &cur = g_smem_set[{dev, fn}];
+  if (smem > cur || cur == 0) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (smem > cur) cur = smem;
+  }
+}
+
+int occupancy(const void *fn, int threads, size_t smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  const auto key = std::make_tuple(dev, fn, threads, smem);
+  auto it = g_occ.find(key);
+  if (it != g_occ.end()) return it->second;
+  int per = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, smem) != cudaSuccess ||
+      per < 1)
+    per = 1;
+  g_occ[key] = per;
+  return per;
 }
 
 static std::atomic<unsigned long long> g_launches{0};
@@ -401,6 +443,14 @@ int cszi_decompress(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
                         reinterpret_cast<const u64 *>(&ctl->n_outliers), g, radius, level_eb,
                         nlev, variant, order, y, st));
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
+int cszi_ctl_fetch(const cszi_ctl *ctl, cszi_ctl *host, void *stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaMemcpyAsync(host, ctl, sizeof(cszi_ctl), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return CSZI_E_CUDA;
+  return CSZI_OK;
 }
 
 int cszi_ctl_init(cszi_ctl *ctl, void *stream) {

@@ -17,6 +17,13 @@ typedef unsigned long long u64;
 
 // Host-side count of kernels this library launched (cszi_launch_count()).
 void note_launch(int n = 1);
+// Host-side launch helpers with per-device caches (the runtime queries cost
+// microseconds of CPU each, and the GPU idles while the host launches the
+// first kernels of a call): SM count, the dynamic shared-memory opt-in
+// (raised only when a larger size is requested) and occupancy.
+int sm_count();
+void ensure_smem(const void *fn, size_t smem);
+int occupancy(const void *fn, int threads, size_t smem);
 
 // ---------------------------------------------------------------------------
 // memory-model helpers (release/acquire at gpu scope)

@@ -1421,7 +1421,7 @@ int launch_codebook(const u64 *hist, int nbins, uint8_t *lengths, uint32_t *word
   while (npow2 < nbins) npow2 <<= 1;
   // keys[npow2] + parent[2*nbins] + len[nbins] + internal keys / depths
   const size_t smem = sizeof(u64) * (npow2 + nbins) + sizeof(int32_t) * 3 * nbins + nbins + 16;
-  cudaFuncSetAttribute(k_codebook, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  ensure_smem((const void *)k_codebook, smem);
   k_codebook<<<1, CB_NT, smem, st>>>(hist, nbins, lengths, words, ctl);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
@@ -1433,7 +1433,7 @@ int launch_canonical(const uint8_t *lengths, int nbins, uint32_t *words, void *d
                      cszi_ctl *ctl, cudaStream_t st) {
   if (nbins > 65536 || nbins < 1) return CSZI_E_UNSUPPORTED;
   const size_t smem = nbins + 16;
-  cudaFuncSetAttribute(k_canonical, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  ensure_smem((const void *)k_canonical, smem);
   k_canonical<<<1, CB_NT, smem, st>>>(lengths, nbins, words,
                                       reinterpret_cast<DecTables *>(dec_tables), ctl);
   note_launch();
@@ -1520,17 +1520,15 @@ int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *length
   S.nz_lane = reinterpret_cast<uint32_t *>(S.lane_pre + 32 * nc);
   cudaMemsetAsync(p, 0, (size_t)(nt * 16 + 16), st);
   const int nbins = 2 * R;
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int sms = sm_count(), per_sm = 1;
   const size_t smem_c = sizeof(uint32_t) * (nbins + 2) + 16;
   const size_t smem_p = sizeof(uint2) * (nbins + 2) + 16 + sizeof(uint32_t) * ENC_SW * ENC_NW;
   auto kc = mode == 0 ? k_enc_count<0> : k_enc_count<1>;
   auto kp = mode == 0 ? k_enc_pack<0> : k_enc_pack<1>;
-  cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c);
-  cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p);
+  ensure_smem((const void *)kc, smem_c);
+  ensure_smem((const void *)kp, smem_p);
   const u64 wblocks = (nch + ENC_NW - 1) / ENC_NW;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kc, ENC_NT, smem_c);
+  per_sm = occupancy((const void *)kc, ENC_NT, smem_c);
   u64 blocks = (u64)sms * (per_sm < 1 ? 1 : per_sm);
   if (blocks > wblocks) blocks = wblocks;
   // bitmap path: needs the bitmap and the histogram (stream length known
@@ -1545,7 +1543,7 @@ int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *length
                                                nzp ? words : nullptr);
   k_scan_pair<<<(unsigned)npt, PS_NT, 0, st>>>(S, nch, mode, out, cap_bytes / 4, ctl, bit_base,
                                                 lengths, words, R, n, nzp ? 1 : 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, ENC_NT, smem_p);
+  per_sm = occupancy((const void *)kp, ENC_NT, smem_p);
   blocks = (u64)sms * (per_sm < 1 ? 1 : per_sm);
   if (blocks > wblocks) blocks = wblocks;
   kp<<<(unsigned)blocks, ENC_NT, smem_p, st>>>(src, n, R, lengths, words, out, cap_bytes / 4,
@@ -1571,9 +1569,8 @@ int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *length
       note_launch(3);
     } else {
       const size_t smem_s = sizeof(uint2) * (nbins + 2) + 16;
-      cudaFuncSetAttribute(k_enc_sparse, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem_s);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_enc_sparse, ENC_NT, smem_s);
+      ensure_smem((const void *)k_enc_sparse, smem_s);
+      per_sm = occupancy((const void *)k_enc_sparse, ENC_NT, smem_s);
       blocks = (u64)sms * (per_sm < 1 ? 1 : per_sm);
       if (blocks > wblocks) blocks = wblocks;
       k_enc_sparse<<<(unsigned)blocks, ENC_NT, smem_s, st>>>(

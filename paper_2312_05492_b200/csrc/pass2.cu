@@ -344,10 +344,8 @@ int launch_pass2_encode(const uint8_t *in, const u64 *Np, u64 cap_n, uint8_t *ou
   S.rest = S.fs + nc;
   S.lit0 = reinterpret_cast<uint8_t *>(S.rest + nc);
   cudaMemsetAsync(p, 0, (size_t)(nt * 16 + 16), st);
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_p2_emit, P2_NT, 0);
+  int sms = sm_count(), per_sm = 1;
+  per_sm = occupancy((const void *)k_p2_emit, P2_NT, 0);
   if (per_sm < 1) per_sm = 1;
   u64 grid = (u64)sms * per_sm;
   const u64 wb = (nc + P2_NW - 1) / P2_NW;

@@ -752,12 +752,12 @@ static int launch_predict_t(const float *x, const cszi_geom *g, int32_t radius,
   if (nblk > 0x7fffffffLL) return CSZI_E_UNSUPPORTED;
   if (exact) {
     auto k = k_predict<BZ, BY, BX, CSZI_NT, true>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem((const void *)k, smem);
     k<<<(unsigned)nblk, CSZI_NT, smem, st>>>(x, P, ctl, sym, hist, hsm ? 1 : 0);
     note_launch();
   } else {
     auto k = k_predict<BZ, BY, BX, CSZI_NT, false>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem((const void *)k, smem);
     k<<<(unsigned)nblk, CSZI_NT, smem, st>>>(x, P, ctl, sym, hist, hsm ? 1 : 0);
     note_launch();
   }
@@ -776,7 +776,7 @@ static int launch_recon_t(const uint16_t *sym, const float *anchors, const u64 *
   const int64_t nblk = (int64_t)P.nb[0] * P.nb[1] * P.nb[2];
   if (nblk > 0x7fffffffLL) return CSZI_E_UNSUPPORTED;
   auto k = k_reconstruct<BZ, BY, BX, CSZI_NT>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  ensure_smem((const void *)k, smem);
   k<<<(unsigned)nblk, CSZI_NT, smem, st>>>(sym, anchors, oidx, oval, nout, nout_dev, P, lc, y);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
@@ -805,11 +805,11 @@ static int launch_predict_fast(const float *x, const cszi_geom *g, int32_t radiu
   if (nblk > 0x7fffffffLL) return CSZI_E_UNSUPPORTED;
   if (exact) {
     auto k = k_predict_fast<LY, NT, true>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem((const void *)k, smem);
     k<<<(unsigned)nblk, NT, smem, st>>>(x, P, ctl, sym, hist, hsm ? 1 : 0);
   } else {
     auto k = k_predict_fast<LY, NT, false>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem((const void *)k, smem);
     k<<<(unsigned)nblk, NT, smem, st>>>(x, P, ctl, sym, hist, hsm ? 1 : 0);
   }
   note_launch();
@@ -827,7 +827,7 @@ static int launch_recon_fast(const uint16_t *sym, const float *anchors, const u6
   const int64_t nblk = (int64_t)P.nb[0] * P.nb[1] * P.nb[2];
   if (nblk > 0x7fffffffLL) return CSZI_E_UNSUPPORTED;
   auto k = k_reconstruct_fast<LY, NT>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  ensure_smem((const void *)k, smem);
   k<<<(unsigned)nblk, NT, smem, st>>>(sym, anchors, oidx, oval, nout, nout_dev, P, lc, y);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;

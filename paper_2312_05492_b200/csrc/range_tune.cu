@@ -317,9 +317,7 @@ int launch_ctl_init(cszi_ctl *ctl, cudaStream_t st) {
 }
 
 int launch_range(const float *x, uint64_t n, cszi_ctl *ctl, cudaStream_t st) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = sm_count();
   u64 blocks = (n / 4 + 255) / 256;
   const u64 cap = (u64)sms * 8;
   if (blocks > cap) blocks = cap;

@@ -1192,11 +1192,7 @@ static bool make_tmap(CUtensorMap *tm, const void *base, CUtensorMapDataType dt,
 
 // resident CTAs x SMs, capped by the tile count
 static unsigned persistent_grid(const void *k, size_t smem, int64_t ntiles) {
-  int dev = 0, sms = 148, per = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, NT, smem) != cudaSuccess || per < 1)
-    per = 1;
+  const int sms = sm_count(), per = occupancy(k, NT, smem);
   const int64_t need = (ntiles + NW - 1) / NW;
   const int64_t cap = (int64_t)per * sms;
   return (unsigned)(need < cap ? need : cap);
@@ -1268,7 +1264,7 @@ static int launch_predict_t3(const float *x, const cszi_geom *g, int32_t radius,
   const int64_t nall = (int64_t)G.nt[0] * G.nt[1] * G.nt[2];
   const size_t smem =
       128 + (size_t)NW * P_WARP + (G.hist_smem ? sizeof(uint32_t) * 2 * radius : 0);
-  cudaFuncSetAttribute(k_t3_predict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  ensure_smem((const void *)k_t3_predict, smem);
   const unsigned grid = persistent_grid((const void *)k_t3_predict, smem, nall);
   k_t3_predict<<<grid, NT, smem, st>>>(tm, x, G, ctl, sym, hist, nzmap, sched_slot());
   note_launch();
@@ -1286,8 +1282,7 @@ static int launch_recon_t3(const uint16_t *sym, const float *anchors, const u64 
               : 0;
   const int64_t nall = (int64_t)G.nt[0] * G.nt[1] * G.nt[2];
   const size_t smem = 128 + (size_t)NW * R_WARP;
-  cudaFuncSetAttribute(k_t3_reconstruct, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)smem);
+  ensure_smem((const void *)k_t3_reconstruct, smem);
   const unsigned grid = persistent_grid((const void *)k_t3_reconstruct, smem, nall);
   k_t3_reconstruct<<<grid, NT, smem, st>>>(tm, sym, anchors, oidx, oval, nout, nout_dev, G, lc,
                                            y, sched_slot());

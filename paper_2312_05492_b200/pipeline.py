@@ -117,6 +117,34 @@ def _caps_for(n: int, worst: bool) -> _lib.Caps:
     return c
 
 
+_prep_cache = {}
+
+
+def _compress_prep(extents, layout, rel, eb, R, a, variants, dim_order, exact, worst):
+    """(params, geom, caps, workspace bytes, payload capacity) of a compress
+    call, memoised: the structs are read-only inputs of cszi_compress, and
+    building them sits between the caller and the first kernel launch."""
+    key = (extents, layout.anchor_stride, rel, eb, R, a, variants, dim_order, exact, worst)
+    hit = _prep_cache.get(key)
+    if hit is not None:
+        return hit
+    lib = _lib.load()
+    rank = len(extents)
+    params = make_params(rank, rel, eb, R, a, layout.anchor_stride, variants, dim_order, exact)
+    geom = make_geom(extents, layout)
+    n = 1
+    for e in extents:
+        n *= e
+    caps = _caps_for(n, worst)
+    ws_bytes = int(lib.cszi_compress_workspace_size(ctypes.byref(geom), R, ctypes.byref(caps)))
+    pcap = int(lib.cszi_payload_capacity(ctypes.byref(geom), R, ctypes.byref(caps)))
+    if len(_prep_cache) > 256:
+        _prep_cache.clear()
+    hit = (params, geom, caps, ws_bytes, pcap)
+    _prep_cache[key] = hit
+    return hit
+
+
 def compress_device(grid: Grid, eb: float, mode: str = "rel", predictor: str = "interp",
                     pass2: bool = True, pass2_codec: int = DEFAULT_CODEC, alpha: float = None,
                     variants=None, dim_order=None, quant_radius: int = 512,
@@ -177,17 +205,14 @@ def compress_device(grid: Grid, eb: float, mode: str = "rel", predictor: str = "
         rng = key_to_float(c0.vmax_key) - key_to_float(c0.vmin_key)
         eb_abs = float(eb)
         a = compute_alpha(eb_abs / rng if rng > 0 else eb_abs)
-    params = make_params(rank, mode == "rel", float(eb), R, a, layout.anchor_stride, variants,
-                         dim_order, exact)
-    geom = make_geom(grid.dims.extents, layout)
     dev_pass2 = 1 if (pass2 and codec_enc is None) else 0
     worst = _caps_hint.get(n, False)
     while True:
-        caps = _caps_for(n, worst)
-        ws_bytes = int(lib.cszi_compress_workspace_size(ctypes.byref(geom), R, ctypes.byref(caps)))
+        params, geom, caps, ws_bytes, pcap = _compress_prep(
+            grid.dims.extents, layout, mode == "rel", float(eb), R, a, variants, dim_order,
+            bool(exact), worst)
         ws = _lib.WS.get(ws_bytes, "compress")
-        pay = _payload_buf(int(lib.cszi_payload_capacity(ctypes.byref(geom), R,
-                                                             ctypes.byref(caps))))
+        pay = _payload_buf(pcap)
         _lib.check(lib.cszi_compress(_lib.ptr(x), ctypes.byref(geom), ctypes.byref(params),
                                      ctypes.byref(caps), dev_pass2, 1 if range_done else 0,
                                      _lib.ptr(pay), _lib.ptr(ws), ws.numel(), ctl.ptr, st),

@@ -70,3 +70,13 @@ def test_outlier_heavy_and_exact_paths():
     g = P.Grid(P.Dims(data.shape), data)
     a = P.compress_device(g, 1e-4, exact=True).to_bytes()
     assert a == O.compress(data, 1e-4)
+
+
+@pytest.mark.parametrize("shape", [(37, 21, 64), (9, 15, 96), (70, 8, 32)])
+def test_nonr_bitmap_encoder(shape):
+    # nx % 32 == 0: the predictor writes the non-R bitmap and the sparse
+    # stream is encoded from it; partial z / y tiles take the edge epilogue
+    data = _smooth(shape, seed=7, noise=0.001)
+    data[shape[0] // 2, 3, 5] = 40.0  # one outlier
+    for eb in (1e-3, 1e-2):
+        _round_trip_equals_oracle(data, eb)

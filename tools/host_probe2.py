@@ -13,6 +13,13 @@ def t(name, fn, n=200):
     for _ in range(n): fn()
     torch.cuda.synchronize(); print(f"{name:28s} {1e6*(time.perf_counter()-t0)/n:8.1f} us")
 t("DeviceCtl()", lambda: _lib.DeviceCtl())
+t("stream_ptr()", lambda: _lib.stream_ptr())
+t("torch current_stream", lambda: torch.cuda.current_stream().cuda_stream)
+t("current_device()", lambda: torch.cuda.current_device())
+t("x.contiguous()", lambda: x.contiguous())
+t("lib.load()", lambda: _lib.load())
+t("P.Dims(shape)", lambda: P.Dims(x.shape))
+t("_lib.ptr(x)", lambda: _lib.ptr(x))
 t("ctl_init launch", lambda: lib.cszi_ctl_init(ctl.ptr, st))
 t("fetch()", lambda: ctl.fetch())
 t("stream.synchronize()", lambda: torch.cuda.current_stream().synchronize())
