@@ -73,9 +73,11 @@ __global__ void k_ctl_reset_outputs(cszi_ctl *ctl) {
 
 // Sections after the anchors and codebook: bitstream bytes, then the
 // outlier section (archive.py:184-189: u64 count + packed (u64, f32)).
+// oval == nullptr: the values are gathered from the field x (the bitmap
+// encode lists only the outlier indices)
 __global__ void k_assemble(uint8_t *raw, u64 head, const uint8_t *bits, const u64 *oidx,
-                           const float *oval, u64 raw_cap, u64 bits_cap, u64 o_cap,
-                           cszi_ctl *ctl, int is_payload, int bits_in_place) {
+                           const float *oval, const float *x, u64 raw_cap, u64 bits_cap,
+                           u64 o_cap, cszi_ctl *ctl, int is_payload, int bits_in_place) {
   const u64 nbits = ctl->bits;
   const u64 k = ctl->n_outliers;
   const u64 nbytes = (nbits + 7) / 8;
@@ -95,7 +97,7 @@ __global__ void k_assemble(uint8_t *raw, u64 head, const uint8_t *bits, const u6
   for (u64 r = tid; r < k; r += nthr) {
     uint8_t *q = os + 8 + 12 * r;
     const u64 ix = oidx[r];
-    const uint32_t vb = __float_as_uint(oval[r]);
+    const uint32_t vb = __float_as_uint(oval ? oval[r] : x[ix]);
 #pragma unroll
     for (int b = 0; b < 8; ++b) q[b] = (uint8_t)(ix >> (8 * b));
 #pragma unroll
@@ -384,7 +386,8 @@ int cszi_compress(const float *x, const cszi_geom *g, const cszi_params *p,
                    caps->outlier_cap, W.enc_scratch, ctl, st, 0, 0, nz ? W.nzmap : nullptr,
                    W.hist));
   k_assemble<<<grid_for(n / 16), 256, 0, st>>>(raw, head, reinterpret_cast<uint8_t *>(W.bits),
-                                                W.oidx, W.oval, raw_cap, caps->bits_cap,
+                                                W.oidx, nz ? nullptr : W.oval, x, raw_cap,
+                                                caps->bits_cap,
                                                 caps->outlier_cap, ctl, pass2 ? 0 : 1,
                                                 in_place ? 1 : 0);
   note_launch();

@@ -186,20 +186,20 @@ __global__ void __launch_bounds__(CB_NT) k_codebook(const u64 *__restrict__ hist
     overflow = 0;
   }
   __syncthreads();
-  for (int s = threadIdx.x; s < npow2; s += blockDim.x) {
-    u64 k = ~0ull;
-    if (s < nbins) {
-      const u64 f = hist[s];
-      len_s[s] = 0;
-      if (f) {
-        k = (f << 16) | (u64)s;
-        atomicAdd(&alive, 1);
-      }
-    }
-    keys[s] = k;
+  // compact the non-empty bins (any order: they are sorted next), so the
+  // sort runs over the next power of two of the leaf count (31 leaves at
+  // the bench's 1e-3) instead of all 2R bins
+  for (int s = threadIdx.x; s < nbins; s += blockDim.x) {
+    const u64 f = hist[s];
+    len_s[s] = 0;
+    if (f) keys[atomicAdd(&alive, 1)] = (f << 16) | (u64)s;
   }
   __syncthreads();
   const int m = alive;
+  int mp2 = 1;
+  while (mp2 < m) mp2 <<= 1;
+  for (int s = m + threadIdx.x; s < mp2; s += blockDim.x) keys[s] = ~0ull;
+  __syncthreads();
   if (m == 0) {
     if (threadIdx.x == 0) ctl->flags |= CSZI_F_EMPTY_HISTOGRAM;
     for (int s = threadIdx.x; s < nbins; s += blockDim.x) {
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(CB_NT) k_codebook(const u64 *__restrict__ hist
     }
     return;
   }
-  bitonic_sort_u64(keys, npow2);
+  bitonic_sort_u64(keys, mp2);
   // keys[0..m) = leaves sorted by (freq, symbol); leaf i is node i,
   // internal node k (creation order) is node m + k.
   if (threadIdx.x == 0) {
@@ -511,9 +511,8 @@ __global__ void __launch_bounds__(PS_NT) k_scan_pair(EncScratch S, u64 nch, int 
   }
 }
 
-__global__ void k_enc_zero(const uint8_t *lengths, const uint32_t *words, int R, u64 n,
-                           uint32_t *out, u64 cap_words, const cszi_ctl *ctl, uint32_t bit_base) {
-  if (!enc_sparse(lengths, words, R, n, ctl)) return;
+// zero the sparse stream's words [0, bits + bit_base + 1 word), grid-strided
+DEV void zero_stream(uint32_t *out, u64 cap_words, const cszi_ctl *ctl, uint32_t bit_base) {
   u64 nw = (ctl->bits + bit_base + 31) / 32 + 1;
   if (nw > cap_words) nw = cap_words;
   // words up to the first 16-byte boundary, then 16-byte stores
@@ -525,6 +524,12 @@ __global__ void k_enc_zero(const uint8_t *lengths, const uint32_t *words, int R,
   const u64 nv = (nw - lead) / 4;
   for (u64 i = tid; i < nv; i += nthr) o4[i] = make_uint4(0, 0, 0, 0);
   for (u64 i = lead + nv * 4 + tid; i < nw; i += nthr) out[i] = 0u;
+}
+
+__global__ void k_enc_zero(const uint8_t *lengths, const uint32_t *words, int R, u64 n,
+                           uint32_t *out, u64 cap_words, const cszi_ctl *ctl, uint32_t bit_base) {
+  if (!enc_sparse(lengths, words, R, n, ctl)) return;
+  zero_stream(out, cap_words, ctl, bit_base);
 }
 
 // OR one codeword (word, len) into the zeroed MSB-first stream at bit pos.
@@ -689,16 +694,6 @@ DEV void nz_visit(const uint16_t *__restrict__ sp, const uint32_t wv[4], uint4 *
   }
 }
 
-// o_val[k] = x[o_idx[k] - idx_offset] for the outliers listed by k_enc_nz_emit
-__global__ void k_outlier_values(const u64 *__restrict__ o_idx, const float *__restrict__ xval,
-                                 float *__restrict__ o_val, u64 o_cap, u64 idx_offset,
-                                 const cszi_ctl *ctl) {
-  const u64 k = ctl->n_outliers < o_cap ? ctl->n_outliers : o_cap;
-  for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < k;
-       r += (u64)gridDim.x * blockDim.x)
-    o_val[r] = xval[o_idx[r] - idx_offset];
-}
-
 // Combining writer of one lane's codewords into the zeroed MSB-first
 // stream: bits of the same 32-bit word are merged in a register.  A lane's
 // range covers >= 128 bits, so only its first and last words can be shared
@@ -744,13 +739,14 @@ struct WordOr {
 __global__ void __launch_bounds__(NZ_FW * 32) k_enc_nz_count(
     const uint16_t *__restrict__ src, const uint32_t *__restrict__ nzmap, u64 n, int R,
     const uint8_t *__restrict__ lengths, const uint32_t *__restrict__ words, EncScratch S,
-    u64 nsc, const cszi_ctl *ctl) {
+    u64 nsc, const cszi_ctl *ctl, uint32_t *out, u64 cap_words, uint32_t bit_base) {
   const int lane = threadIdx.x & 31;
+  if (!enc_sparse(lengths, words, R, n, ctl)) return;
+  zero_stream(out, cap_words, ctl, bit_base);  // (k_enc_zero's job, one launch less)
   const u64 t = nz_tile(nsc);
   if (t >= nsc) return;
   uint32_t wv[4];
   nz_words(nzmap, n, t, lane, wv);
-  if (!enc_sparse(lengths, words, R, n, ctl)) return;
   __shared__ uint4 slots[NZ_FW * 32][4];
   uint32_t ex = 0, o = 0;
   nz_visit(src + t * NZ_SC + 128 * lane, wv, slots[threadIdx.x], [&](uint32_t, uint32_t s) {
@@ -1552,21 +1548,22 @@ int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *length
   note_launch(3);
   if (mode == 0) {
     // sparse alternative (each kernel checks the same device-side predicate)
-    k_enc_zero<<<(unsigned)(sms * 4), 256, 0, st>>>(lengths, words, R, n, out, cap_bytes / 4, ctl,
-                                                    bit_base);
+    if (!nzp)
+      k_enc_zero<<<(unsigned)(sms * 4), 256, 0, st>>>(lengths, words, R, n, out, cap_bytes / 4,
+                                                      ctl, bit_base);
     const auto *s16 = reinterpret_cast<const uint16_t *>(src);
     if (nzp) {
       const u64 nsc = (n + NZ_SC - 1) / NZ_SC;
       const unsigned nb = (unsigned)((nsc + NZ_FW - 1) / NZ_FW);
-      k_enc_nz_count<<<nb, NZ_FW * 32, 0, st>>>(s16, nzmap, n, R, lengths, words, S, nsc, ctl);
+      k_enc_nz_count<<<nb, NZ_FW * 32, 0, st>>>(s16, nzmap, n, R, lengths, words, S, nsc, ctl,
+                                                 out, cap_bytes / 4, bit_base);
       k_scan_pair<<<(unsigned)((nsc + PS_TILE - 1) / PS_TILE), PS_NT, 0, st>>>(
           S, nsc, mode, out, cap_bytes / 4, ctl, bit_base, lengths, words, R, n, 2);
       k_enc_nz_emit<<<nb, NZ_FW * 32, 0, st>>>(s16, nzmap, n, R, lengths, words, out,
                                                cap_bytes / 4, xval, o_idx, o_val, o_cap, S, nsc,
                                                idx_offset, ctl, bit_base);
-      k_outlier_values<<<(unsigned)(sms * 8), 256, 0, st>>>(o_idx, xval, o_val, o_cap,
-                                                             idx_offset, ctl);
-      note_launch(3);
+      // o_val is not filled on this path: the caller gathers x[o_idx] (k_assemble)
+      note_launch(2);
     } else {
       const size_t smem_s = sizeof(uint2) * (nbins + 2) + 16;
       ensure_smem((const void *)k_enc_sparse, smem_s);
