@@ -393,8 +393,13 @@ __global__ void __launch_bounds__(256) k_p2d_tables(const uint8_t *__restrict__ 
     ct[0][p] = c;
   }
   __syncthreads();
+  // pointer doubling until every entry walk sits on a terminal (positions
+  // >= clen loop on themselves with count 0, so nothing changes after):
+  // literal-heavy chunks need 4-5 rounds, all-run chunks 10
   int cur = 0;
   for (int r = 0; r < 12; ++r) {
+    const bool open = threadIdx.x < P2D_D && nx[cur][threadIdx.x] < clen;
+    if (!__syncthreads_or(open)) break;
     for (int p = threadIdx.x; p < P2D_P; p += blockDim.x) {
       const int a = nx[cur][p];
       nx[cur ^ 1][p] = nx[cur][a];
