@@ -172,10 +172,12 @@ DEV void sample_plan(const TuneArgs &A, SamplePlan &sp) {
 // profiled dim d, vals[(p*3 + d)*5 + k] = bits of the values at offsets
 // -3, -1, +1, +3 along d (k = 0..3) and of the point itself (k = 4); 0 when
 // the value's plane is outside [zlo, zhi) (another shard owns it).
-__global__ void __launch_bounds__(256) k_sample_gather(const float *__restrict__ x, TuneArgs A,
-                                                       int32_t *vals) {
-  SamplePlan sp;
-  sample_plan(A, sp);
+// One block of 1024 threads: the plan is built once in shared memory and
+// every sample load is in flight at the same time (a thread per value).
+__global__ void __launch_bounds__(1024) k_sample_gather(const float *__restrict__ x, TuneArgs A,
+                                                        int32_t *vals) {
+  __shared__ SamplePlan sp;
+  if (threadIdx.x == 0) sample_plan(A, sp);
   const int rank = A.rank, pad = A.pad_axes;
   for (int w = threadIdx.x; w < CSZI_SAMPLE_WORDS; w += blockDim.x) vals[w] = 0;
   __syncthreads();
@@ -359,7 +361,7 @@ int launch_sample_gather(const float *x, const cszi_geom *g, int32_t *vals, cuda
   p.have_alpha = 1;
   const int rc = tune_args(g, &p, A);
   if (rc != CSZI_OK) return rc;
-  k_sample_gather<<<1, 256, 0, st>>>(x, A, vals);
+  k_sample_gather<<<1, 1024, 0, st>>>(x, A, vals);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
