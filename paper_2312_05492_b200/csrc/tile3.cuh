@@ -959,10 +959,12 @@ __global__ void __launch_bounds__(NT, 3)
         // non-R bit per code (outliers included) for the sparse encoder: the
         // map is zeroed beforehand and only groups holding a non-R code (~5%
         // on smooth fields) OR their byte into the row's word
+        // the four lanes of a row own one byte each of its word: plain
+        // byte stores (shared atomics here cost ~15 us over the launch)
         if (nzmap)
-          atomicOr(&nzs[row], (ne_r2(a.x, rr) | (ne_r2(a.y, rr) << 2) | (ne_r2(b.x, rr) << 4) |
-                               (ne_r2(b.y, rr) << 6))
-                                  << (8 * c));
+          reinterpret_cast<uint8_t *>(nzs)[4 * row + c] =
+              (uint8_t)(ne_r2(a.x, rr) | (ne_r2(a.y, rr) << 2) | (ne_r2(b.x, rr) << 4) |
+                        (ne_r2(b.y, rr) << 6));
         const uint32_t w[4] = {a.x, a.y, b.x, b.y};
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
