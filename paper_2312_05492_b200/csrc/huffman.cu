@@ -734,71 +734,144 @@ struct WordOr {
   }
 };
 
+// Balanced path: a super-chunk with K <= NZ_LCAP set bits (all but the few
+// dense edge super-chunks) lists them as (j | symbol << 16) in symbol order
+// in shared memory -- each lane loads the symbol groups under its own bits
+// -- and the lanes then take contiguous rank ranges of the list, so the
+// per-symbol work is spread evenly instead of following the bitmap's lanes.
+constexpr int NZ_LCAP = 256;
+
+DEV uint32_t nz_pairs(const uint16_t *__restrict__ sp_lane, const uint32_t wv[4], uint32_t pc,
+                      int lane, uint4 *slot, uint32_t *lst) {
+  const uint32_t incl = warp_incl_scan(pc);
+  const uint32_t K = __shfl_sync(CSZI_FULL, incl, 31);
+  if (K > (uint32_t)NZ_LCAP) return K;
+  uint32_t k = incl - pc;
+  nz_visit(sp_lane, wv, slot,
+           [&](uint32_t j, uint32_t s) { lst[k++] = (uint32_t)(lane * 128) + j | (s << 16); });
+  __syncwarp();
+  return K;
+}
+
 // per super-chunk: stream bits (R = 1 bit) and outliers -> S.ch_bits /
-// S.ch_out; per lane the exclusive prefixes (extra bits | outliers << 18)
+// S.ch_out; dense super-chunks also the per-lane exclusive prefixes
+// (extra bits | outliers << 18) for the emit's per-lane path
 __global__ void __launch_bounds__(NZ_FW * 32) k_enc_nz_count(
     const uint16_t *__restrict__ src, const uint32_t *__restrict__ nzmap, u64 n, int R,
     const uint8_t *__restrict__ lengths, const uint32_t *__restrict__ words, EncScratch S,
     u64 nsc, const cszi_ctl *ctl, uint32_t *out, u64 cap_words, uint32_t bit_base) {
+  __shared__ uint4 slots[NZ_FW * 32][4];
+  __shared__ uint32_t lsts[NZ_FW][NZ_LCAP];
   const int lane = threadIdx.x & 31;
   if (!enc_sparse(lengths, words, R, n, ctl)) return;
   zero_stream(out, cap_words, ctl, bit_base);  // (k_enc_zero's job, one launch less)
   const u64 t = nz_tile(nsc);
   if (t >= nsc) return;
   uint32_t wv[4];
-  nz_words(nzmap, n, t, lane, wv);
-  __shared__ uint4 slots[NZ_FW * 32][4];
-  uint32_t ex = 0, o = 0;
-  nz_visit(src + t * NZ_SC + 128 * lane, wv, slots[threadIdx.x], [&](uint32_t, uint32_t s) {
-    ex += (uint32_t)__ldg(lengths + (s ? s : (uint32_t)R)) - 1u;  // outlier 0 is coded as R
-    o += s == 0;
-  });
-  // ex < 2^17 (128 symbols x 31 extra bits), o <= 128: one packed scan
-  const uint32_t v = ex | (o << 18);
-  const uint32_t incl = warp_incl_scan(v);
-  S.nz_lane[t * 32 + lane] = incl - v;
-  if (lane == 31) {
-    S.ch_bits[t] = (uint32_t)min((u64)NZ_SC, n - t * NZ_SC) + (incl & 0x3ffffu);
-    S.ch_out[t] = incl >> 18;
+  const uint32_t pc = nz_words(nzmap, n, t, lane, wv);
+  const uint16_t *sp_lane = src + t * NZ_SC + 128 * lane;
+  uint32_t *lst = lsts[threadIdx.x >> 5];
+  const uint32_t K = nz_pairs(sp_lane, wv, pc, lane, slots[threadIdx.x], lst);
+  const uint32_t lenR1 = 1u;  // sparse streams: R is the 1-bit "0"
+  uint32_t tot;
+  if (K <= (uint32_t)NZ_LCAP) {
+    uint32_t v = 0;
+    for (uint32_t i = lane; i < K; i += 32) {
+      const uint32_t s = lst[i] >> 16;
+      v += ((uint32_t)__ldg(lengths + (s ? s : (uint32_t)R)) - lenR1) | ((uint32_t)(s == 0) << 18);
+    }
+    tot = warp_sum(v);
+  } else {
+    uint32_t ex = 0, o = 0;
+    nz_visit(sp_lane, wv, slots[threadIdx.x], [&](uint32_t, uint32_t s) {
+      ex += (uint32_t)__ldg(lengths + (s ? s : (uint32_t)R)) - lenR1;  // outlier 0 is coded as R
+      o += s == 0;
+    });
+    // ex < 2^17 (128 symbols x 31 extra bits), o <= 128: one packed scan
+    const uint32_t v = ex | (o << 18);
+    const uint32_t incl = warp_incl_scan(v);
+    S.nz_lane[t * 32 + lane] = incl - v;
+    tot = __shfl_sync(CSZI_FULL, incl, 31);
+  }
+  if (lane == 0) {
+    S.ch_bits[t] = (uint32_t)min((u64)NZ_SC, n - t * NZ_SC) + (tot & 0x3ffffu);
+    S.ch_out[t] = tot >> 18;
   }
 }
 
-__global__ void __launch_bounds__(NZ_FW * 32) k_enc_nz_emit(
+__global__ void __launch_bounds__(NZ_FW * 32, 12) k_enc_nz_emit(
     const uint16_t *__restrict__ src, const uint32_t *__restrict__ nzmap, u64 n, int R,
     const uint8_t *__restrict__ lengths, const uint32_t *__restrict__ words,
     uint32_t *__restrict__ out, u64 cap_words, const float *__restrict__ xval, u64 *o_idx,
     float *o_val, u64 o_cap, EncScratch S, u64 nsc, u64 idx_offset, cszi_ctl *ctl,
     uint32_t bit_base) {
+  __shared__ uint4 slots[NZ_FW * 32][4];
+  __shared__ uint32_t lsts[NZ_FW][NZ_LCAP];
   const int lane = threadIdx.x & 31;
   const u64 t = nz_tile(nsc);
   if (t >= nsc) return;
   uint32_t wv[4];
   const uint32_t pc = nz_words(nzmap, n, t, lane, wv);
   if (!enc_sparse(lengths, words, R, n, ctl)) return;
-  if (pc == 0) return;
-  const uint32_t lp = S.nz_lane[t * 32 + lane];
-  // bit_off counts whole symbols: lane-local symbol j starts at
-  // pos0 + j + (extra bits of the lane's codewords before it)
-  const u64 g0 = t * NZ_SC + 128 * (u64)lane;
-  const u64 pos0 = S.bit_off[t] + bit_base + 128 * (u64)lane + (lp & 0x3ffffu);
-  u64 ko = S.out_off[t] + (lp >> 18);
-  uint32_t extra = 0;
+  if (!__any_sync(CSZI_FULL, pc != 0)) return;
+  const u64 sc0 = t * NZ_SC;
+  const uint16_t *sp_lane = src + sc0 + 128 * lane;
+  uint32_t *lst = lsts[threadIdx.x >> 5];
+  const uint32_t K = nz_pairs(sp_lane, wv, pc, lane, slots[threadIdx.x], lst);
+  // bit_off counts whole symbols: super-chunk symbol j starts at
+  // base + j + (extra bits of the codewords before it)
+  const u64 base = S.bit_off[t] + bit_base;
   bool cap_hit = false;
-  WordOr wo{out, cap_words, pos0 >> 5};
-  __shared__ uint4 slots[NZ_FW * 32][4];
-  nz_visit(src + g0, wv, slots[threadIdx.x], [&](uint32_t j, uint32_t s) {
-    const uint32_t sI = s ? s : (uint32_t)R;
-    const uint32_t len = __ldg(lengths + sI), cw = __ldg(words + sI);
-    if (cw) wo.put(pos0 + j + extra, cw, len);
-    extra += len - 1;
-    if (s == 0) {  // values: k_outlier_values (a dependent load here stalls the lane)
-      if (ko < o_cap) o_idx[ko] = g0 + j + idx_offset;
-      else cap_hit = true;
-      ko++;
+  if (K <= (uint32_t)NZ_LCAP) {
+    const uint32_t per = (K + 31) / 32;
+    const uint32_t r0 = min(lane * per, K), r1 = min(r0 + per, K);
+    uint32_t v = 0;
+    for (uint32_t i = r0; i < r1; ++i) {
+      const uint32_t s = lst[i] >> 16;
+      v += ((uint32_t)__ldg(lengths + (s ? s : (uint32_t)R)) - 1u) | ((uint32_t)(s == 0) << 18);
     }
-  });
-  wo.flush(true);
-  if (cap_hit || wo.cap_hit) atomicOr(&ctl->flags, (uint32_t)CSZI_F_CAPACITY);
+    const uint32_t pre = warp_incl_scan(v) - v;
+    if (r0 < r1) {
+      uint32_t extra = pre & 0x3ffffu;
+      u64 ko = S.out_off[t] + (pre >> 18);
+      WordOr wo{out, cap_words, (base + (lst[r0] & 0xffffu) + extra) >> 5};
+      for (uint32_t i = r0; i < r1; ++i) {
+        const uint32_t pr = lst[i], j = pr & 0xffffu, s = pr >> 16;
+        const uint32_t sI = s ? s : (uint32_t)R;
+        const uint32_t len = __ldg(lengths + sI), cw = __ldg(words + sI);
+        if (cw) wo.put(base + j + extra, cw, len);
+        extra += len - 1;
+        if (s == 0) {  // values: gathered by k_assemble
+          if (ko < o_cap) o_idx[ko] = sc0 + j + idx_offset;
+          else cap_hit = true;
+          ko++;
+        }
+      }
+      wo.flush(true);
+      cap_hit |= wo.cap_hit;
+    }
+  } else if (pc) {
+    const uint32_t lp = S.nz_lane[t * 32 + lane];
+    const u64 g0 = sc0 + 128 * (u64)lane;
+    const u64 pos0 = base + 128 * (u64)lane + (lp & 0x3ffffu);
+    u64 ko = S.out_off[t] + (lp >> 18);
+    uint32_t extra = 0;
+    WordOr wo{out, cap_words, pos0 >> 5};
+    nz_visit(sp_lane, wv, slots[threadIdx.x], [&](uint32_t j, uint32_t s) {
+      const uint32_t sI = s ? s : (uint32_t)R;
+      const uint32_t len = __ldg(lengths + sI), cw = __ldg(words + sI);
+      if (cw) wo.put(pos0 + j + extra, cw, len);
+      extra += len - 1;
+      if (s == 0) {
+        if (ko < o_cap) o_idx[ko] = g0 + j + idx_offset;
+        else cap_hit = true;
+        ko++;
+      }
+    });
+    wo.flush(true);
+    cap_hit |= wo.cap_hit;
+  }
+  if (cap_hit) atomicOr(&ctl->flags, (uint32_t)CSZI_F_CAPACITY);
 }
 
 template <int MODE>
