@@ -80,3 +80,15 @@ def test_nonr_bitmap_encoder(shape):
     data[shape[0] // 2, 3, 5] = 40.0  # one outlier
     for eb in (1e-3, 1e-2):
         _round_trip_equals_oracle(data, eb)
+
+
+def test_bitmap_encoder_many_outliers():
+    # sparse stream (R = "0") with thousands of outliers spread over the
+    # super-chunks: outlier order and values come from the bitmap path
+    data = _smooth((64, 64, 96), seed=9)
+    flat = data.reshape(-1)
+    flat[::97] = 1000.0
+    flat[5000:5400] = -1000.0  # a dense run: super-chunk with > 256 non-R symbols
+    blob = _round_trip_equals_oracle(data, 1e-3, mode="abs")
+    sec = P.parse_archive(blob).outliers  # u64 count + 12-byte records
+    assert int.from_bytes(sec[:8], "little") > 2000
