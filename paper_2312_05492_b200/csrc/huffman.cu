@@ -1437,10 +1437,20 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_write_zr(Stream s, const DecTabl
         const bool vec = (w0 % PER) == 0;
         const u64 va = vec ? (ra + PER - 1) / PER : rb, vb = vec ? rb / PER : rb;
         if (vec && va <= vb) {
-          for (u64 f = ra + lane; f < va * PER; f += 32) out[f] = zv;
-          for (u64 v = va + lane; v < vb; v += 32)
-            __stcs(reinterpret_cast<uint4 *>(out) + v, zz);
-          for (u64 f = vb * PER + lane; f < rb; f += 32) out[f] = zv;
+          // 32-bit loop counters relative to the warp's range (< 2^32 symbols)
+          const int lead = (int)(va * PER - ra), nv = (int)(vb - va), tail = (int)(rb - vb * PER);
+          if (lane < lead) out[ra + lane] = zv;
+          uint4 *o4 = reinterpret_cast<uint4 *>(out) + va;
+          int v = lane;
+#pragma unroll 1
+          for (; v + 96 < nv; v += 128) {
+            __stcs(o4 + v, zz);
+            __stcs(o4 + v + 32, zz);
+            __stcs(o4 + v + 64, zz);
+            __stcs(o4 + v + 96, zz);
+          }
+          for (; v < nv; v += 32) __stcs(o4 + v, zz);
+          if (lane < tail) out[vb * PER + lane] = zv;
         } else {
           for (u64 f = ra + lane; f < rb; f += 32) out[f] = zv;
         }
@@ -1448,20 +1458,28 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_write_zr(Stream s, const DecTabl
     }
     __syncwarp();
     if (!active) return;
-    while (pos < end && k < k1) {
-      const uint32_t w = br.peek(ss, pos);
+    // 32-bit counters relative to the chunk (a chunk holds at most DEC_C
+    // symbols and ends at most 32 bits past its DEC_C-bit window)
+    const u64 pos0 = pos, kb = k;
+    const uint32_t pend = (uint32_t)(end - pos0), kend = (uint32_t)(k1 - kb);
+    const uint32_t plim = (uint32_t)min(s.nb - pos0, (u64)0xffffffffu);
+    uint32_t p = 0, kk = 0;
+    OutT *o = out + (kb - w0);  // may point below out; only written at kb + kk >= w0
+    const uint32_t kskip = kb >= w0 ? 0u : (uint32_t)(w0 - kb);
+    while (p < pend && kk < kend) {
+      const uint32_t w = br.peek(ss, pos0 + p);
       if (!(w >> 31)) {
-        const u64 adv = min(min((u64)__clz(w), end - pos), k1 - k);
-        pos += adv;
-        k += adv;
+        const uint32_t adv = min(min((uint32_t)__clz(w), pend - p), kend - kk);
+        p += adv;
+        kk += adv;
         continue;
       }
       uint32_t len;
       const uint32_t sym = decode_at(T, sorted, w, len);
-      if (len == 0 || pos + len > s.nb) break;  // dead chain: reported by k_dec_check
-      pos += len;
-      if (k >= w0) out[k - w0] = (sizeof(OutT) == 4) ? (OutT)((int32_t)sym - R) : (OutT)sym;
-      ++k;
+      if (len == 0 || p + len > plim) break;  // dead chain: reported by k_dec_check
+      p += len;
+      if (kk >= kskip) o[kk] = (sizeof(OutT) == 4) ? (OutT)((int32_t)sym - R) : (OutT)sym;
+      ++kk;
     }
     return;
   }
