@@ -1134,29 +1134,32 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_spec(Stream s, const DecTables *
   if (j >= M) return;
   SmemReader br;
   br.init();
-  u64 pos = j * DEC_C;
-  const u64 end = min((j + 1) * DEC_C, s.nb);
+  // 32-bit chunk-relative position (a chunk ends at most 32 bits past its window)
+  const u64 pos0 = j * DEC_C;
+  const uint32_t pend = (uint32_t)(min((j + 1) * DEC_C, s.nb) - pos0);
+  const uint32_t plim = (uint32_t)min(s.nb - pos0, (u64)0xffffffffu);
+  uint32_t p = 0;
   uint32_t cnt = 0;
   uint8_t dead = 0;
   const bool zr = T.zrun != 0;
-  while (pos < end) {
-    const uint32_t w = br.peek(ss, pos);
+  while (p < pend) {
+    const uint32_t w = br.peek(ss, pos0 + p);
     if (zr && !(w >> 31)) {  // run of the "0" codeword
-      const u64 adv = min((u64)__clz(w), end - pos);
-      pos += adv;
-      cnt += (uint32_t)adv;
+      const uint32_t adv = min((uint32_t)__clz(w), pend - p);
+      p += adv;
+      cnt += adv;
       continue;
     }
     uint32_t len;
     decode_at(T, sorted, w, len);
-    if (len == 0 || pos + len > s.nb) {
+    if (len == 0 || p + len > plim) {
       dead = 1;
       break;
     }
-    pos += len;
+    p += len;
     cnt++;
   }
-  spec_exit[j] = pos;
+  spec_exit[j] = pos0 + p;
   spec_cnt[j] = cnt;
   spec_dead[j] = dead;
 }
