@@ -26,7 +26,7 @@ __global__ void k_ctl_init(cszi_ctl *ctl) {
 
 // One read of x: min/max over order-preserving keys and the first non-finite
 // flat index (NaN/Inf have an all-ones exponent).
-__global__ void __launch_bounds__(256) k_range(const float *__restrict__ x, uint64_t n,
+__global__ void __launch_bounds__(256, 4) k_range(const float *__restrict__ x, uint64_t n,
                                                cszi_ctl *ctl) {
   uint32_t kmin = 0xffffffffu, kmax = 0u;
   u64 bad = ~0ull;
@@ -42,24 +42,34 @@ __global__ void __launch_bounds__(256) k_range(const float *__restrict__ x, uint
     const float4 *x4 = reinterpret_cast<const float4 *>(x);
     constexpr uint32_t EXP = 0x7f800000u;
     u64 i = tid;
-    for (; i + nthr < n4; i += 2 * nthr) {
-      const float4 va = __ldcs(x4 + i);
-      const float4 vb = __ldcs(x4 + i + nthr);
-      const uint32_t b[8] = {__float_as_uint(va.x), __float_as_uint(va.y), __float_as_uint(va.z),
-                             __float_as_uint(va.w), __float_as_uint(vb.x), __float_as_uint(vb.y),
-                             __float_as_uint(vb.z), __float_as_uint(vb.w)};
+    // four float4 per thread in flight (64 KB per SM at 4 blocks): enough
+    // bytes outstanding to cover HBM latency (two left it at ~75% of peak)
+    for (; i + 3 * nthr < n4; i += 4 * nthr) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcs(x4 + i + u * nthr);
       bool nf = false;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        nf |= (b[j] & EXP) == EXP;
-        const uint32_t k = b[j] ^ ((uint32_t)((int32_t)b[j] >> 31) | 0x80000000u);
-        kmin = min(kmin, k);
-        kmax = max(kmax, k);
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t b[4] = {__float_as_uint(v[u].x), __float_as_uint(v[u].y),
+                               __float_as_uint(v[u].z), __float_as_uint(v[u].w)};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          nf |= (b[j] & EXP) == EXP;
+          const uint32_t k = b[j] ^ ((uint32_t)((int32_t)b[j] >> 31) | 0x80000000u);
+          kmin = min(kmin, k);
+          kmax = max(kmax, k);
+        }
       }
       if (nf) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if ((b[j] & EXP) == EXP) bad = min(bad, 4 * (j < 4 ? i : i + nthr) + (j & 3));
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t b[4] = {__float_as_uint(v[u].x), __float_as_uint(v[u].y),
+                                 __float_as_uint(v[u].z), __float_as_uint(v[u].w)};
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if ((b[j] & EXP) == EXP) bad = min(bad, 4 * (i + u * nthr) + j);
+        }
       }
     }
     for (; i < n4; i += nthr) {
@@ -321,7 +331,7 @@ int launch_ctl_init(cszi_ctl *ctl, cudaStream_t st) {
 int launch_range(const float *x, uint64_t n, cszi_ctl *ctl, cudaStream_t st) {
   const int sms = sm_count();
   u64 blocks = (n / 4 + 255) / 256;
-  const u64 cap = (u64)sms * 8;
+  const u64 cap = (u64)sms * occupancy((const void *)k_range, 256, 0);  // one resident wave
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   k_range<<<(unsigned)blocks, 256, 0, st>>>(x, n, ctl);
