@@ -1175,20 +1175,19 @@ __global__ void __launch_bounds__(256) k_dec_sync(Stream s, const DecTables *G,
                                                  const uint8_t *chg_prev, u64 *X, uint32_t *K,
                                                  uint8_t *D, uint8_t *chg, uint32_t *nchg) {
   __shared__ DecSmem T;
-  load_dec_smem(T, G, sorted);
   const u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x;
-  if (j >= M) return;
-  u64 e;
-  if (it == 0) {
-    e = (j == 0) ? 0 : spec_exit[j - 1];
-  } else {
-    if (j == 0 || !chg_prev[j - 1]) {
-      X[j] = X_prev[j];
-      chg[j] = 0;
-      return;
-    }
-    e = X_prev[j - 1];
+  // iterations > 0: only chunks whose predecessor moved re-walk; blocks
+  // without one skip the table load (most of them once the chains meet)
+  bool need = j < M;
+  if (need && it > 0 && (j == 0 || !chg_prev[j - 1])) {
+    X[j] = X_prev[j];
+    chg[j] = 0;
+    need = false;
   }
+  if (!__syncthreads_or(need)) return;
+  load_dec_smem(T, G, sorted);
+  if (!need) return;
+  const u64 e = (it == 0) ? ((j == 0) ? 0 : spec_exit[j - 1]) : X_prev[j - 1];
   const u64 end = min((j + 1) * DEC_C, s.nb);
   BitReader ba, bb;
   ba.init();
