@@ -465,10 +465,12 @@ __global__ void __launch_bounds__(PS_NT) k_scan_pair(EncScratch S, u64 nch, int 
                                                     const uint32_t *p_words, int R, u64 n,
                                                     int when) {
   __shared__ u64 ws[PS_NT / 32 + 1];
-  // when: 0 always, 1 dense streams only, 2 sparse streams only
-  if (when && enc_sparse(p_len, p_words, R, n, ctl) != (when == 2)) return;
   __shared__ u64 s_t, s_pb, s_po;
-  if (threadIdx.x == 0) s_t = atomicAdd(S.ticket, 1u);
+  // when: 0 always, 1 dense streams only, 2 sparse streams only.  The two
+  // conditional launches draw tickets from separate counters, so the ticket
+  // is requested together with the predicate's loads (one latency, not two).
+  if (threadIdx.x == 0) s_t = atomicAdd(S.ticket + (when == 2 ? 1 : 0), 1u);
+  if (when && enc_sparse(p_len, p_words, R, n, ctl) != (when == 2)) return;
   __syncthreads();
   const u64 t = s_t;
   const u64 base = t * PS_TILE + (u64)threadIdx.x * PS_IPT;
@@ -499,8 +501,9 @@ __global__ void __launch_bounds__(PS_NT) k_scan_pair(EncScratch S, u64 nch, int 
       S.bit_off[base + i] = rb;
       S.out_off[base + i] = ro;
       // a word holding an unaligned chunk boundary is ORed by both chunks
+      // (the bitmap path zeroed the whole stream already)
       const u64 ab = rb + bit_base;  // bit position in the output words
-      if ((ab & 31) && (ab >> 5) < cap_words) out[ab >> 5] = 0u;
+      if (when != 2 && (ab & 31) && (ab >> 5) < cap_words) out[ab >> 5] = 0u;
     }
     rb += vb[i];
     ro += vo[i];
