@@ -35,7 +35,7 @@ int launch_gather_anchors(const float *x, const cszi_geom *g, float *out, cudaSt
 int launch_hist_i32(const int32_t *codes, u64 n, int R, u64 *hist, cszi_ctl *ctl,
                     cudaStream_t st);
 int launch_codebook(const u64 *hist, int nbins, uint8_t *lengths, uint32_t *words,
-                    cszi_ctl *ctl, cudaStream_t st);
+                    cszi_ctl *ctl, cudaStream_t st, bool set_bits = false);
 size_t dec_tables_bytes(int nbins);
 int launch_canonical(const uint8_t *lengths, int nbins, uint32_t *words, void *dec_tables,
                      cszi_ctl *ctl, cudaStream_t st);
@@ -44,7 +44,8 @@ int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *length
                   const uint32_t *words, uint32_t *out, u64 cap_bytes, const float *xval,
                   u64 *o_idx, float *o_val, u64 o_cap, void *scratch, cszi_ctl *ctl,
                   cudaStream_t st, u64 idx_offset, uint32_t bit_base = 0,
-                  const uint32_t *nzmap = nullptr, const u64 *hist = nullptr);
+                  const uint32_t *nzmap = nullptr, const u64 *hist = nullptr,
+                  bool bits_known = false);
 u64 dec_scratch_bytes(u64 nbytes, int table_mode);
 int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *dec_tables,
                   void *out, int out_kind, void *scratch, cszi_ctl *ctl, cudaStream_t st,
@@ -376,7 +377,7 @@ int cszi_compress(const float *x, const cszi_geom *g, const cszi_params *p,
   uint8_t *raw = pass2 ? W.raw : payload;
   CK(launch_gather_anchors(x, g, reinterpret_cast<float *>(raw), st));
   uint8_t *lengths = raw + 4 * na;  // the codebook section is the length table
-  CK(launch_codebook(W.hist, (int)nbins, lengths, W.words, ctl, st));
+  CK(launch_codebook(W.hist, (int)nbins, lengths, W.words, ctl, st, true));
   const u64 head = 4 * na + nbins;
   // the bitstream is packed straight into its section when the section is
   // word-aligned (R even); otherwise into W.bits and copied by k_assemble
@@ -384,7 +385,7 @@ int cszi_compress(const float *x, const cszi_geom *g, const cszi_params *p,
   uint32_t *bits_out = in_place ? reinterpret_cast<uint32_t *>(raw + head) : W.bits;
   CK(launch_encode(0, W.sym, n, R, lengths, W.words, bits_out, caps->bits_cap, x, W.oidx, W.oval,
                    caps->outlier_cap, W.enc_scratch, ctl, st, 0, 0, nz ? W.nzmap : nullptr,
-                   W.hist));
+                   W.hist, true));  // k_codebook already set ctl->bits
   k_assemble<<<grid_for(n / 16), 256, 0, st>>>(raw, head, reinterpret_cast<uint8_t *>(W.bits),
                                                 W.oidx, nz ? nullptr : W.oval, x, raw_cap,
                                                 caps->bits_cap,

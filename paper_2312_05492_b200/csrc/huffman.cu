@@ -169,7 +169,7 @@ DEV void canonical_block(const uint8_t *len_s, int nbins, uint32_t *words, DecTa
 
 __global__ void __launch_bounds__(CB_NT) k_codebook(const u64 *__restrict__ hist, int nbins,
                                                     uint8_t *lengths, uint32_t *words,
-                                                    cszi_ctl *ctl) {
+                                                    cszi_ctl *ctl, int set_bits) {
   // shared layout: keys[npow2] | ik[nbins] | parent[2*nbins] | dep[nbins] | len[nbins]
   extern __shared__ __align__(16) unsigned char sm_raw[];
   int npow2 = 1;
@@ -253,8 +253,23 @@ __global__ void __launch_bounds__(CB_NT) k_codebook(const u64 *__restrict__ hist
   }
   __syncthreads();
   if (overflow && threadIdx.x == 0) ctl->flags |= CSZI_F_LENGTH_OVERFLOW;
-  for (int s = threadIdx.x; s < nbins; s += blockDim.x) lengths[s] = len_s[s];
+  // set_bits: stream length = sum of count x length (what k_total_bits
+  // computes; the encoder's scan rewrites the same value), one launch less
+  // for cszi_compress (a slab encode's histogram is not this one)
+  __shared__ u64 bsum[CB_NT / 32];
+  u64 bits = 0;
+  for (int s = threadIdx.x; s < nbins; s += blockDim.x) {
+    lengths[s] = len_s[s];
+    bits += hist[s] * len_s[s];
+  }
+  bits = warp_sum(bits);
+  if ((threadIdx.x & 31) == 0) bsum[threadIdx.x >> 5] = bits;
   __syncthreads();
+  if (threadIdx.x < 32) {
+    bits = (threadIdx.x < (int)(blockDim.x >> 5)) ? bsum[threadIdx.x] : 0;
+    bits = warp_sum(bits);
+    if (threadIdx.x == 0 && set_bits) ctl->bits = bits;
+  }
   canonical_block(len_s, nbins, words, nullptr, nullptr, ctl);
 }
 
@@ -1507,14 +1522,14 @@ int launch_hist_i32(const int32_t *codes, u64 n, int R, u64 *hist, cszi_ctl *ctl
 }
 
 int launch_codebook(const u64 *hist, int nbins, uint8_t *lengths, uint32_t *words,
-                    cszi_ctl *ctl, cudaStream_t st) {
+                    cszi_ctl *ctl, cudaStream_t st, bool set_bits) {
   if (nbins > 16384 || nbins < 1) return CSZI_E_UNSUPPORTED;
   int npow2 = 1;
   while (npow2 < nbins) npow2 <<= 1;
   // keys[npow2] + parent[2*nbins] + len[nbins] + internal keys / depths
   const size_t smem = sizeof(u64) * (npow2 + nbins) + sizeof(int32_t) * 3 * nbins + nbins + 16;
   ensure_smem((const void *)k_codebook, smem);
-  k_codebook<<<1, CB_NT, smem, st>>>(hist, nbins, lengths, words, ctl);
+  k_codebook<<<1, CB_NT, smem, st>>>(hist, nbins, lengths, words, ctl, set_bits ? 1 : 0);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
@@ -1592,7 +1607,7 @@ int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *length
                   const uint32_t *words, uint32_t *out, u64 cap_bytes, const float *xval,
                   u64 *o_idx, float *o_val, u64 o_cap, void *scratch, cszi_ctl *ctl,
                   cudaStream_t st, u64 idx_offset, uint32_t bit_base,
-                  const uint32_t *nzmap, const u64 *hist) {
+                  const uint32_t *nzmap, const u64 *hist, bool bits_known) {
   if (n == 0) return CSZI_OK;
   if (mode != 0 || (n & 31) || (reinterpret_cast<uintptr_t>(src) & 15)) nzmap = nullptr;
   const u64 nch = (n + ENC_CH - 1) / ENC_CH;
@@ -1626,8 +1641,8 @@ int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *length
   // bitmap path: needs the bitmap and the histogram (stream length known
   // up front); count / scan / pack over 1024-symbol chunks then run only
   // for a dense stream, the k_enc_nz_* kernels only for a sparse one
-  const bool nzp = nzmap && hist;
-  if (nzp) {
+  const bool nzp = nzmap && (hist || bits_known);
+  if (nzp && !bits_known) {
     k_total_bits<<<1, 1024, 0, st>>>(hist, lengths, nbins, ctl);
     note_launch();
   }
