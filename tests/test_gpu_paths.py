@@ -92,3 +92,17 @@ def test_bitmap_encoder_many_outliers():
     blob = _round_trip_equals_oracle(data, 1e-3, mode="abs")
     sec = P.parse_archive(blob).outliers  # u64 count + 12-byte records
     assert int.from_bytes(sec[:8], "little") > 2000
+
+
+def test_bitmap_and_full_scan_encoders_identical():
+    # CSZI_NO_NZ=1 turns the predictor's non-R bitmap off: the sparse stream
+    # then comes from the full-symbol packer; both must give the same bytes
+    data = _smooth((40, 48, 64), seed=4, noise=0.002)
+    data.reshape(-1)[::211] = 50.0
+    ref = _round_trip_equals_oracle(data, 1e-3)
+    os.environ["CSZI_NO_NZ"] = "1"
+    try:
+        blob = P.compress(P.Grid(P.Dims(data.shape), data), 1e-3)
+    finally:
+        del os.environ["CSZI_NO_NZ"]
+    assert blob == ref
