@@ -187,6 +187,10 @@ int cszi_ctl_fetch(const cszi_ctl *ctl, cszi_ctl *host, void *stream);
 /* value_range + finite scan (grid.py:60-62, :104-108) into ctl. */
 int cszi_range(const float *x, uint64_t n, cszi_ctl *ctl, void *stream);
 
+/* cszi_ctl_init + cszi_range in one call (the Grid constructor's device
+ * path, grid.py:19-63): one host call less before the first launch. */
+int cszi_scan_field(const float *x, uint64_t n, cszi_ctl *ctl, void *stream);
+
 /* profile_samples + select_config + plan_levels (tuning.py:42-129,
  * predictor.py:122-136) on a ctl holding the range of x; samples is a
  * device scratch of CSZI_SAMPLE_WORDS int32. */

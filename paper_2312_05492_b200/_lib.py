@@ -138,6 +138,7 @@ _SIGS = {
     "cszi_ctl_init": (ctypes.c_int, [_vp, _vp]),
     "cszi_ctl_fetch": (ctypes.c_int, [_vp, _vp, _vp]),
     "cszi_range": (ctypes.c_int, [_vp, _u64, _vp, _vp]),
+    "cszi_scan_field": (ctypes.c_int, [_vp, _u64, _vp, _vp]),
     "cszi_tune": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "cszi_predict": (ctypes.c_int, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
     "cszi_reconstruct": (

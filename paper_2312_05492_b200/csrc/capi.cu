@@ -465,6 +465,12 @@ int cszi_range(const float *x, uint64_t n, cszi_ctl *ctl, void *stream) {
   return launch_range(x, n, ctl, reinterpret_cast<cudaStream_t>(stream));
 }
 
+int cszi_scan_field(const float *x, uint64_t n, cszi_ctl *ctl, void *stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CK(launch_ctl_init(ctl, st));
+  return launch_range(x, n, ctl, st);
+}
+
 int cszi_tune(const float *x, const cszi_geom *g, const cszi_params *p, int32_t *samples,
               cszi_ctl *ctl, void *stream) {
   CK(check_geom(g, p->radius));

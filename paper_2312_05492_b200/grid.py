@@ -95,9 +95,8 @@ class Grid:
             )
         lib = _lib.load()
         ctl = _lib.DeviceCtl()
-        st = _lib.stream_ptr()
-        _lib.check(lib.cszi_ctl_init(ctl.ptr, st), "ctl_init")
-        _lib.check(lib.cszi_range(_lib.ptr(t), t.numel(), ctl.ptr, st), "range")
+        _lib.check(lib.cszi_scan_field(_lib.ptr(t), t.numel(), ctl.ptr, _lib.stream_ptr()),
+                   "range")
         c = ctl.fetch()
         if c.first_nonfinite != 2**64 - 1:
             raise NonFiniteValue(int(c.first_nonfinite))

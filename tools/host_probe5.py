@@ -21,11 +21,11 @@ def comp(*a):
     marks["c1"] = time.perf_counter(); return r
 comp.argtypes = f_comp.argtypes
 lib.cszi_compress = comp
-f_range = lib.cszi_range
+f_range = lib.cszi_scan_field
 def rng(*a):
     marks["r0"] = time.perf_counter(); r = f_range(*a); marks["r1"] = time.perf_counter(); return r
 rng.argtypes = f_range.argtypes
-lib.cszi_range = rng
+lib.cszi_scan_field = rng
 orig_fetch = _lib.DeviceCtl.fetch
 def fetch(self):
     t0 = time.perf_counter(); r = orig_fetch(self); rec("fetch(sync) total", time.perf_counter() - t0); return r
