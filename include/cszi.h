@@ -204,6 +204,13 @@ int cszi_tune(const float *x, const cszi_geom *g, const cszi_params *p, int32_t 
 int cszi_predict(const float *x, const cszi_geom *g, int32_t radius, int32_t exact,
                  uint16_t *sym, uint64_t *hist, cszi_ctl *ctl, void *stream);
 
+/* cszi_predict that also writes the non-R bitmap nzmap (bit j of word w set
+ * when symbol 32w + j is not R; (planes of x) * ny * nx / 8 bytes) when the
+ * layout allows it (3-D default layout, nx % 32 == 0): *nz_done = 1 then. */
+int cszi_predict_nz(const float *x, const cszi_geom *g, int32_t radius, int32_t exact,
+                    uint16_t *sym, uint64_t *hist, uint32_t *nzmap, int32_t *nz_done,
+                    cszi_ctl *ctl, void *stream);
+
 /* Inverse interpolation (predictor.py:423-465) from uint16 symbols
  * (0xFFFF marks an outlier whose value is found in out_idx/out_val). */
 int cszi_reconstruct(const uint16_t *sym, const float *anchors, const uint64_t *out_idx,
@@ -242,6 +249,15 @@ int cszi_encode_sym_at(const uint16_t *sym, uint64_t n, int32_t radius, const ui
                        uint32_t bit_base, uint8_t *out, uint64_t cap_bytes, uint64_t *out_idx,
                        float *out_val, uint64_t out_cap, void *workspace, cszi_ctl *ctl,
                        void *stream);
+
+/* cszi_encode_sym_at driven by the bitmap of cszi_predict_nz; hist = the
+ * histogram of these n symbols (gives the stream length up front).  out_val
+ * is not written: an outlier's value is x[out_idx - idx_offset]. */
+int cszi_encode_sym_nz(const uint16_t *sym, uint64_t n, int32_t radius, const uint8_t *lengths,
+                       const uint32_t *words, const float *x, uint64_t idx_offset,
+                       uint32_t bit_base, uint8_t *out, uint64_t cap_bytes, uint64_t *out_idx,
+                       float *out_val, uint64_t out_cap, const uint32_t *nzmap,
+                       const uint64_t *hist, void *workspace, cszi_ctl *ctl, void *stream);
 
 /* dst (zeroed, bytes) |= nbits of src placed at bit offset dst_bit (MSB-first). */
 int cszi_concat_bits(uint8_t *dst, uint64_t dst_bit, const uint8_t *src, uint64_t nbits,

@@ -158,6 +158,12 @@ _SIGS = {
         [_vp, _u64, _i32, _vp, _vp, _vp, _u64, ctypes.c_uint32, _vp, _u64, _vp, _vp, _u64, _vp,
          _vp, _vp],
     ),
+    "cszi_encode_sym_nz": (
+        ctypes.c_int,
+        [_vp, _u64, _i32, _vp, _vp, _vp, _u64, ctypes.c_uint32, _vp, _u64, _vp, _vp, _u64, _vp,
+         _vp, _vp, _vp, _vp],
+    ),
+    "cszi_predict_nz": (ctypes.c_int, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
     "cszi_concat_bits": (ctypes.c_int, [_vp, _u64, _vp, _u64, _vp]),
     "cszi_pack_outliers": (ctypes.c_int, [_vp, _vp, _u64, _vp, _vp]),
     "cszi_histogram_i32": (ctypes.c_int, [_vp, _u64, _i32, _vp, _vp, _vp]),

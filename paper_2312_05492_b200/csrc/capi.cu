@@ -503,6 +503,19 @@ int cszi_encode_sym_at(const uint16_t *sym, uint64_t n, int32_t radius, const ui
                        bit_base);
 }
 
+int cszi_encode_sym_nz(const uint16_t *sym, uint64_t n, int32_t radius, const uint8_t *lengths,
+                       const uint32_t *words, const float *x, uint64_t idx_offset,
+                       uint32_t bit_base, uint8_t *out, uint64_t cap_bytes, uint64_t *out_idx,
+                       float *out_val, uint64_t out_cap, const uint32_t *nzmap,
+                       const uint64_t *hist, void *workspace, cszi_ctl *ctl, void *stream) {
+  if ((reinterpret_cast<uintptr_t>(out) & 3) || bit_base > 31 || !nzmap || !hist)
+    return CSZI_E_INVALID_ARG;
+  return launch_encode(0, sym, n, radius, lengths, words, reinterpret_cast<uint32_t *>(out),
+                       cap_bytes, x, reinterpret_cast<u64 *>(out_idx), out_val, out_cap,
+                       workspace, ctl, reinterpret_cast<cudaStream_t>(stream), idx_offset,
+                       bit_base, nzmap, reinterpret_cast<const u64 *>(hist), false);
+}
+
 int cszi_encode_sym(const uint16_t *sym, uint64_t n, int32_t radius, const uint8_t *lengths,
                     const uint32_t *words, const float *x, uint64_t idx_offset, uint8_t *out,
                     uint64_t cap_bytes, uint64_t *out_idx, float *out_val, uint64_t out_cap,
@@ -528,6 +541,19 @@ int cszi_predict(const float *x, const cszi_geom *g, int32_t radius, int32_t exa
   CK(check_geom(g, radius));
   cudaMemsetAsync(hist, 0, 8 * 2 * (size_t)radius, st);
   return launch_predict(x, g, radius, ctl, sym, reinterpret_cast<u64 *>(hist), exact != 0, st);
+}
+
+int cszi_predict_nz(const float *x, const cszi_geom *g, int32_t radius, int32_t exact,
+                    uint16_t *sym, uint64_t *hist, uint32_t *nzmap, int32_t *nz_done,
+                    cszi_ctl *ctl, void *stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CK(check_geom(g, radius));
+  cudaMemsetAsync(hist, 0, 8 * 2 * (size_t)radius, st);
+  bool nz = false;
+  const int rc = launch_predict(x, g, radius, ctl, sym, reinterpret_cast<u64 *>(hist), exact != 0,
+                                st, nzmap, &nz);
+  if (nz_done) *nz_done = nz ? 1 : 0;
+  return rc;
 }
 
 int cszi_reconstruct(const uint16_t *sym, const float *anchors, const uint64_t *out_idx,

@@ -201,13 +201,20 @@ class GpuSlabBackend:
         n_own = (s.z1 - s.z0) * ny * nx
         sym = t.empty(n_own + 16, dtype=t.int16, device="cuda")
         hist = t.zeros(2 * s.radius, dtype=t.int64, device="cuda")
+        # non-R bitmap over the planes held (slab + halo): drives the sparse
+        # encoder as in single-GPU compress
+        nzmap = t.empty(s.x.numel() // 32 + 4, dtype=t.int32, device="cuda")
+        nz_done = ctypes.c_int32(0)
         g = self.geom(s)
         if n_own:
-            _lib.check(lib.cszi_predict(_lib.ptr(s.x), ctypes.byref(g), s.radius, 0, _lib.ptr(sym),
-                                        _lib.ptr(hist), s.scratch["ctl"].ptr, _lib.stream_ptr()),
-                       "predict")
+            _lib.check(lib.cszi_predict_nz(_lib.ptr(s.x), ctypes.byref(g), s.radius, 0,
+                                           _lib.ptr(sym), _lib.ptr(hist), _lib.ptr(nzmap),
+                                           ctypes.byref(nz_done), s.scratch["ctl"].ptr,
+                                           _lib.stream_ptr()), "predict")
         s.scratch["sym"] = sym
         s.scratch["n_own"] = n_own
+        s.scratch["nzmap"] = nzmap if nz_done.value else None
+        s.scratch["hist_local"] = hist.clone() if nz_done.value else None
         return hist
 
     def codebook(self, s: SlabState, hist):
@@ -242,7 +249,15 @@ class GpuSlabBackend:
         oval = t.empty(ocap, dtype=t.float32, device="cuda")
         ws = _lib.WS.get(int(lib.cszi_encode_sym_workspace_size(max(n, 1))), "enc_slab")
         ctl = s.scratch["ctl"]
-        if n:
+        nzmap = s.scratch.get("nzmap")
+        if n and nzmap is not None:
+            _lib.check(lib.cszi_encode_sym_nz(
+                _lib.ptr(s.scratch["sym"]), n, s.radius, _lib.ptr(s.scratch["lengths"]),
+                _lib.ptr(s.scratch["words"]), _lib.ptr(s.x), s.z0 * ny * nx, int(bit_base),
+                _lib.ptr(bits), cap, _lib.ptr(oidx), _lib.ptr(oval), ocap, _lib.ptr(nzmap),
+                _lib.ptr(s.scratch["hist_local"]), _lib.ptr(ws), ctl.ptr, _lib.stream_ptr()),
+                "encode")
+        elif n:
             _lib.check(lib.cszi_encode_sym_at(
                 _lib.ptr(s.scratch["sym"]), n, s.radius, _lib.ptr(s.scratch["lengths"]),
                 _lib.ptr(s.scratch["words"]), _lib.ptr(s.x), s.z0 * ny * nx, int(bit_base),
@@ -269,7 +284,14 @@ class GpuSlabBackend:
         nbits, nout = int(counts[0]), int(counts[1])
         nw = (s.scratch.get("bit_base", 0) + nbits + 31) // 32  # whole words, phase-packed
         bits = s.scratch["bits"][: 4 * nw]
-        return bits, s.scratch["oidx"][:nout], s.scratch["oval"][:nout]
+        oidx = s.scratch["oidx"][:nout]
+        if s.scratch.get("nzmap") is not None and nout:
+            # the bitmap encoder lists outlier indices only: values from the slab
+            ny, nx = s.extents[1], s.extents[2]
+            oval = s.x.reshape(-1)[oidx - s.z0 * ny * nx]
+        else:
+            oval = s.scratch["oval"][:nout]
+        return bits, oidx, oval
 
     def assemble(self, s0: SlabState, anchors, bit_pieces, nbits, oidx, oval, pass2: bool,
                  alpha: float):

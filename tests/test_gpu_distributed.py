@@ -12,7 +12,8 @@ from oracle import oracle as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("shape", [(64, 40, 70), (41, 30, 37), (57, 33, 47), (112, 56, 58), (9, 20, 33)])
+@pytest.mark.parametrize("shape", [(64, 40, 70), (41, 30, 37), (57, 33, 47), (112, 56, 58), (9, 20, 33),
+                                   (73, 40, 64), (40, 24, 96)])  # nx % 32 == 0: bitmap slab encodes
 def test_slab_sharding_is_byte_identical(shape):
     import torch
 
