@@ -1286,12 +1286,19 @@ __global__ void k_dec_first_dead(u64 M, const uint8_t *D, u64 *first_dead) {
   const u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x;
   if (j < M && D[j]) atomicMin(first_dead, j);
 }
-__global__ void k_dec_check(const u64 *off, const uint32_t *K, const u64 *first_dead,
-                            const u64 *total, u64 n, cszi_ctl *ctl) {
-  const u64 fd = *first_dead;
-  const u64 avail = (fd != ~0ull) ? off[fd] + K[fd] : *total;
-  ctl->decoded_symbols = avail;
-  if (avail < n) ctl->flags |= CSZI_F_TRUNCATED;
+// decoded-symbol count / truncation check, run by thread 0 of block 0 of
+// whichever write kernel proceeds (one launch less)
+struct DecCheck {
+  const u64 *first_dead;
+  const u64 *total;
+  cszi_ctl *ctl;
+};
+DEV void dec_check(const u64 *off, const uint32_t *K, u64 n, const DecCheck &C) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const u64 fd = *C.first_dead;
+  const u64 avail = (fd != ~0ull) ? off[fd] + K[fd] : *C.total;
+  C.ctl->decoded_symbols = avail;
+  if (avail < n) atomicOr(&C.ctl->flags, (uint32_t)CSZI_F_TRUNCATED);
 }
 
 // Fallback for streams whose chunks do not self-synchronise (e.g. codebooks
@@ -1351,8 +1358,9 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_write(Stream s, const DecTables 
                                                      const uint16_t *sorted, u64 M, const u64 *X,
                                                      const u64 *off, const uint32_t *cnts,
                                                      u64 n, int R, OutT *__restrict__ out, u64 w0,
-                                                     u64 w1) {
+                                                     u64 w1, DecCheck C) {
   if (zrun_tables(G)) return;  // zero-run streams: k_dec_write_zr
+  dec_check(off, cnts, n, C);
   __shared__ DecSmem T;
   __shared__ uint32_t sw[DEC_SW];
   constexpr int K = (sizeof(OutT) == 2) ? DEC_K : DEC_K / 2;
@@ -1388,7 +1396,7 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_write(Stream s, const DecTables 
         uint32_t len;
         const uint32_t sym = decode_at(T, sorted, w, len);
         if (len == 0 || pos + len > s.nb) {
-          pos = end;  // dead chain: truncation is reported by k_dec_check
+          pos = end;  // dead chain: truncation is reported by dec_check
           break;
         }
         pos += len;
@@ -1416,8 +1424,9 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_write_zr(Stream s, const DecTabl
                                                         const uint16_t *sorted, u64 M,
                                                         const u64 *X, const u64 *off,
                                                         const uint32_t *cnts, u64 n, int R,
-                                                        OutT *__restrict__ out, u64 w0, u64 w1) {
+                                                        OutT *__restrict__ out, u64 w0, u64 w1, DecCheck C) {
   if (!zrun_tables(G)) return;  // k_dec_write handles other streams
+  dec_check(off, cnts, n, C);
   __shared__ DecSmem T;
   __shared__ uint32_t sw[DEC_SW];
   const u64 j0 = (u64)blockIdx.x * DEC_NT;
@@ -1496,7 +1505,7 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_write_zr(Stream s, const DecTabl
       }
       uint32_t len;
       const uint32_t sym = decode_at(T, sorted, w, len);
-      if (len == 0 || p + len > plim) break;  // dead chain: reported by k_dec_check
+      if (len == 0 || p + len > plim) break;  // dead chain: reported by dec_check
       p += len;
       if (kk >= kskip) o[kk] = (sizeof(OutT) == 4) ? (OutT)((int32_t)sym - R) : (OutT)sym;
       ++kk;
@@ -1782,18 +1791,18 @@ int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *de
   launch_excl_scan_u32(K, M, off, total, scan_ws, st);
   k_dec_first_dead<<<blocks, 256, 0, st>>>(M, D, first_dead);
   note_launch();
-  k_dec_check<<<1, 1, 0, st>>>(off, K, first_dead, total, n, ctl);
-  note_launch();
+  const DecCheck C{first_dead, total, ctl};
   if (out_kind == 0) {
     k_dec_write<uint16_t><<<dblocks, DEC_NT, 0, st>>>(s, G, sorted, M, X0, off, K, n, R,
-                                                      reinterpret_cast<uint16_t *>(out), w0, w1);
+                                                      reinterpret_cast<uint16_t *>(out), w0, w1,
+                                                      C);
     k_dec_write_zr<uint16_t><<<dblocks, DEC_NT, 0, st>>>(
-        s, G, sorted, M, X0, off, K, n, R, reinterpret_cast<uint16_t *>(out), w0, w1);
+        s, G, sorted, M, X0, off, K, n, R, reinterpret_cast<uint16_t *>(out), w0, w1, C);
   } else {
     k_dec_write<int32_t><<<dblocks, DEC_NT, 0, st>>>(s, G, sorted, M, X0, off, K, n, R,
-                                                     reinterpret_cast<int32_t *>(out), w0, w1);
+                                                     reinterpret_cast<int32_t *>(out), w0, w1, C);
     k_dec_write_zr<int32_t><<<dblocks, DEC_NT, 0, st>>>(
-        s, G, sorted, M, X0, off, K, n, R, reinterpret_cast<int32_t *>(out), w0, w1);
+        s, G, sorted, M, X0, off, K, n, R, reinterpret_cast<int32_t *>(out), w0, w1, C);
   }
   note_launch(2);
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
