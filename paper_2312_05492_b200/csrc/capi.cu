@@ -38,7 +38,8 @@ int launch_codebook(const u64 *hist, int nbins, uint8_t *lengths, uint32_t *word
                     cszi_ctl *ctl, cudaStream_t st, bool set_bits = false);
 size_t dec_tables_bytes(int nbins);
 int launch_canonical(const uint8_t *lengths, int nbins, uint32_t *words, void *dec_tables,
-                     cszi_ctl *ctl, cudaStream_t st);
+                     cszi_ctl *ctl, cudaStream_t st,
+                     u64 expect_raw_len = 0);
 u64 enc_scratch_bytes(u64 n);
 int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *lengths,
                   const uint32_t *words, uint32_t *out, u64 cap_bytes, const float *xval,
@@ -155,9 +156,6 @@ __global__ void k_outliers_mark(const u64 *oidx, const cszi_ctl *ctl, u64 n, uin
   }
 }
 
-__global__ void k_check_raw_len(const cszi_ctl *ctl_ro, cszi_ctl *ctl, u64 expect) {
-  if (ctl_ro->raw_len != expect) ctl->flags |= CSZI_F_P2_LENGTH;
-}
 
 // ---------------------------------------------------------------------------
 // workspace layout
@@ -420,8 +418,6 @@ int cszi_decompress(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
   const uint8_t *raw = payload;
   if (pass2) {
     CK(launch_pass2_decode(payload, payload_len, W.raw, raw_len, W.p2_scratch, ctl, st, 1));
-    k_check_raw_len<<<1, 1, 0, st>>>(ctl, ctl, raw_len);
-    note_launch();
     raw = W.raw;
   }
   if (sec_len[1] != nbins) return CSZI_E_MALFORMED;
@@ -429,7 +425,8 @@ int cszi_decompress(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
   const uint8_t *lengths = raw + sec_len[0];
   const uint8_t *bits = lengths + sec_len[1];
   const uint8_t *outl = bits + sec_len[2];
-  CK(launch_canonical(lengths, (int)nbins, nullptr, W.dec_tables, ctl, st));
+  // (the pass-2 raw-length check runs inside k_canonical)
+  CK(launch_canonical(lengths, (int)nbins, nullptr, W.dec_tables, ctl, st, pass2 ? raw_len : 0));
   u64 w0 = 0;
   const u64 wn = sym_window(g, &w0);  // z-slab shard: only its symbol window
   CK(launch_decode(bits, sec_len[2], n, radius, W.dec_tables, W.sym, 0, W.dec_scratch, ctl, st,

@@ -275,8 +275,12 @@ __global__ void __launch_bounds__(CB_NT) k_codebook(const u64 *__restrict__ hist
 
 __global__ void __launch_bounds__(CB_NT) k_canonical(const uint8_t *__restrict__ lengths,
                                                      int nbins, uint32_t *words,
-                                                     DecTables *dec, cszi_ctl *ctl) {
+                                                     DecTables *dec, cszi_ctl *ctl,
+                                                     u64 expect_raw_len) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
+  // pass-2 length check of the decompress path (was its own 1-thread launch)
+  if (expect_raw_len && threadIdx.x == 0 && ctl->raw_len != expect_raw_len)
+    atomicOr(&ctl->flags, (uint32_t)CSZI_F_P2_LENGTH);
   uint8_t *len_s = sm_raw;
   for (int s = threadIdx.x; s < nbins; s += blockDim.x) len_s[s] = lengths[s];
   __syncthreads();
@@ -1546,12 +1550,13 @@ int launch_codebook(const u64 *hist, int nbins, uint8_t *lengths, uint32_t *word
 size_t dec_tables_bytes(int nbins) { return sizeof(DecTables) + sizeof(uint16_t) * nbins + 16; }
 
 int launch_canonical(const uint8_t *lengths, int nbins, uint32_t *words, void *dec_tables,
-                     cszi_ctl *ctl, cudaStream_t st) {
+                     cszi_ctl *ctl, cudaStream_t st,
+                     u64 expect_raw_len) {
   if (nbins > 65536 || nbins < 1) return CSZI_E_UNSUPPORTED;
   const size_t smem = nbins + 16;
   ensure_smem((const void *)k_canonical, smem);
   k_canonical<<<1, CB_NT, smem, st>>>(lengths, nbins, words,
-                                      reinterpret_cast<DecTables *>(dec_tables), ctl);
+                                      reinterpret_cast<DecTables *>(dec_tables), ctl, expect_raw_len);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
