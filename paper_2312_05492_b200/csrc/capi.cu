@@ -14,8 +14,9 @@ namespace cszi {
 int launch_ctl_init(cszi_ctl *ctl, cudaStream_t st);
 int launch_range(const float *x, uint64_t n, cszi_ctl *ctl, cudaStream_t st);
 int launch_tune(const float *x, const cszi_geom *g, const cszi_params *p, cszi_ctl *ctl,
-                int32_t *vals, cudaStream_t st);
-int launch_sample_gather(const float *x, const cszi_geom *g, int32_t *vals, cudaStream_t st);
+                int32_t *vals, cudaStream_t st, bool reset_outputs = false);
+int launch_sample_gather(const float *x, const cszi_geom *g, int32_t *vals, cudaStream_t st,
+                         cszi_ctl *reset_ctl = nullptr);
 int launch_tune_from_samples(const int32_t *vals, const cszi_geom *g, const cszi_params *p,
                              cszi_ctl *ctl, cudaStream_t st);
 uint64_t slab_anchor_count(const cszi_geom *g);
@@ -62,16 +63,7 @@ int launch_pass2_decode(const uint8_t *in, u64 n, uint8_t *out, u64 cap, void *s
 // small device helpers of the pipeline
 // ---------------------------------------------------------------------------
 // Reset the output fields of ctl, keeping the range of a prior cszi_range.
-__global__ void k_ctl_reset_outputs(cszi_ctl *ctl) {
-  ctl->bits = 0;
-  ctl->n_outliers = 0;
-  ctl->raw_len = 0;
-  ctl->payload_len = 0;
-  ctl->decoded_symbols = 0;
-  ctl->flags = 0;
-  ctl->max_len = 0;
-  for (int i = 0; i < 8; ++i) ctl->scratch[i] = 0;
-}
+
 
 // Sections after the anchors and codebook: bitstream bytes, then the
 // outlier section (archive.py:184-189: u64 count + packed (u64, f32)).
@@ -364,11 +356,9 @@ int cszi_compress(const float *x, const cszi_geom *g, const cszi_params *p,
   if (!range_done) {
     CK(launch_ctl_init(ctl, st));
     CK(launch_range(x, n, ctl, st));
-  } else {
-    k_ctl_reset_outputs<<<1, 1, 0, st>>>(ctl);
-    note_launch();
   }
-  CK(launch_tune(x, g, p, ctl, W.samples, st));
+  // a prior range scan is kept; its output fields are reset by the sample gather
+  CK(launch_tune(x, g, p, ctl, W.samples, st, range_done != 0));
   cudaMemsetAsync(W.hist, 0, 8 * nbins, st);
   bool nz = false;
   CK(launch_predict(x, g, R, ctl, W.sym, W.hist, p->exact != 0, st, W.nzmap, &nz));

@@ -17,6 +17,18 @@ typedef unsigned long long u64;
 
 // Host-side count of kernels this library launched (cszi_launch_count()).
 void note_launch(int n = 1);
+// Reset the output fields of ctl, keeping the range (and tuned config) of a
+// prior scan: one thread.
+DEV void ctl_reset_outputs(cszi_ctl *ctl) {
+  ctl->bits = 0;
+  ctl->n_outliers = 0;
+  ctl->raw_len = 0;
+  ctl->payload_len = 0;
+  ctl->decoded_symbols = 0;
+  ctl->flags = 0;
+  ctl->max_len = 0;
+  for (int i = 0; i < 8; ++i) ctl->scratch[i] = 0;
+}
 // Host-side launch helpers with per-device caches (the runtime queries cost
 // microseconds of CPU each, and the GPU idles while the host launches the
 // first kernels of a call): SM count, the dynamic shared-memory opt-in

@@ -185,9 +185,12 @@ DEV void sample_plan(const TuneArgs &A, SamplePlan &sp) {
 // One block of 1024 threads: the plan is built once in shared memory and
 // every sample load is in flight at the same time (a thread per value).
 __global__ void __launch_bounds__(1024) k_sample_gather(const float *__restrict__ x, TuneArgs A,
-                                                        int32_t *vals) {
+                                                        int32_t *vals, cszi_ctl *reset_ctl) {
   __shared__ SamplePlan sp;
-  if (threadIdx.x == 0) sample_plan(A, sp);
+  if (threadIdx.x == 0) {
+    if (reset_ctl) ctl_reset_outputs(reset_ctl);  // (was its own 1-thread launch)
+    sample_plan(A, sp);
+  }
   const int rank = A.rank, pad = A.pad_axes;
   for (int w = threadIdx.x; w < CSZI_SAMPLE_WORDS; w += blockDim.x) vals[w] = 0;
   __syncthreads();
@@ -365,13 +368,14 @@ static int tune_args(const cszi_geom *g, const cszi_params *p, TuneArgs &A) {
   return CSZI_OK;
 }
 
-int launch_sample_gather(const float *x, const cszi_geom *g, int32_t *vals, cudaStream_t st) {
+int launch_sample_gather(const float *x, const cszi_geom *g, int32_t *vals, cudaStream_t st,
+                         cszi_ctl *reset_ctl) {
   TuneArgs A;
   cszi_params p{};
   p.have_alpha = 1;
   const int rc = tune_args(g, &p, A);
   if (rc != CSZI_OK) return rc;
-  k_sample_gather<<<1, 1024, 0, st>>>(x, A, vals);
+  k_sample_gather<<<1, 1024, 0, st>>>(x, A, vals, reset_ctl);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
@@ -388,8 +392,8 @@ int launch_tune_from_samples(const int32_t *vals, const cszi_geom *g, const cszi
 
 // single device: gather (into ctl->scratch-sized device buffer) + decide
 int launch_tune(const float *x, const cszi_geom *g, const cszi_params *p, cszi_ctl *ctl,
-                int32_t *vals, cudaStream_t st) {
-  int rc = launch_sample_gather(x, g, vals, st);
+                int32_t *vals, cudaStream_t st, bool reset_outputs) {
+  int rc = launch_sample_gather(x, g, vals, st, reset_outputs ? ctl : nullptr);
   if (rc != CSZI_OK) return rc;
   return launch_tune_from_samples(vals, g, p, ctl, st);
 }
