@@ -218,6 +218,19 @@ int cszi_reconstruct(const uint16_t *sym, const float *anchors, const uint64_t *
                      const double *level_eb, int32_t nlev, const int32_t variant[3],
                      const int32_t order[3], float *y, void *stream);
 
+/* interpolate_level (predictor.py:367-392): the per-dimension passes of
+ * ONE level (stride s, bound level_eb) over a device reconstruction buffer
+ * recon[ext] (float32, C order), in dim order `order` (padded axes), with the
+ * anchor lattice restored from anchor_block (lattice row-major) after each
+ * pass.  mode 0 = Compress (reads source, writes recon, codes = q or 0,
+ * is_outlier 0/1 for every pass point), mode 1 = Decompress (reads codes,
+ * is_outlier, outlier_values[ext]; writes recon).  Replaces the reference's
+ * numpy _run_pass / _split_pass (predictor.py:283-364). */
+int cszi_interp_level(float *recon, const float *source, int32_t *codes, uint8_t *is_outlier,
+                      const float *outlier_values, const float *anchor_block, const cszi_geom *g,
+                      int64_t stride, double level_eb, const int32_t variant[3],
+                      const int32_t order[3], int32_t radius, int32_t mode, void *stream);
+
 /* gather_anchors (predictor.py:250-256): lattice row-major float32 values
  * (of the anchor planes inside g->slab when a slab is set). */
 int cszi_gather_anchors(const float *x, const cszi_geom *g, float *out, void *stream);

@@ -145,6 +145,11 @@ _SIGS = {
         ctypes.c_int, [_vp, _vp, _vp, _vp, _u64, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp]
     ),
     "cszi_gather_anchors": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "cszi_interp_level": (
+        ctypes.c_int,
+        [_vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_double, _vp, _vp, _i32, _i32,
+         _vp],
+    ),
     "cszi_slab_anchor_count": (_u64, [_vp]),
     "cszi_sample_gather": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "cszi_tune_from_samples": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
@@ -255,7 +260,11 @@ def ptr(tensor) -> ctypes.c_void_p:
 
 
 class Workspace:
-    """Grow-only per-device scratch buffer (uint8 torch tensor)."""
+    """Grow-only scratch buffers (uint8 torch tensors) keyed by (device,
+    stream, purpose).  Calls on one stream are ordered, so they may share a
+    buffer; calls on different streams get different buffers (a buffer
+    allocated and used on one stream only is also safe to free and regrow:
+    the caching allocator reuses it in that stream's order)."""
 
     def __init__(self):
         self._bufs = {}
@@ -263,7 +272,7 @@ class Workspace:
     def get(self, nbytes: int, key: str = "ws"):
         t = require_cuda()
         dev = t.cuda.current_device()
-        k = (dev, key)
+        k = (dev, _raw_stream(), key)
         buf = self._bufs.get(k)
         if buf is None or buf.numel() < nbytes:
             self._bufs[k] = None

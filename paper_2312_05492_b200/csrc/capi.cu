@@ -33,6 +33,10 @@ int launch_reconstruct(const uint16_t *sym, const float *anchors, const u64 *oid
                        const double *leb, int nlev, const int32_t variant[3],
                        const int32_t order[3], float *y, cudaStream_t st);
 int launch_gather_anchors(const float *x, const cszi_geom *g, float *out, cudaStream_t st);
+int launch_interp_level(float *recon, const float *source, int32_t *codes, uint8_t *is_out,
+                        const float *oval, const float *anchor_block, const cszi_geom *g,
+                        int64_t s, double leb, const int32_t variant[3], const int32_t order[3],
+                        int32_t R, int32_t mode, cudaStream_t st);
 int launch_hist_i32(const int32_t *codes, u64 n, int R, u64 *hist, cszi_ctl *ctl,
                     cudaStream_t st);
 int launch_codebook(const u64 *hist, int nbins, uint8_t *lengths, uint32_t *words,
@@ -551,6 +555,18 @@ int cszi_reconstruct(const uint16_t *sym, const float *anchors, const uint64_t *
   return launch_reconstruct(sym, anchors, reinterpret_cast<const u64 *>(out_idx), out_val, n_out,
                             nullptr, g, radius, level_eb, nlev, variant, order, y,
                             reinterpret_cast<cudaStream_t>(stream));
+}
+
+int cszi_interp_level(float *recon, const float *source, int32_t *codes, uint8_t *is_outlier,
+                      const float *outlier_values, const float *anchor_block, const cszi_geom *g,
+                      int64_t stride, double level_eb, const int32_t variant[3],
+                      const int32_t order[3], int32_t radius, int32_t mode, void *stream) {
+  if (!g || g->rank < 1 || g->rank > 3 || !recon || !codes || !is_outlier || !anchor_block ||
+      (mode == 0 && !source) || (mode == 1 && !outlier_values))
+    return CSZI_E_INVALID_ARG;
+  return launch_interp_level(recon, source, codes, is_outlier, outlier_values, anchor_block, g,
+                             stride, level_eb, variant, order, radius, mode,
+                             reinterpret_cast<cudaStream_t>(stream));
 }
 
 int cszi_gather_anchors(const float *x, const cszi_geom *g, float *out, void *stream) {

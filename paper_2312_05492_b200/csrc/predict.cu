@@ -837,10 +837,8 @@ int launch_predict(const float *x, const cszi_geom *g, int32_t radius, const csz
                    uint16_t *sym, u64 *hist, bool exact, cudaStream_t st, uint32_t *nzmap,
                    bool *nz_done) {
   if (nz_done) *nz_done = false;
-  if (g->rank == 3 && layout_is<fast::L3>(g) && !getenv("CSZI_OLD_PREDICT"))
-    return t3::launch_predict_t3(x, g, radius, ctl, sym, hist, exact, st, nzmap, nz_done);
   if (g->rank == 3 && layout_is<fast::L3>(g))
-    return launch_predict_fast<fast::L3, 128>(x, g, radius, ctl, sym, hist, exact, st);
+    return t3::launch_predict_t3(x, g, radius, ctl, sym, hist, exact, st, nzmap, nz_done);
   if (g->rank == 2 && layout_is<fast::L2>(g))
     return launch_predict_fast<fast::L2, 128>(x, g, radius, ctl, sym, hist, exact, st);
   if (g->rank == 1 && layout_is<fast::L1>(g))
@@ -865,11 +863,8 @@ int launch_reconstruct(const uint16_t *sym, const float *anchors, const u64 *oid
     lc.order[a] = order[a];
     lc.variant[a] = variant[a];
   }
-  if (g->rank == 3 && layout_is<fast::L3>(g) && nlev == 3 && !getenv("CSZI_OLD_PREDICT"))
+  if (g->rank == 3 && layout_is<fast::L3>(g) && nlev == 3)
     return t3::launch_recon_t3(sym, anchors, oidx, oval, nout, nout_dev, g, radius, lc, y, st);
-  if (g->rank == 3 && layout_is<fast::L3>(g))
-    return launch_recon_fast<fast::L3, 128>(sym, anchors, oidx, oval, nout, nout_dev, g, radius,
-                                            lc, y, st);
   if (g->rank == 2 && layout_is<fast::L2>(g))
     return launch_recon_fast<fast::L2, 128>(sym, anchors, oidx, oval, nout, nout_dev, g, radius,
                                             lc, y, st);
@@ -887,6 +882,127 @@ int launch_reconstruct(const uint16_t *sym, const float *anchors, const u64 *oid
     rc = launch_recon_t<1, 1, 1024>(sym, anchors, oidx, oval, nout, nout_dev, g, radius, lc, y, st);
   }
   return rc;
+}
+
+// ---------------------------------------------------------------------------
+// interpolate_level (predictor.py:367-392): one level's per-dimension passes
+// over a global-memory reconstruction buffer, one thread per pass point, in
+// the reference's exact point set and arithmetic, anchors restored after
+// each pass.  This is the fine-grained API (the reference's tests drive the
+// predictor level by level); the compress / decompress path runs all levels
+// inside the tile kernels instead.
+// ---------------------------------------------------------------------------
+struct LevelPass {
+  int64_t ext[3];
+  int64_t cnt[3];   // lattice points per axis
+  int64_t step[3];  // lattice step per axis (d: 2s starting at s)
+  int64_t tile;     // super-chunk extent along d
+  int d;
+  int s;
+  int R;
+  double leb, e2, wo, wi;
+};
+
+// mode 0 (Compress): source -> recon / codes (q or 0) / is_outlier;
+// mode 1 (Decompress): codes / is_outlier / outlier_values -> recon
+__global__ void k_level_pass(LevelPass L, int mode, float *__restrict__ recon,
+                             const float *__restrict__ source, int32_t *__restrict__ codes,
+                             uint8_t *__restrict__ is_out, const float *__restrict__ oval) {
+  const int64_t total = L.cnt[0] * L.cnt[1] * L.cnt[2];
+  const int64_t st1 = L.ext[2], st0 = L.ext[1] * L.ext[2];
+  const int64_t sd = (L.d == 0) ? st0 : (L.d == 1) ? st1 : 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i2 = i % L.cnt[2], r = i / L.cnt[2], i1 = r % L.cnt[1], i0 = r / L.cnt[1];
+    int64_t c[3] = {i0 * L.step[0], i1 * L.step[1], i2 * L.step[2]};
+    c[L.d] += L.s;  // odd multiples of s along d
+    const int64_t pd = c[L.d], ed = L.ext[L.d], s = L.s;
+    const int64_t off = pd % L.tile;
+    const bool m3 = off >= 3 * s;
+    const bool p1 = pd + s <= ed - 1;
+    const bool p3 = (off <= L.tile - 3 * s) && (pd + 3 * s <= ed - 1);
+    const int cs = !p1 ? 4 : m3 ? (p3 ? 0 : 1) : (p3 ? 2 : 3);
+    const int64_t ix = c[0] * st0 + c[1] * st1 + c[2];
+    const double vm1 = f2d(recon[ix - s * sd]);
+    const double vp1 = p1 ? f2d(recon[ix + s * sd]) : 0.0;
+    const double vm3 = m3 ? f2d(recon[ix - 3 * s * sd]) : 0.0;
+    const double vp3 = p3 ? f2d(recon[ix + 3 * s * sd]) : 0.0;
+    const double pred = spline4(cs, L.wo, L.wi, vm3, vm1, vp1, vp3);
+    if (mode == 0) {
+      float rec;
+      const uint32_t sy = quantize<true>(pred, source[ix], L.leb, L.e2, 0.0, L.R, rec);
+      recon[ix] = rec;
+      codes[ix] = sy ? (int32_t)sy - L.R : 0;
+      is_out[ix] = sy ? 0 : 1;
+    } else {
+      const double q = (double)codes[ix];
+      const float rec = __double2float_rn(dadd(pred, dmul(L.e2, q)));
+      recon[ix] = is_out[ix] ? oval[ix] : rec;
+    }
+  }
+}
+
+// recon[anchor lattice] = anchor_block (lattice row-major)
+__global__ void k_anchor_restore(float *__restrict__ recon, const float *__restrict__ block,
+                                 int64_t e0, int64_t e1, int64_t e2, int64_t S, int64_t na0,
+                                 int64_t na1, int64_t na2) {
+  const int64_t total = na0 * na1 * na2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i2 = i % na2, t = i / na2, i1 = t % na1, i0 = t / na1;
+    const int64_t c0 = min(i0 * S, e0 - 1), c1 = min(i1 * S, e1 - 1), c2 = min(i2 * S, e2 - 1);
+    recon[(c0 * e1 + c1) * e2 + c2] = block[i];
+  }
+}
+
+int launch_interp_level(float *recon, const float *source, int32_t *codes, uint8_t *is_out,
+                        const float *oval, const float *anchor_block, const cszi_geom *g,
+                        int64_t s, double leb, const int32_t variant[3], const int32_t order[3],
+                        int32_t R, int32_t mode, cudaStream_t st) {
+  if (s < 1 || (s & (s - 1)) || !(leb > 0) || R < 2 || (mode != 0 && mode != 1))
+    return CSZI_E_INVALID_ARG;
+  const int64_t S = g->stride;
+  int64_t na[3];
+  for (int a = 0; a < 3; ++a) na[a] = (g->ext[a] - 1) / S + 1 + (((g->ext[a] - 1) % S) ? 1 : 0);
+  const int pad = 3 - g->rank;
+  int passed = 0;
+  for (int i = 0; i < g->rank; ++i) {
+    const int d = order[i];
+    if (d < pad || d > 2) return CSZI_E_INVALID_ARG;
+    LevelPass L;
+    int64_t total = 1;
+    for (int a = 0; a < 3; ++a) {
+      L.ext[a] = g->ext[a];
+      if (a == d) {
+        L.step[a] = 2 * s;
+        L.cnt[a] = g->ext[a] > s ? (g->ext[a] - s + 2 * s - 1) / (2 * s) : 0;
+      } else {
+        L.step[a] = ((passed >> a) & 1) ? s : 2 * s;
+        L.cnt[a] = (g->ext[a] + L.step[a] - 1) / L.step[a];
+      }
+      total *= L.cnt[a];
+    }
+    L.tile = g->tile[d];
+    L.d = d;
+    L.s = (int)s;
+    L.R = R;
+    L.leb = leb;
+    L.e2 = 2.0 * leb;
+    L.wo = variant[d] == 0 ? NAK_O : NAT_O;
+    L.wi = variant[d] == 0 ? NAK_I : NAT_I;
+    if (total > 0) {
+      int64_t blocks = (total + 255) / 256;
+      if (blocks > (int64_t)sm_count() * 16) blocks = (int64_t)sm_count() * 16;
+      k_level_pass<<<(unsigned)blocks, 256, 0, st>>>(L, mode, recon, source, codes, is_out, oval);
+      note_launch();
+      const int64_t ta = na[0] * na[1] * na[2];
+      k_anchor_restore<<<(unsigned)std::min<int64_t>((ta + 255) / 256, 4096), 256, 0, st>>>(
+          recon, anchor_block, g->ext[0], g->ext[1], g->ext[2], S, na[0], na[1], na[2]);
+      note_launch();
+    }
+    passed |= 1 << d;
+  }
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
 int launch_gather_anchors(const float *x, const cszi_geom *g, float *out, cudaStream_t st) {

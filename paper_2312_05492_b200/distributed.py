@@ -29,7 +29,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .archive import EB_ABS, EB_REL, PREDICTOR_INTERP, pack_header
+from .archive import EB_ABS, EB_REL, HEADER_SIZE, PREDICTOR_INTERP, pack_header, unpack_header
 from .errors import EmptyHistogram, Inconsistent, LengthOverflow, NonFiniteValue
 from .pipeline import DeviceArchive
 from .predictor import count_anchors, ctl_order, ctl_variants, default_layout, make_geom, make_params
@@ -469,6 +469,11 @@ def decompress_sharded(data, nz: int = None, group=None):
         head = data[:HEADER_SIZE] if not isinstance(data, DeviceArchive) else data.header
         nz = unpack_header(bytes(head), len(data)).extents[0]
     z0, z1 = slab_bounds(nz, dist.get_world_size(group))[dist.get_rank(group)]
+    if z1 <= z0:  # more ranks than z tiles: this rank owns no planes
+        t = _lib.require_cuda()
+        head = data.header if isinstance(data, DeviceArchive) else bytes(data[:HEADER_SIZE])
+        ext = unpack_header(head, len(data)).extents
+        return z0, z1, t.empty((0, ext[1], ext[2]), dtype=t.float32, device="cuda")
     return z0, z1, decompress_slab(data, z0, z1)
 
 

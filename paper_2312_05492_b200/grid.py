@@ -100,8 +100,9 @@ class Grid:
         c = ctl.fetch()
         if c.first_nonfinite != 2**64 - 1:
             raise NonFiniteValue(int(c.first_nonfinite))
+        # The tensor is aliased, not copied: compress() rescans it per call,
+        # so no range from this scan is kept (in-place updates stay visible).
         self._dev = t.view(self.dims.extents)
-        self._ctl = ctl
 
     @classmethod
     def wrap_host(cls, dims: Dims, arr) -> "Grid":
@@ -206,14 +207,17 @@ def store_raw(grid: Grid, path) -> None:
 
 
 def value_range(grid: Grid) -> tuple:
-    """(min, max, max - min) as Python floats (grid.py:104-108); device grids
-    report the range their construction-time range kernel computed."""
-    if grid.is_device and grid._ctl is not None:
-        from ._lib import Ctl  # noqa: F401
-
-        c = grid._ctl.fetch()
+    """(min, max, max - min) as Python floats (grid.py:104-108); a device grid
+    is scanned on the GPU (order-independent min / max: exact)."""
+    if grid.is_device:
+        from . import _lib
         from ._keys import key_to_float
 
+        ctl = _lib.DeviceCtl()
+        t = grid.tensor
+        _lib.check(_lib.load().cszi_scan_field(_lib.ptr(t), t.numel(), ctl.ptr,
+                                               _lib.stream_ptr()), "range")
+        c = ctl.fetch()
         lo = key_to_float(c.vmin_key)
         hi = key_to_float(c.vmax_key)
         return lo, hi, hi - lo

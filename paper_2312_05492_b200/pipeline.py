@@ -186,8 +186,11 @@ def compress_device(grid: Grid, eb: float, mode: str = "rel", predictor: str = "
     st = _lib.stream_ptr()
     x = grid.tensor
     n = grid.dims.count
-    range_done = grid.is_device and grid._ctl is not None
-    ctl = grid._ctl if range_done else _lib.DeviceCtl()
+    # The range / finite scan runs inside every call (a device Grid may have
+    # been updated in place since construction; the reference recomputes
+    # value_range per compress, tuning.py:46), with a per-call ctl record.
+    range_done = False
+    ctl = _lib.DeviceCtl()
     if alpha is not None:
         a = float(alpha)
     elif mode == "rel":
@@ -382,6 +385,11 @@ def decompress_device(data, threads: int = None, slab=None):
     if d_payload is None:
         d_payload = _lib.to_device_u8(h_payload)
     raw_len = sum(h.sec_lens)
+    if dev_pass2 and raw_len > 128 * d_payload.numel():
+        # a zero-run control byte expands to at most 128 bytes (pass2.py:30-67):
+        # a header claiming more cannot match, so fail before sizing buffers
+        raise LengthMismatch(f"sections total {raw_len} bytes exceeds what a "
+                             f"{d_payload.numel()}-byte pass-2 stream can hold")
     if not dev_pass2 and d_payload.numel() != raw_len:
         raise LengthMismatch(f"sections total {d_payload.numel()} bytes, header says {raw_len}")
     dims = Dims(h.extents)
@@ -399,8 +407,12 @@ def decompress_device(data, threads: int = None, slab=None):
         if h.rank != 3 or layout.anchor_stride != 8 or layout.super_chunk_extents != (8, 8, 32):
             raise NotImplementedError("slab decompress needs a 3-D default-layout archive")
         nz = h.extents[0]
-        if not (0 <= z0 < z1 <= nz) or z0 % 8:
-            raise ValueError(f"slab [{z0}, {z1}) must start on an anchor plane inside [0, {nz})")
+        if not (0 <= z0 < z1 <= nz) or z0 % 8 or (z1 % 8 and z1 != nz):
+            # a slab is a run of whole 8-plane tiles: its last tile's closing
+            # plane (z1, or nz - 1) is decoded as the halo; an unaligned z1
+            # would cut a tile the reconstructor stores in full
+            raise ValueError(f"slab [{z0}, {z1}) must start and end on anchor planes "
+                             f"(multiples of 8, or {nz}) inside [0, {nz}]")
         geom.slab[0], geom.slab[1] = z0, z1
         out_n = (z1 - z0) * h.extents[1] * h.extents[2]
     plan = plan_levels(layout.anchor_stride, h.eb_abs, h.alpha)

@@ -258,6 +258,85 @@ def ctl_order(c: _lib.Ctl, rank: int) -> tuple:
 
 
 # ---------------------------------------------------------------------------
+# level execution (predictor.py:264-392): the fine-grained per-level API
+# ---------------------------------------------------------------------------
+
+@dataclass
+class Compress:
+    """Quantize against ``source`` while reconstructing (predictor.py:264-271).
+    Arrays are numpy (updated in place after the GPU pass) or CUDA tensors
+    (updated in HBM)."""
+
+    source: object
+    codes: object
+    is_outlier: object
+    anchor_block: object
+
+
+@dataclass
+class Decompress:
+    """Reconstruct from stored codes and outlier values (predictor.py:274-281)."""
+
+    codes: object
+    is_outlier: object
+    outlier_values: object
+    anchor_block: object
+
+
+def _dev(a, dtype):
+    """(CUDA tensor view, write-back numpy array or None) for a level operand."""
+    t = _lib.torch()
+    if isinstance(a, t.Tensor):
+        if not a.is_cuda or not a.is_contiguous():
+            raise ValueError("device operands must be contiguous CUDA tensors")
+        if dtype == np.bool_:
+            return a.view(t.uint8), None
+        return a, None
+    arr = np.asarray(a)
+    host = np.ascontiguousarray(arr, dtype=dtype)
+    d = t.from_numpy(host.view(np.uint8) if dtype == np.bool_ else host).cuda()
+    return d, arr
+
+
+def interpolate_level(recon, level: LevelStep, config: PredictorConfig, mode,
+                      threads: int = 1) -> None:
+    """Run one level's per-dimension passes on the GPU (predictor.py:367-392);
+    ``recon`` must hold lattice 2s.  Same point sets, arithmetic and anchor
+    restores as the reference; numpy operands are written back in place."""
+    t = _lib.require_cuda()
+    lib = _lib.load()
+    extents = tuple(int(e) for e in (recon.shape if hasattr(recon, "shape") else ()))
+    rank = len(extents)
+    if rank != config.layout.rank:
+        raise Inconsistent("recon rank does not match the layout")
+    d_rec, h_rec = _dev(recon, np.float32)
+    comp = isinstance(mode, Compress)
+    if not comp and not isinstance(mode, Decompress):
+        raise TypeError("mode must be Compress or Decompress")
+    d_codes, h_codes = _dev(mode.codes, np.int32)
+    d_out, h_out = _dev(mode.is_outlier, np.bool_)
+    d_anc, _ = _dev(mode.anchor_block, np.float32)
+    d_src = _dev(mode.source, np.float32)[0] if comp else None
+    d_oval = None if comp else _dev(mode.outlier_values, np.float32)[0]
+    geom = make_geom(extents, config.layout)
+    pad = 3 - rank
+    var = (ctypes.c_int32 * 3)(*((0,) * pad + tuple(int(v) for v in config.cubic_variant_per_dim)))
+    order = (ctypes.c_int32 * 3)(*(tuple(pad + int(d) for d in config.dim_order) + (0,) * pad))
+    _lib.check(lib.cszi_interp_level(
+        _lib.ptr(d_rec), _lib.ptr(d_src) if comp else None, _lib.ptr(d_codes), _lib.ptr(d_out),
+        None if comp else _lib.ptr(d_oval), _lib.ptr(d_anc), ctypes.byref(geom),
+        int(level.stride), float(level.eb), var, order, int(config.quant_radius),
+        0 if comp else 1, _lib.stream_ptr()), "interp_level")
+    if h_rec is not None:
+        h_rec[...] = d_rec.cpu().numpy().reshape(h_rec.shape)
+    if comp:
+        if h_codes is not None:
+            h_codes[...] = d_codes.cpu().numpy().reshape(h_codes.shape)
+        if h_out is not None:
+            h_out[...] = d_out.cpu().numpy().view(np.bool_).reshape(h_out.shape)
+
+
+# ---------------------------------------------------------------------------
 # GPU-backed predictor API
 # ---------------------------------------------------------------------------
 

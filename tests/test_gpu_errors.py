@@ -103,3 +103,49 @@ def test_device_grid_nonfinite():
     with pytest.raises(P.NonFiniteValue) as e:
         P.Grid(P.Dims((1000,)), x)
     assert e.value.index == 123
+
+
+def test_pass2_section_lengths_beyond_expansion_rejected(blobs):
+    """A header whose section lengths exceed what the pass-2 stream could
+    expand to fails with LengthMismatch before any buffer is sized."""
+    _, p2 = blobs
+    b = bytearray(p2)
+    # sec_lens live at offset 64 (<4s6B3B3B2I3Q3d then 5Q): inflate the bitstream
+    off = struct.calcsize("<4s6B3B3B2I3Q3d") + 16
+    struct.pack_into("<Q", b, off, 1 << 40)
+    with pytest.raises(P.LengthMismatch):
+        P.decompress(bytes(b))
+
+
+def test_slab_end_must_be_tile_aligned():
+    import torch
+
+    rng = np.random.default_rng(5)
+    data = smooth_field(rng, (40, 16, 32))
+    arch = P.compress_device(P.Grid(P.Dims(data.shape), torch.from_numpy(data).cuda()), 1e-3)
+    with pytest.raises(ValueError):
+        P.decompress_device(arch, slab=(0, 12))
+    with pytest.raises(ValueError):
+        P.decompress_device(arch, slab=(4, 16))
+    whole = P.decompress_device(arch).tensor
+    assert torch.equal(P.decompress_device(arch, slab=(8, 16)), whole[8:16])
+    assert torch.equal(P.decompress_device(arch, slab=(32, 40)), whole[32:40])
+
+
+def test_device_grid_updated_in_place_is_rescanned():
+    """A device Grid aliases its tensor; compress sees in-place updates (the
+    reference recomputes the range per call)."""
+    import torch
+
+    rng = np.random.default_rng(6)
+    data = smooth_field(rng, (24, 16, 32))
+    x = torch.from_numpy(data).cuda()
+    g = P.Grid(P.Dims(data.shape), x)
+    a0 = P.compress(g, 1e-3)
+    x.mul_(3.0)
+    a1 = P.compress(g, 1e-3)
+    assert a1 == P.compress(P.Grid(P.Dims(data.shape), data * np.float32(3.0)), 1e-3)
+    assert a1 != a0
+    x[3, 4, 5] = float("nan")
+    with pytest.raises(P.NonFiniteValue):
+        P.compress(g, 1e-3)

@@ -1,5 +1,6 @@
-"""Full-size checks: the bench workload (512^3, rel 1e-3) byte-identical to
-the oracle, plus size-independent properties on other SURVEY §8 configs."""
+"""Full-size check: the bench workload (512^3, rel 1e-3, field generated on the
+GPU as bench.py does) byte-identical to the oracle.  The other BASELINE
+configs are pinned to the reference's own archives in test_gpu_configs.py."""
 import hashlib
 
 import numpy as np
@@ -30,19 +31,3 @@ def test_nyx_512_cube_archive_identical_to_oracle():
     # checksum of the decompressed field against the oracle's
     assert hashlib.sha256(y.data.tobytes()).digest() == \
         hashlib.sha256(O.decompress(ref).tobytes()).digest()
-
-
-@pytest.mark.parametrize("shape,eb", [((100, 500, 500), 1e-2), ((256, 384, 384), 1e-5),
-                                      ((449, 449, 235), 1e-3)])
-def test_survey_configs_round_trip(shape, eb):
-    from bench import smooth_field_gpu
-
-    x = smooth_field_gpu(shape)
-    g = P.Grid(P.Dims(shape), x)
-    arch = P.compress_device(g, eb)
-    y = P.decompress_device(arch)
-    eb_abs = P.archive.unpack_header(arch.header, len(arch)).eb_abs
-    assert (x.double() - y.tensor.double()).abs().max().item() <= eb_abs
-    # encode -> decode -> re-encode is idempotent
-    arch2 = P.compress_device(P.Grid(P.Dims(shape), x), eb)
-    assert arch2.to_bytes() == arch.to_bytes()
