@@ -5,8 +5,11 @@
 #include <atomic>
 #include <map>
 #include <mutex>
+#include <initializer_list>
 #include <tuple>
 #include <cstring>
+#include <string>
+#include <vector>
 
 #include "common.cuh"
 
@@ -325,6 +328,89 @@ int occupancy(const void *fn, int threads, size_t smem) {
 static std::atomic<unsigned long long> g_launches{0};
 void note_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
 
+// ---------------------------------------------------------------------------
+// CUDA-graph replay of the whole-path entry points.  A compress / decompress
+// call is a fixed, data-independent launch sequence (every data-dependent
+// decision is a device predicate), so it is captured once per distinct
+// argument set (pointers, geometry, parameters, stream, device, env
+// switches) and replayed with one cudaGraphLaunch: the GPU no longer waits
+// on the host issuing ~20 launches, and the host issues one.  Captures run
+// on a private stream (the caller's may be the legacy default stream, which
+// cannot be captured); the executable graph is launched on the caller's.
+// CSZI_NO_GRAPH=1 launches directly.
+// ---------------------------------------------------------------------------
+struct GraphEntry {
+  std::string key;
+  cudaGraphExec_t exec;
+  unsigned long long launches;
+};
+static std::mutex g_graph_mu;
+static std::vector<GraphEntry> g_graphs;  // most recently used last
+constexpr size_t GRAPH_CACHE = 16;
+
+static cudaStream_t capture_stream(int dev) {
+  static cudaStream_t cs[64] = {};
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!cs[dev]) cudaStreamCreateWithFlags(&cs[dev], cudaStreamNonBlocking);
+  return cs[dev];
+}
+
+template <class F>
+static int run_graphed(std::string key, cudaStream_t st, F &&body) {
+  if (getenv("CSZI_NO_GRAPH")) return body(st);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const void *sp = st;
+  key.append(reinterpret_cast<const char *>(&sp), sizeof(sp));
+  key.append(reinterpret_cast<const char *>(&dev), sizeof(dev));
+  for (const char *e : {"CSZI_NO_TMA", "CSZI_NO_NZ"}) key.push_back(getenv(e) ? '1' : '0');
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  for (size_t i = 0; i < g_graphs.size(); ++i) {
+    if (g_graphs[i].key == key) {
+      GraphEntry e = g_graphs[i];
+      g_graphs.erase(g_graphs.begin() + i);
+      g_graphs.push_back(e);
+      if (cudaGraphLaunch(e.exec, st) != cudaSuccess) return CSZI_E_CUDA;
+      note_launch((int)e.launches);
+      return CSZI_OK;
+    }
+  }
+  cudaStream_t cs = capture_stream(dev);
+  if (!cs) return body(st);
+  const unsigned long long l0 = g_launches.load();
+  if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+    cudaGetLastError();
+    return body(st);
+  }
+  const int rc = body(cs);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(cs, &graph);
+  const unsigned long long nl = g_launches.load() - l0;
+  g_launches.fetch_sub(nl);  // captured, not executed
+  if (rc != CSZI_OK || ec != cudaSuccess || !graph) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    return rc != CSZI_OK ? rc : CSZI_E_CUDA;
+  }
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ei != cudaSuccess) return CSZI_E_CUDA;
+  if (g_graphs.size() >= GRAPH_CACHE) {
+    cudaGraphExecDestroy(g_graphs.front().exec);
+    g_graphs.erase(g_graphs.begin());
+  }
+  g_graphs.push_back({key, exec, nl});
+  if (cudaGraphLaunch(exec, st) != cudaSuccess) return CSZI_E_CUDA;
+  note_launch((int)nl);
+  return CSZI_OK;
+}
+
+template <class T>
+static void key_add(std::string &k, const T &v) {
+  k.append(reinterpret_cast<const char *>(&v), sizeof(T));
+}
+
 }  // namespace cszi
 
 using namespace cszi;
@@ -344,10 +430,10 @@ uint64_t cszi_payload_capacity(const cszi_geom *g, int32_t radius, const cszi_ca
   return raw + raw / 128 + 64;
 }
 
-int cszi_compress(const float *x, const cszi_geom *g, const cszi_params *p,
-                  const cszi_caps *caps, int32_t pass2, int32_t range_done, uint8_t *payload,
-                  void *workspace, uint64_t ws_bytes, cszi_ctl *ctl, void *stream) {
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+static int compress_body(const float *x, const cszi_geom *g, const cszi_params *p,
+                         const cszi_caps *caps, int32_t pass2, int32_t range_done,
+                         uint8_t *payload, void *workspace, uint64_t ws_bytes, cszi_ctl *ctl,
+                         cudaStream_t st) {
   const int32_t R = p->radius;
   CK(check_geom(g, R));
   CompressWS W;
@@ -388,18 +474,35 @@ int cszi_compress(const float *x, const cszi_geom *g, const cszi_params *p,
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
+int cszi_compress(const float *x, const cszi_geom *g, const cszi_params *p,
+                  const cszi_caps *caps, int32_t pass2, int32_t range_done, uint8_t *payload,
+                  void *workspace, uint64_t ws_bytes, cszi_ctl *ctl, void *stream) {
+  if (!x || !g || !p || !caps || !ctl) return CSZI_E_INVALID_ARG;
+  std::string k("C");
+  for (const void *q : {(const void *)x, (const void *)payload, (const void *)workspace, (const void *)ctl})
+    key_add(k, q);
+  key_add(k, *g);
+  key_add(k, *p);
+  key_add(k, *caps);
+  key_add(k, pass2);
+  key_add(k, range_done);
+  key_add(k, ws_bytes);
+  return run_graphed(std::move(k), reinterpret_cast<cudaStream_t>(stream), [&](cudaStream_t st) {
+    return compress_body(x, g, p, caps, pass2, range_done, payload, workspace, ws_bytes, ctl, st);
+  });
+}
+
 uint64_t cszi_decompress_workspace_size(const cszi_geom *g, int32_t radius,
                                         const uint64_t sec_len[4], uint64_t payload_len) {
   return layout_decompress(g, radius, reinterpret_cast<const u64 *>(sec_len), payload_len, 1,
                            nullptr, nullptr) + 256;
 }
 
-int cszi_decompress(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
-                    const uint64_t sec_len[4], const cszi_geom *g, int32_t radius,
-                    const double *level_eb, int32_t nlev, const int32_t variant[3],
-                    const int32_t order[3], int32_t table_mode, float *y, void *workspace,
-                    uint64_t ws_bytes, cszi_ctl *ctl, void *stream) {
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+static int decompress_body(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
+                           const uint64_t sec_len[4], const cszi_geom *g, int32_t radius,
+                           const double *level_eb, int32_t nlev, const int32_t variant[3],
+                           const int32_t order[3], int32_t table_mode, float *y,
+                           void *workspace, uint64_t ws_bytes, cszi_ctl *ctl, cudaStream_t st) {
   CK(check_geom(g, radius));
   DecompressWS W;
   const u64 need = layout_decompress(g, radius, reinterpret_cast<const u64 *>(sec_len),
@@ -438,6 +541,34 @@ int cszi_decompress(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
                         reinterpret_cast<const u64 *>(&ctl->n_outliers), g, radius, level_eb,
                         nlev, variant, order, y, st));
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
+int cszi_decompress(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
+                    const uint64_t sec_len[4], const cszi_geom *g, int32_t radius,
+                    const double *level_eb, int32_t nlev, const int32_t variant[3],
+                    const int32_t order[3], int32_t table_mode, float *y, void *workspace,
+                    uint64_t ws_bytes, cszi_ctl *ctl, void *stream) {
+  if (!payload || !sec_len || !g || !level_eb || !variant || !order || !ctl || nlev < 0 ||
+      nlev > CSZI_MAX_LEVELS)
+    return CSZI_E_INVALID_ARG;
+  std::string k("D");
+  for (const void *q : {(const void *)payload, (const void *)y, (const void *)workspace, (const void *)ctl})
+    key_add(k, q);
+  key_add(k, payload_len);
+  key_add(k, pass2);
+  k.append(reinterpret_cast<const char *>(sec_len), 4 * sizeof(uint64_t));
+  key_add(k, *g);
+  key_add(k, radius);
+  k.append(reinterpret_cast<const char *>(level_eb), nlev * sizeof(double));
+  key_add(k, nlev);
+  k.append(reinterpret_cast<const char *>(variant), 3 * sizeof(int32_t));
+  k.append(reinterpret_cast<const char *>(order), 3 * sizeof(int32_t));
+  key_add(k, table_mode);
+  key_add(k, ws_bytes);
+  return run_graphed(std::move(k), reinterpret_cast<cudaStream_t>(stream), [&](cudaStream_t st) {
+    return decompress_body(payload, payload_len, pass2, sec_len, g, radius, level_eb, nlev,
+                           variant, order, table_mode, y, workspace, ws_bytes, ctl, st);
+  });
 }
 
 int cszi_ctl_fetch(const cszi_ctl *ctl, cszi_ctl *host, void *stream) {

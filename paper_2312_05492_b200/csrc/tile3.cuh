@@ -37,6 +37,8 @@
 
 #include <cuda.h>
 
+#include "interp_common.cuh"
+
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
@@ -64,6 +66,7 @@ constexpr int R_WARP = ((SYM_BYTES + BUF_BYTES) + 127) & ~127;   // 18304
 
 struct Lv {
   double leb, e2, inv, lebs;
+  float a32;  // interior fast path: accept |RN32(rec - o)| <= a32 (see quant_i)
 };
 
 struct Geo {
@@ -722,6 +725,8 @@ DEV void run_levels(const Tile &T, const Cfg &C, int R, bool exact, const Out &O
   }
 }
 
+#include "tile3i.cuh"
+
 // Interior tiles (closing plane inside the grid on every axis) form the box
 // ni[0] x ni[1] x ni[2]; edge tiles are the shell around it (z beyond, then
 // y beyond, then x beyond).  t indexes one set, x fastest.
@@ -887,6 +892,7 @@ __global__ void __launch_bounds__(NT, 3)
     C.lv[i].e2 = dmul(2.0, leb);
     C.lv[i].inv = ctl->inv_e2[i];
     C.lv[i].lebs = dsub(fmin(dmul(leb, 1.0 - 0x1p-40), 0x1p100), 0x1p-148);
+    C.lv[i].a32 = __fmul_rd(__double2float_rd(leb), 1.0f - 0x1p-23f);
     C.order[i] = ctl->order[i];
     C.nak[i] = ctl->variant[i] == 0;
   }
@@ -911,8 +917,14 @@ __global__ void __launch_bounds__(NT, 3)
     T.codes = codes;
     T.syms = 0;
     tile_init(T, G, o, t >= nint);
-    // codes default to R (anchors: code 0, predictor.py:414)
-    for (int i = lane; i < NCODE / 8; i += 32) sts_u4(codes + 16u * i, make_uint4(rr, rr, rr, rr));
+    // codes default to R (anchors: code 0, predictor.py:414).  Interior
+    // tiles write every owned non-anchor code in their passes, so only the
+    // four anchors of the tile's (0, 0) row are set; edge tiles reset all.
+    if (t >= nint) {
+      for (int i = lane; i < NCODE / 8; i += 32) sts_u4(codes + 16u * i, make_uint4(rr, rr, rr, rr));
+    } else if (lane < 4) {
+      sts_u16(codes + 2u * 8 * lane, (uint32_t)R);
+    }
     if (nzmap) {
       nzs[lane] = 0u;
       nzs[lane + 32] = 0u;
@@ -927,8 +939,8 @@ __global__ void __launch_bounds__(NT, 3)
     __syncwarp();
     T3P_CLOCK(c2);
     const unsigned int raw = ticket_issue(q);
-    if (T.bnd) run_levels<0, true>(T, C, R, exact, O);
-    else run_levels<0, false>(T, C, R, exact, O);
+    if (T.bnd || exact) run_levels<0, true>(T, C, R, exact, O);
+    else run_levels_i<0>(T, C, R, O);
     T3P_CLOCK(c3);
     // staging buffer free: prefetch the next tile
     const int tn = ticket_read(raw);
@@ -1066,6 +1078,7 @@ __global__ void __launch_bounds__(NT, 3)
     C.lv[i].e2 = dmul(2.0, leb);
     C.lv[i].inv = 0.0;
     C.lv[i].lebs = 0.0;
+    C.lv[i].a32 = 0.f;
     C.order[i] = lc.order[i];
     C.nak[i] = lc.variant[i] == 0;
   }
@@ -1119,7 +1132,7 @@ __global__ void __launch_bounds__(NT, 3)
     __syncwarp();
     const unsigned int raw = ticket_issue(q);
     if (T.bnd) run_levels<1, true>(T, C, R, false, O);
-    else run_levels<1, false>(T, C, R, false, O);
+    else run_levels_i<1>(T, C, R, O);
     const int tn = ticket_read(raw);
     if (lane == 0 && tn < ntiles && G.tma) {
       int on[3];
@@ -1249,7 +1262,7 @@ static bool t3_geo(const cszi_geom *g, int32_t radius, Geo &G) {
   return true;
 }
 
-static int launch_predict_t3(const float *x, const cszi_geom *g, int32_t radius,
+int launch_predict_t3(const float *x, const cszi_geom *g, int32_t radius,
                              const cszi_ctl *ctl, uint16_t *sym, u64 *hist, bool exact,
                              cudaStream_t st, uint32_t *nzmap, bool *nz_done) {
   Geo G;
@@ -1273,7 +1286,7 @@ static int launch_predict_t3(const float *x, const cszi_geom *g, int32_t radius,
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
-static int launch_recon_t3(const uint16_t *sym, const float *anchors, const u64 *oidx,
+int launch_recon_t3(const uint16_t *sym, const float *anchors, const u64 *oidx,
                            const float *oval, u64 nout, const u64 *nout_dev, const cszi_geom *g,
                            int32_t radius, const LevelCfg &lc, float *y, cudaStream_t st) {
   Geo G;

@@ -1,9 +1,13 @@
 """Grid data model (mirrors ebcomp/grid.py:19-108).
 
 A Grid holds up to three dimensions of float32, slowest axis first.  Besides
-the reference's host (numpy) form, a Grid may wrap a CUDA tensor: the finite
-scan (grid.py:60-62) then runs as the libcszi range kernel, which also
-leaves the value range (grid.py:104-108) on the device for compress().
+the reference's host (numpy) form, a Grid may wrap a CUDA tensor.  Its finite
+scan (grid.py:60-62) is deferred to the first use of the grid: compress()
+runs the libcszi range kernel on every call anyway (value_range,
+grid.py:104-108) and raises NonFiniteValue from that scan before any other
+error, so a device grid costs no extra pass over HBM and no host sync at
+construction; ``data``, ``value_range`` and the fine-grained predictor entry
+points run the scan explicitly (``ensure_finite``).
 """
 
 from __future__ import annotations
@@ -93,16 +97,29 @@ class Grid:
             raise SizeMismatch(
                 f"{t.numel()} values for dims {self.dims.extents} ({self.dims.count} expected)"
             )
+        # The tensor is aliased, not copied (in-place updates stay visible to
+        # compress, which rescans it per call).  _ctl: finite scan done.
+        self._dev = t.view(self.dims.extents)
+        self._ctl = False
+
+    def ensure_finite(self) -> None:
+        """Run the deferred finite scan of a device grid (grid.py:60-62)."""
+        if self._dev is None or self._ctl:
+            return
+        from . import _lib
+
         lib = _lib.load()
         ctl = _lib.DeviceCtl()
+        t = self._dev
         _lib.check(lib.cszi_scan_field(_lib.ptr(t), t.numel(), ctl.ptr, _lib.stream_ptr()),
                    "range")
         c = ctl.fetch()
         if c.first_nonfinite != 2**64 - 1:
             raise NonFiniteValue(int(c.first_nonfinite))
-        # The tensor is aliased, not copied: compress() rescans it per call,
-        # so no range from this scan is kept (in-place updates stay visible).
-        self._dev = t.view(self.dims.extents)
+        self._ctl = True
+
+    def _mark_finite(self) -> None:
+        self._ctl = True
 
     @classmethod
     def wrap_host(cls, dims: Dims, arr) -> "Grid":
@@ -120,7 +137,7 @@ class Grid:
         g = cls.__new__(cls)
         g.dims = dims
         g._np = None
-        g._ctl = None
+        g._ctl = True
         g._dev = tensor.reshape(dims.extents)
         return g
 
@@ -128,6 +145,7 @@ class Grid:
     @property
     def data(self) -> np.ndarray:
         if self._np is None:
+            self.ensure_finite()
             self._np = self._dev.cpu().numpy().reshape(self.dims.extents)
         return self._np
 
@@ -218,6 +236,9 @@ def value_range(grid: Grid) -> tuple:
         _lib.check(_lib.load().cszi_scan_field(_lib.ptr(t), t.numel(), ctl.ptr,
                                                _lib.stream_ptr()), "range")
         c = ctl.fetch()
+        if c.first_nonfinite != 2**64 - 1:
+            raise NonFiniteValue(int(c.first_nonfinite))
+        grid._mark_finite()
         lo = key_to_float(c.vmin_key)
         hi = key_to_float(c.vmax_key)
         return lo, hi, hi - lo

@@ -229,6 +229,7 @@ def compress_device(grid: Grid, eb: float, mode: str = "rel", predictor: str = "
         break
     if c.flags & _lib.F_NONFINITE:
         raise NonFiniteValue(int(c.first_nonfinite))
+    grid._mark_finite()
     if c.flags & _lib.F_EB_NONPOSITIVE:
         raise Inconsistent("absolute error bound must be positive")
     if c.flags & _lib.F_EMPTY_HISTOGRAM:

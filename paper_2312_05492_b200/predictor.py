@@ -344,6 +344,7 @@ def _run_predict(grid: Grid, config: PredictorConfig, exact: bool = False):
     """cszi_tune (explicit config) + cszi_predict -> (sym uint16 tensor, hist, ctl)."""
     t = _lib.require_cuda()
     lib = _lib.load()
+    grid.ensure_finite()
     x = grid.tensor
     rank = grid.dims.rank
     geom = make_geom(grid.dims.extents, config.layout)

@@ -100,9 +100,16 @@ def test_device_grid_nonfinite():
 
     x = torch.ones(1000, device="cuda")
     x[123] = float("inf")
-    with pytest.raises(P.NonFiniteValue) as e:
-        P.Grid(P.Dims((1000,)), x)
-    assert e.value.index == 123
+    # the device grid defers its finite scan to first use (grid.py:60-62)
+    g = P.Grid(P.Dims((1000,)), x)
+    for use in (lambda: P.compress_device(g, 1e-3), lambda: g.data, g.ensure_finite,
+                lambda: P.value_range(g)):
+        with pytest.raises(P.NonFiniteValue) as e:
+            use()
+        assert e.value.index == 123
+    # abs mode reads the range back before anything else
+    with pytest.raises(P.NonFiniteValue):
+        P.compress(P.Grid(P.Dims((1000,)), x), 1e-3, mode="abs")
 
 
 def test_pass2_section_lengths_beyond_expansion_rejected(blobs):
