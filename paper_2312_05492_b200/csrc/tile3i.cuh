@@ -91,9 +91,17 @@ __device__ __noinline__ void fix_line(uint32_t a0, uint32_t stb, int np, uint32_
 
 // D = x: a lane walks one row (z, y) of the pass lattice; rows z in
 // [0, 8] step STZ, y in [0, 8] step STY.
+//
+// Closing planes at level 1: a point on the closing plane of axis A (z = 8,
+// y = 8 or x = 32) only ever feeds an A-pass, so once A has been passed at
+// the finest level its closing plane is dead (compress: its codes belong to
+// the next tile; decompress: it is not stored).  Level-1 passes after the
+// A-pass skip it (the last pass of a tile runs 64 instead of 81 rows).
 template <int S, int STZ, int STY, int MODE, bool NAK>
 DEV void iwalk_x(const Tile &T, double wo, double wi, const Lv &L, int R, const Out &O) {
-  constexpr int NZr = 8 / STZ + 1, NYr = 8 / STY + 1, NL = NZr * NYr, NP = 16 / S;
+  constexpr int NZr = (S == 1 && STZ == 1) ? 8 : 8 / STZ + 1;
+  constexpr int NYr = (S == 1 && STY == 1) ? 8 : 8 / STY + 1;
+  constexpr int NL = NZr * NYr, NP = 16 / S;
   // the last pass of a compress tile: its values are never read again
   constexpr bool LAST = MODE == 0 && S == 1 && STZ == 1 && STY == 1;
   const int lane = threadIdx.x & 31;
@@ -201,8 +209,8 @@ DEV void iwalk_col(const Tile &T, double wo, double wi, const Lv &L, int R, cons
   constexpr uint32_t PD4 = 4u * ((D == 0) ? PZ : PX);
   constexpr int NE = (STX == 1) ? 4 : (STX == 2) ? 2 : 1;  // x-lines per quad
   constexpr int QS_ = (STX == 8) ? 2 : 1;                   // quad step
-  constexpr int NQ = (STX == 8) ? 5 : 9;
-  constexpr int NA = 8 / STA + 1;
+  constexpr int NQ = (STX == 8) ? 5 : (S == 1 && STX == 1) ? 8 : 9;
+  constexpr int NA = (S == 1 && STA == 1) ? 8 : 8 / STA + 1;
   constexpr int ITEMS = NA * NQ;
   constexpr int NP = 4 / S;
   constexpr int NV = NP + 1;
