@@ -175,6 +175,35 @@ int cszi_decompress(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
                     const int32_t order[3], int32_t table_mode, float *y, void *workspace,
                     uint64_t ws_bytes, cszi_ctl *ctl, void *stream);
 
+/* ---- Lorenzo predictor (pipeline.py:123-150 / :202-203, lorenzo.py) ----
+ * compress(predictor="lorenzo"): range scan, eb_abs (rel: eb * range when
+ * the range is positive, else eb), the Lorenzo recurrence (wavefront tiles
+ * on the GPU, bit-exact with _kernels.py:104-215), histogram, codebook,
+ * Huffman, sections (no anchor section) and pass-2.  ctl->eb_abs, bits,
+ * n_outliers, payload_len and flags as for cszi_compress.  The payload
+ * capacity of cszi_payload_capacity() suffices. */
+uint64_t cszi_compress_lorenzo_workspace_size(const cszi_geom *g, int32_t radius,
+                                              const cszi_caps *caps);
+int cszi_compress_lorenzo(const float *x, const cszi_geom *g, int32_t mode_rel, double eb,
+                          int32_t radius, const cszi_caps *caps, int32_t pass2, uint8_t *payload,
+                          void *workspace, uint64_t ws_bytes, cszi_ctl *ctl, void *stream);
+/* decompress of a Lorenzo archive (an anchor section is ignored); workspace size:
+ * cszi_decompress_workspace_size(). */
+int cszi_decompress_lorenzo(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
+                            const uint64_t sec_len[4], const cszi_geom *g, int32_t radius,
+                            double eb_abs, int32_t table_mode, float *y, void *workspace,
+                            uint64_t ws_bytes, cszi_ctl *ctl, void *stream);
+/* lorenzo_predict_quantize (lorenzo.py:22-33): symbols q + radius (0 for an
+ * outlier) of x under the absolute bound eb_abs; rec: float32[n] scratch
+ * (the reconstruction). */
+int cszi_lorenzo_predict(const float *x, const cszi_geom *g, double eb_abs, int32_t radius,
+                         uint16_t *sym, float *rec, cszi_ctl *ctl, void *stream);
+/* lorenzo_reconstruct (lorenzo.py:36-53): symbols q + radius (0xFFFF at an
+ * outlier, whose value is looked up in out_idx / out_val) -> y. */
+int cszi_lorenzo_reconstruct(const uint16_t *sym, const uint64_t *out_idx, const float *out_val,
+                             uint64_t n_out, const cszi_geom *g, double eb_abs, int32_t radius,
+                             float *y, void *stream);
+
 /* ---- stage entry points (fine-grained API of the reference) ------------ */
 
 /* ctl := initial state (range keys reset, counters and flags zero). */

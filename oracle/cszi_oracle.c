@@ -496,3 +496,67 @@ int64_t orc_range(const float *x, int64_t n, float *lo, float *hi) {
   *hi = b;
   return -1;
 }
+
+/*
+ * Lorenzo predictor — _kernels.py:104-215 (lorenzo_1d/2d/3d), driven by
+ * lorenzo.py:22-53.  Rank-r grids are padded to 3D with leading extent-1
+ * axes; each rank keeps the reference's own expression (the 1D / 2D sums
+ * are not rewritten as the 3D one).  compress != 0: quantize `orig` into
+ * codes / is_out and write the reconstruction; else replay codes / is_out /
+ * outval into recon.
+ */
+int orc_lorenzo(int compress, int rank, const int64_t ext[3], const float *orig, float *recon,
+                int32_t *codes, uint8_t *is_out, const float *outval, double e2, int64_t radius,
+                double bound) {
+  const int64_t nz = ext[0], ny = ext[1], nx = ext[2];
+  for (int64_t z = 0; z < nz; ++z)
+    for (int64_t y = 0; y < ny; ++y)
+      for (int64_t x = 0; x < nx; ++x) {
+        const int64_t i = (z * ny + y) * nx + x;
+        double pred;
+        if (rank == 1) {
+          pred = x > 0 ? (double)recon[i - 1] : 0.0;
+        } else if (rank == 2) {
+          const double a = y > 0 ? (double)recon[i - nx] : 0.0;
+          const double b = x > 0 ? (double)recon[i - 1] : 0.0;
+          const double c = (y > 0 && x > 0) ? (double)recon[i - nx - 1] : 0.0;
+          pred = a + b - c;
+        } else {
+          const int64_t pz = ny * nx;
+          const double a1 = z > 0 ? (double)recon[i - pz] : 0.0;
+          const double a2 = y > 0 ? (double)recon[i - nx] : 0.0;
+          const double a3 = x > 0 ? (double)recon[i - 1] : 0.0;
+          const double a4 = (y > 0 && x > 0) ? (double)recon[i - nx - 1] : 0.0;
+          const double a5 = (z > 0 && x > 0) ? (double)recon[i - pz - 1] : 0.0;
+          const double a6 = (z > 0 && y > 0) ? (double)recon[i - pz - nx] : 0.0;
+          const double a7 = (z > 0 && y > 0 && x > 0) ? (double)recon[i - pz - nx - 1] : 0.0;
+          pred = a1 + a2 + a3 - a4 - a5 - a6 + a7;
+        }
+        if (compress) {
+          const double o = (double)orig[i];
+          const double t = (o - pred) / e2;
+          int64_t q = 0;
+          float r = 0.0f;
+          int outlier = 1;
+          if (fabs(t) < (double)radius - 0.5) {
+            q = (int64_t)trunc(t + copysign(0.5, t));
+            if (llabs(q) < radius) {
+              r = (float)(pred + e2 * (double)q);
+              if (fabs((double)r - o) <= bound) outlier = 0;
+            }
+          }
+          if (outlier) {
+            codes[i] = 0;
+            is_out[i] = 1;
+            recon[i] = orig[i];
+          } else {
+            codes[i] = (int32_t)q;
+            recon[i] = r;
+          }
+        } else {
+          if (is_out[i]) recon[i] = outval[i];
+          else recon[i] = (float)(pred + e2 * (double)codes[i]);
+        }
+      }
+  return ORC_OK;
+}

@@ -135,6 +135,19 @@ _SIGS = {
         ctypes.c_int,
         [_vp, _u64, _i32, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _i32, _vp, _vp, _u64, _vp, _vp],
     ),
+    "cszi_compress_lorenzo_workspace_size": (_u64, [_vp, _i32, _vp]),
+    "cszi_compress_lorenzo": (
+        ctypes.c_int,
+        [_vp, _vp, _i32, ctypes.c_double, _i32, _vp, _i32, _vp, _vp, _u64, _vp, _vp],
+    ),
+    "cszi_decompress_lorenzo": (
+        ctypes.c_int,
+        [_vp, _u64, _i32, _vp, _vp, _i32, ctypes.c_double, _i32, _vp, _vp, _u64, _vp, _vp],
+    ),
+    "cszi_lorenzo_predict": (ctypes.c_int, [_vp, _vp, ctypes.c_double, _i32, _vp, _vp, _vp, _vp]),
+    "cszi_lorenzo_reconstruct": (
+        ctypes.c_int, [_vp, _vp, _vp, _u64, _vp, ctypes.c_double, _i32, _vp, _vp]
+    ),
     "cszi_ctl_init": (ctypes.c_int, [_vp, _vp]),
     "cszi_ctl_fetch": (ctypes.c_int, [_vp, _vp, _vp]),
     "cszi_range": (ctypes.c_int, [_vp, _u64, _vp, _vp]),

@@ -66,6 +66,12 @@ u64 p2dec_scratch_bytes(u64 n);
 int launch_pass2_decode(const uint8_t *in, u64 n, uint8_t *out, u64 cap, void *scratch,
                         cszi_ctl *ctl, cudaStream_t st, int expand);
 
+int launch_lorenzo(int mode, const float *x, float *rec, uint16_t *sym, const cszi_geom *g,
+                   const cszi_ctl *ctl, double e2, int R, const u64 *oidx, const float *oval,
+                   const u64 *nout_dev, u64 nout_host, cudaStream_t st);
+int launch_lorenzo_eb(cszi_ctl *ctl, double eb, int rel, int R, cudaStream_t st);
+int launch_hist_sym(const uint16_t *sym, u64 n, int R, u64 *hist, cudaStream_t st);
+
 // ---------------------------------------------------------------------------
 // small device helpers of the pipeline
 // ---------------------------------------------------------------------------
@@ -216,6 +222,16 @@ static u64 layout_compress(const cszi_geom *g, int32_t R, const cszi_caps *caps,
   w.p2_scratch = c.take(p2enc_scratch_bytes(raw_capacity(g, R, caps)));
   if (W) *W = w;
   return c.used;
+}
+
+// Lorenzo compress: the interp layout (no anchors are written) plus the
+// float reconstruction the recurrence reads back across tiles
+static u64 layout_compress_lz(const cszi_geom *g, int32_t R, const cszi_caps *caps, void *base,
+                              CompressWS *W, float **rec) {
+  const u64 used = layout_compress(g, R, caps, base, W);
+  if (rec) *rec = base ? reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(base) + used)
+                       : nullptr;
+  return used + al(4 * grid_n(g) + 16);
 }
 
 struct DecompressWS {
@@ -415,6 +431,8 @@ static void key_add(std::string &k, const T &v) {
 
 using namespace cszi;
 
+static double dmul_host(double a, double b) { return a * b; }  // exact (x2)
+
 extern "C" {
 
 const char *cszi_version(void) {
@@ -569,6 +587,152 @@ int cszi_decompress(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
     return decompress_body(payload, payload_len, pass2, sec_len, g, radius, level_eb, nlev,
                            variant, order, table_mode, y, workspace, ws_bytes, ctl, st);
   });
+}
+
+// ---- Lorenzo predictor (pipeline.py:123-150, 202-203) ----------------------
+uint64_t cszi_compress_lorenzo_workspace_size(const cszi_geom *g, int32_t radius,
+                                              const cszi_caps *caps) {
+  return layout_compress_lz(g, radius, caps, nullptr, nullptr, nullptr) + 256;
+}
+
+static int lz_compress_body(const float *x, const cszi_geom *g, int32_t mode_rel, double eb,
+                            int32_t R, const cszi_caps *caps, int32_t pass2, uint8_t *payload,
+                            void *workspace, uint64_t ws_bytes, cszi_ctl *ctl, cudaStream_t st) {
+  CK(check_geom(g, R));
+  CompressWS W;
+  float *rec = nullptr;
+  const u64 need = layout_compress_lz(g, R, caps, workspace, &W, &rec);
+  if (ws_bytes < need) return CSZI_E_CAPACITY;
+  const u64 n = grid_n(g);
+  const u64 nbins = 2 * (u64)R;
+  const u64 raw_cap = raw_capacity(g, R, caps);
+  CK(launch_ctl_init(ctl, st));
+  CK(launch_range(x, n, ctl, st));  // value_range (pipeline.py:124)
+  CK(launch_lorenzo_eb(ctl, eb, mode_rel, R, st));
+  CK(launch_lorenzo(0, x, rec, W.sym, g, ctl, 0.0, R, nullptr, nullptr, nullptr, 0, st));
+  CK(launch_hist_sym(W.sym, n, R, W.hist, st));
+  uint8_t *raw = pass2 ? W.raw : payload;
+  uint8_t *lengths = raw;  // no anchor section
+  CK(launch_codebook(W.hist, (int)nbins, lengths, W.words, ctl, st, true));
+  const u64 head = nbins;
+  const bool in_place = ((reinterpret_cast<uintptr_t>(raw) + head) & 3) == 0;
+  uint32_t *bits_out = in_place ? reinterpret_cast<uint32_t *>(raw + head) : W.bits;
+  CK(launch_encode(0, W.sym, n, R, lengths, W.words, bits_out, caps->bits_cap, x, W.oidx, W.oval,
+                   caps->outlier_cap, W.enc_scratch, ctl, st, 0, 0, nullptr, W.hist, true));
+  k_assemble<<<grid_for(n / 16), 256, 0, st>>>(raw, head, reinterpret_cast<uint8_t *>(W.bits),
+                                                W.oidx, W.oval, x, raw_cap, caps->bits_cap,
+                                                caps->outlier_cap, ctl, pass2 ? 0 : 1,
+                                                in_place ? 1 : 0);
+  note_launch();
+  if (pass2)
+    CK(launch_pass2_encode(raw, reinterpret_cast<const u64 *>(&ctl->raw_len), raw_cap, payload,
+                           W.p2_scratch, ctl, st));
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
+int cszi_compress_lorenzo(const float *x, const cszi_geom *g, int32_t mode_rel, double eb,
+                          int32_t radius, const cszi_caps *caps, int32_t pass2, uint8_t *payload,
+                          void *workspace, uint64_t ws_bytes, cszi_ctl *ctl, void *stream) {
+  if (!x || !g || !caps || !ctl || !payload) return CSZI_E_INVALID_ARG;
+  std::string k("L");
+  for (const void *q : {(const void *)x, (const void *)payload, (const void *)workspace,
+                        (const void *)ctl})
+    key_add(k, q);
+  key_add(k, *g);
+  key_add(k, mode_rel);
+  key_add(k, eb);
+  key_add(k, radius);
+  key_add(k, *caps);
+  key_add(k, pass2);
+  key_add(k, ws_bytes);
+  return run_graphed(std::move(k), reinterpret_cast<cudaStream_t>(stream), [&](cudaStream_t st) {
+    return lz_compress_body(x, g, mode_rel, eb, radius, caps, pass2, payload, workspace,
+                            ws_bytes, ctl, st);
+  });
+}
+
+static int lz_decompress_body(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
+                              const uint64_t sec_len[4], const cszi_geom *g, int32_t radius,
+                              double eb_abs, int32_t table_mode, float *y, void *workspace,
+                              uint64_t ws_bytes, cszi_ctl *ctl, cudaStream_t st) {
+  CK(check_geom(g, radius));
+  DecompressWS W;
+  const u64 need = layout_decompress(g, radius, reinterpret_cast<const u64 *>(sec_len),
+                                     payload_len, 1, workspace, &W);
+  if (ws_bytes < need) return CSZI_E_CAPACITY;
+  const u64 n = grid_n(g);
+  const u64 nbins = 2 * (u64)radius;
+  const u64 raw_len = sec_len[0] + sec_len[1] + sec_len[2] + sec_len[3];
+  if (sec_len[1] != nbins) return CSZI_E_MALFORMED;
+  CK(launch_ctl_init(ctl, st));
+  const uint8_t *raw = payload;
+  if (pass2) {
+    CK(launch_pass2_decode(payload, payload_len, W.raw, raw_len, W.p2_scratch, ctl, st, 1));
+    raw = W.raw;
+  }
+  // an anchor section, if a crafted archive carries one, is ignored as the
+  // reference ignores it for Lorenzo archives
+  const uint8_t *lengths = raw + sec_len[0];
+  const uint8_t *bits = lengths + sec_len[1];
+  const uint8_t *outl = bits + sec_len[2];
+  CK(launch_canonical(lengths, (int)nbins, nullptr, W.dec_tables, ctl, st, pass2 ? raw_len : 0));
+  CK(launch_decode(bits, sec_len[2], n, radius, W.dec_tables, W.sym, 0, W.dec_scratch, ctl, st,
+                   table_mode, 32, 0, n));
+  const u64 kmax = sec_len[3] >= 8 ? (sec_len[3] - 8) / 12 : 0;
+  k_outliers_parse<<<grid_for(kmax), 256, 0, st>>>(outl, sec_len[3], n, W.oidx, W.oval, W.sym,
+                                                   ctl);
+  note_launch();
+  k_outliers_mark<<<grid_for(kmax), 256, 0, st>>>(W.oidx, ctl, n, W.sym, 0, n);
+  note_launch();
+  CK(launch_lorenzo(1, nullptr, y, W.sym, g, ctl, dmul_host(2.0, eb_abs), radius, W.oidx, W.oval,
+                    reinterpret_cast<const u64 *>(&ctl->n_outliers), 0, st));
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
+int cszi_decompress_lorenzo(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
+                            const uint64_t sec_len[4], const cszi_geom *g, int32_t radius,
+                            double eb_abs, int32_t table_mode, float *y, void *workspace,
+                            uint64_t ws_bytes, cszi_ctl *ctl, void *stream) {
+  if (!payload || !sec_len || !g || !ctl || !y) return CSZI_E_INVALID_ARG;
+  std::string k("M");
+  for (const void *q : {(const void *)payload, (const void *)y, (const void *)workspace,
+                        (const void *)ctl})
+    key_add(k, q);
+  key_add(k, payload_len);
+  key_add(k, pass2);
+  k.append(reinterpret_cast<const char *>(sec_len), 4 * sizeof(uint64_t));
+  key_add(k, *g);
+  key_add(k, radius);
+  key_add(k, eb_abs);
+  key_add(k, table_mode);
+  key_add(k, ws_bytes);
+  return run_graphed(std::move(k), reinterpret_cast<cudaStream_t>(stream), [&](cudaStream_t st) {
+    return lz_decompress_body(payload, payload_len, pass2, sec_len, g, radius, eb_abs, table_mode,
+                              y, workspace, ws_bytes, ctl, st);
+  });
+}
+
+// lorenzo_predict_quantize (lorenzo.py:22-33): x -> symbols (q + R, 0 for an
+// outlier); rec: float[n] scratch
+int cszi_lorenzo_predict(const float *x, const cszi_geom *g, double eb_abs, int32_t radius,
+                         uint16_t *sym, float *rec, cszi_ctl *ctl, void *stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CK(check_geom(g, radius));
+  CK(launch_ctl_init(ctl, st));
+  CK(launch_lorenzo_eb(ctl, eb_abs, 0, radius, st));
+  return launch_lorenzo(0, x, rec, sym, g, ctl, 0.0, radius, nullptr, nullptr, nullptr, 0, st);
+}
+
+// lorenzo_reconstruct (lorenzo.py:36-53): symbols (0xFFFF at outliers) -> y
+int cszi_lorenzo_reconstruct(const uint16_t *sym, const uint64_t *out_idx, const float *out_val,
+                             uint64_t n_out, const cszi_geom *g, double eb_abs, int32_t radius,
+                             float *y, void *stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (!g || !sym || !y) return CSZI_E_INVALID_ARG;
+  if (radius < 1 || radius > 32767) return CSZI_E_INVALID_ARG;
+  return launch_lorenzo(1, nullptr, y, const_cast<uint16_t *>(sym), g, nullptr,
+                        dmul_host(2.0, eb_abs), radius, reinterpret_cast<const u64 *>(out_idx),
+                        out_val, nullptr, n_out, st);
 }
 
 int cszi_ctl_fetch(const cszi_ctl *ctl, cszi_ctl *host, void *stream) {

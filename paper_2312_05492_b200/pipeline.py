@@ -156,10 +156,7 @@ def compress_device(grid: Grid, eb: float, mode: str = "rel", predictor: str = "
         raise ValueError("error bound must be positive")
     thread_count(threads)
     if predictor == "lorenzo":
-        raise NotImplementedError(
-            "predictor='lorenzo' (the reference's sequential baseline) is out of scope of the "
-            "B200 path; see DESIGN.md"
-        )
+        return _compress_lorenzo(grid, eb, mode, pass2, pass2_codec, quant_radius)
     if predictor != "interp":
         raise ValueError(f"unknown predictor {predictor!r}")
     rank = grid.dims.rank
@@ -251,6 +248,66 @@ def compress_device(grid: Grid, eb: float, mode: str = "rel", predictor: str = "
     return DeviceArchive(header=header, payload=payload)
 
 
+def _compress_lorenzo(grid: Grid, eb: float, mode: str, pass2: bool, pass2_codec: int,
+                      quant_radius: int) -> DeviceArchive:
+    """pipeline.py:123-150: value_range -> eb_abs -> the Lorenzo recurrence
+    -> sections (no anchors) -> pass-2, one libcszi call on the GPU."""
+    R = int(quant_radius)
+    if R < 2:
+        raise Inconsistent("quantizer radius must be at least 2")
+    if 2 * R > _MAX_BINS:
+        raise NotImplementedError(f"quant_radius {R} exceeds the GPU codebook limit")
+    codec_enc = None
+    if pass2 and pass2_codec != DEFAULT_CODEC:
+        codec_enc = lookup(pass2_codec)[0]
+    _lib.require_cuda()
+    lib = _lib.load()
+    st = _lib.stream_ptr()
+    x = grid.tensor
+    n = grid.dims.count
+    rank = grid.dims.rank
+    geom = make_geom(grid.dims.extents, default_layout(rank))
+    ctl = _lib.DeviceCtl()
+    dev_pass2 = 1 if (pass2 and codec_enc is None) else 0
+    worst = _caps_hint.get(("lz", n), False)
+    while True:
+        caps = _caps_for(n, worst)
+        ws = _lib.WS.get(int(lib.cszi_compress_lorenzo_workspace_size(ctypes.byref(geom), R,
+                                                                      ctypes.byref(caps))),
+                         "compress_lz")
+        pay = _payload_buf(int(lib.cszi_payload_capacity(ctypes.byref(geom), R,
+                                                         ctypes.byref(caps))))
+        _lib.check(lib.cszi_compress_lorenzo(_lib.ptr(x), ctypes.byref(geom),
+                                             1 if mode == "rel" else 0, float(eb), R,
+                                             ctypes.byref(caps), dev_pass2, _lib.ptr(pay),
+                                             _lib.ptr(ws), ws.numel(), ctl.ptr, st),
+                   "compress_lorenzo")
+        c = ctl.fetch()
+        if c.flags & _lib.F_CAPACITY and not worst:
+            worst = True
+            _caps_hint[("lz", n)] = True
+            continue
+        break
+    if c.flags & _lib.F_NONFINITE:
+        raise NonFiniteValue(int(c.first_nonfinite))
+    grid._mark_finite()
+    if c.flags & _lib.F_EMPTY_HISTOGRAM:
+        raise EmptyHistogram("cannot build a codebook from all-zero counts")
+    if c.flags & _lib.F_LENGTH_OVERFLOW:
+        raise LengthOverflow("a symbol would need more than 32 bits")
+    if c.flags & _lib.F_CAPACITY:
+        raise RuntimeError("compress: output capacity exceeded at worst-case sizing")
+    sec = (0, 2 * R, (int(c.bits) + 7) // 8, 8 + 12 * int(c.n_outliers))
+    payload = pay[: int(c.payload_len)]
+    if codec_enc is not None:
+        payload = bytes(codec_enc(payload.cpu().numpy().tobytes()))
+    plen = len(payload) if isinstance(payload, bytes) else payload.numel()
+    header = pack_header(rank, PREDICTOR_LORENZO, _MODE_IDS[mode], bool(pass2), int(pass2_codec),
+                         (0,) * rank, tuple(range(rank)), R, 0, grid.dims.extents, float(eb),
+                         float(c.eb_abs), 1.0, sec, plen)
+    return DeviceArchive(header=header, payload=payload)
+
+
 def compress(grid: Grid, eb: float, mode: str = "rel", predictor: str = "interp",
              pass2: bool = True, pass2_codec: int = DEFAULT_CODEC, alpha: float = None,
              variants=None, dim_order=None, quant_radius: int = 512,
@@ -290,8 +347,6 @@ def _split_input(data):
 def _host_checks(h, dims: Dims):
     """Checks the reference performs on the host side, in its order, returning
     the first failure (exception instance) or None plus the layout."""
-    if h.predictor == PREDICTOR_LORENZO:
-        return NotImplementedError("Lorenzo archives are out of scope of the B200 path"), None
     if h.predictor != PREDICTOR_INTERP:
         return Corrupt(f"unknown predictor id {h.predictor}"), None
     try:
@@ -395,6 +450,10 @@ def decompress_device(data, threads: int = None, slab=None):
         raise LengthMismatch(f"sections total {d_payload.numel()} bytes, header says {raw_len}")
     dims = Dims(h.extents)
     n = dims.count
+    if h.predictor == PREDICTOR_LORENZO:
+        if slab is not None:
+            raise NotImplementedError("slab decompress needs an interp archive")
+        return _decompress_lorenzo(h, d_payload, dev_pass2, dims)
     host_err, layout = _host_checks(h, dims)
     if host_err is None and h.sec_lens[1] != 2 * h.quant_radius:
         host_err = MalformedSection(
@@ -443,6 +502,41 @@ def decompress_device(data, threads: int = None, slab=None):
         raise IndexError("outlier index out of bounds for the grid")
     if slab is not None:
         return y.view(slab[1] - slab[0], h.extents[1], h.extents[2])
+    return Grid.wrap_device(dims, y)
+
+
+def _decompress_lorenzo(h, d_payload, dev_pass2: bool, dims: Dims) -> Grid:
+    """pipeline.py:172-179, 202-203: codebook, Huffman decode, outliers, then
+    the Lorenzo replay (lorenzo.py:36-53) on the GPU."""
+    lib = _lib.load()
+    t = _lib.torch()
+    n = dims.count
+    if h.sec_lens[1] != 2 * h.quant_radius:
+        raise MalformedSection(
+            f"codebook holds {h.sec_lens[1]} lengths for radius {h.quant_radius}")
+    if h.quant_radius < 2 or 2 * h.quant_radius > _MAX_BINS:
+        raise NotImplementedError(f"quant_radius {h.quant_radius} is not supported on the GPU")
+    geom = make_geom(h.extents, default_layout(h.rank))
+    sec = (ctypes.c_uint64 * 4)(*h.sec_lens)
+    R = h.quant_radius
+    y = t.empty(n, dtype=t.float32, device="cuda")
+    ctl = _lib.DeviceCtl()
+    st = _lib.stream_ptr()
+    plen = d_payload.numel()
+    ws = _lib.WS.get(int(lib.cszi_decompress_workspace_size(ctypes.byref(geom), R, sec, plen)),
+                     "decompress")
+    for table_mode in (0, 1):
+        _lib.check(lib.cszi_decompress_lorenzo(_lib.ptr(d_payload), plen, 1 if dev_pass2 else 0,
+                                               sec, ctypes.byref(geom), R, float(h.eb_abs),
+                                               table_mode, _lib.ptr(y), _lib.ptr(ws), ws.numel(),
+                                               ctl.ptr, st), "decompress_lorenzo")
+        c = ctl.fetch()
+        if table_mode == 0 and c.scratch[1] != 0:
+            continue
+        break
+    _raise_device_flags(c, n)
+    if c.flags & _lib.F_OUTLIER_INDEX:
+        raise IndexError("outlier index out of bounds for the grid")
     return Grid.wrap_device(dims, y)
 
 

@@ -3,8 +3,7 @@ package through the ``ebcomp`` import alias (tests/refsuite/ebcomp_alias.py).
 
 The suite is staged (not committed) into baseline/_ref/ref_tests by
 __graft_entry__.build() in the build container; the test skips when the
-staged copy is absent.  Excluded: test_cli.py (the CLI is out of scope) and
-test_lorenzo.py (the Lorenzo predictor)."""
+staged copy is absent.  Excluded: test_cli.py (the CLI is out of scope)."""
 import os
 import subprocess
 import sys
@@ -13,7 +12,7 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 STAGED = os.path.join(ROOT, "baseline", "_ref", "ref_tests")
-EXCLUDE = ("test_cli.py", "test_lorenzo.py")
+EXCLUDE = ("test_cli.py",)
 
 
 @pytest.mark.gpu
