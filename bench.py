@@ -18,6 +18,13 @@ gather to rank 0); the step time is the max over ranks.  --sharded forces
 that path at N = 1 (a 1-rank process group).
 --impl reference times the reference algorithm's CPU implementation (the
 oracle port in oracle/, C + OpenMP on all host cores) on the same workload.
+
+Extra legs in the same JSON line (--no-extra skips them): `eb_0.0001` (the
+512^3 field at the second bound BASELINE names, oracle-checked) and `rtm8`
+(BASELINE configs[3]: 449x449x235 x 8 snapshots, z-slab sharded over the N
+GPUs with one collective per stage for the whole batch).  `roofline` is the
+dominant kernel's; `roofline_step` the whole compress / decompress step's
+against SURVEY §8(d)'s algorithmic bytes.
 """
 
 from __future__ import annotations
@@ -49,6 +56,8 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sharded", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the rel-1e-4 and RTM x 8 legs")
+    ap.add_argument("--eb2", type=float, default=1e-4)
     return ap.parse_args()
 
 
@@ -209,6 +218,45 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def workload_config(shape, eb, world):
+    """The `config` of BOTH arms (identical dicts: same workload)."""
+    nbytes = 4 * math.prod(shape)
+    return {
+        "workload": f"Nyx-shaped {shape[0]}x{shape[1]}x{shape[2]} float32 smooth field "
+                    f"(SURVEY §8d), REL eb {eb:g}, reference defaults (interp predictor, pass-2 "
+                    "codec 0, R=512), one complete archive per step",
+        "shape": list(shape),
+        "eb": eb,
+        "mode": "rel",
+        "per_gpu_input_bytes": nbytes,
+        "l2": "input 537 MB > 126 MB L2 per step; no flush needed",
+        "parallelism": f"replicas x{world} (one field per GPU)" if world == 1
+                       else f"z-slab x{world}",
+    }
+
+
+def step_bytes_per_elem(n, bits, raw_len, payload_len):
+    """SURVEY §8(d) algorithmic bytes per element of a whole step.
+    compress: range 4 + predict (4 + 2) + encode (2 + b/8) + pass-2 (P + P2);
+    decompress: pass-2 (P2 + P) + Huffman decode (b/8 + 2) + inverse
+    interpolation (2 + 4)."""
+    b8 = bits / 8.0 / n
+    P_ = raw_len / n
+    P2 = payload_len / n
+    return 12.0 + b8 + P_ + P2, 8.0 + b8 + P_ + P2
+
+
 def oracle_compress_gbs(data_np, eb, min_seconds=10.0, max_reps=3):
     """Oracle port (C + OpenMP, all host cores) compress throughput."""
     from oracle import oracle as O
@@ -338,6 +386,13 @@ def run_ours(args, rank, world, local):
         except Exception:
             traffic = None
 
+    # ---- step-level roofline (SURVEY §8(d) bytes of the whole step) ----
+    hdr = P.archive.unpack_header(arch.header, len(arch))
+    raw_len = sum(hdr.sec_lens)
+    cb, db = step_bytes_per_elem(n, 8 * hdr.sec_lens[2], raw_len, len(arch) - P.HEADER_SIZE)
+    c_ach = cb * n / (c_ms * 1e-3) / 1e9
+    d_ach = db * n / (d_ms * 1e-3) / 1e9
+
     result = {
         "metric": METRIC,
         "value": round(world * nbytes / (c_ms * 1e-3) / 1e9, 3),
@@ -351,18 +406,9 @@ def run_ours(args, rank, world, local):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": {
-            "workload": f"Nyx-shaped {shape[0]}x{shape[1]}x{shape[2]} float32 smooth field "
-                        f"(SURVEY §8d), REL eb {eb:g}, defaults (interp, pass2, R=512); step = "
-                        "Grid(device tensor) [range+finite scan] + compress to a full archive "
-                        "in HBM",
-            "shape": list(shape),
-            "eb": eb,
-            "mode": "rel",
-            "per_gpu_input_bytes": nbytes,
-            "l2": "input 537 MB > 126 MB L2 per step; no flush needed",
-            "parallelism": f"replicas x{world} (one field per GPU)",
-        },
+        "config": workload_config(shape, eb, world),
+        "step": "Grid(device tensor) + compress_device to a complete archive in HBM (range / "
+                "finite scan inside); decompress_device for the decompress leg",
         "decompress_gbs": round(world * nbytes / (d_ms * 1e-3) / 1e9, 3),
         "decompress_ms_per_step": round(d_ms, 4),
         "cr": round(nbytes / blob_len, 4),
@@ -383,6 +429,16 @@ def run_ours(args, rank, world, local):
             "kernel_ms": round(k_ms, 4),
             "algorithmic_bytes_per_launch": k_bytes,
             "share_of_step": round(k_ms / c_ms, 4),
+        },
+        "roofline_step": {
+            "bound": "hbm", "unit": "GB/s", "peak": peak, "peak_kind": peak_kind,
+            "bytes_per_elem_def": "SURVEY §8(d): compress 12 + b/8 + P + P2, decompress "
+                                  "8 + b/8 + P + P2 (b bits/value, P / P2 pre / post pass-2 "
+                                  "payload bytes per value)",
+            "compress": {"bytes_per_elem": round(cb, 4), "achieved": round(c_ach, 2),
+                         "frac": round(c_ach / peak, 4)},
+            "decompress": {"bytes_per_elem": round(db, 4), "achieved": round(d_ach, 2),
+                           "frac": round(d_ach / peak, 4)},
         },
         "gpu_launches": int(launches),
         "clocks": clk,
@@ -424,18 +480,165 @@ def run_ours(args, rank, world, local):
                                     "d2h_bytes_per_step": nbytes, "ms_per_step": round(ed_ms, 3)}
         result["archive_sha256"] = hashlib.sha256(blob).hexdigest()[:16]
 
+    # ---- the second bound BASELINE names for 512^3 (rel 1e-4) ----
+    if not args.no_extra:
+        result[f"eb_{args.eb2:g}"] = second_bound_leg(args, P, x, dims, nbytes, peak, world)
+        result["rtm8"] = rtm8_leg(args, P, rank, world)
+
     # ---- CPU baseline: oracle port on the host cores (rank 0, N=1 only) ----
     if rank == 0 and world == 1 and not args.no_cpu:
         data_np = x.cpu().numpy()
         gbs, oblob, reps = oracle_compress_gbs(data_np, eb)
         result["cpu_baseline"] = {
             "value": round(gbs, 4), "unit": "GB/s", "cores": cpu_cores(), "kind": "port",
+            "cpu_model": cpu_model(),
             "sample": f"full {shape[0]}x{shape[1]}x{shape[2]} field, {reps} compress run(s) of "
                       "oracle/ (C+OpenMP restatement of ebcomp)",
         }
         if not args.no_e2e:
             result["parity_vs_oracle"] = bool(oblob == blob)
     return result
+
+
+def events_ms(fn, steps, world):
+    """CUDA-event time per call of fn over `steps` calls (barrier + sync on
+    both sides), max over ranks."""
+    import torch
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    ev0.record()
+    for _ in range(steps):
+        out = fn()
+    ev1.record()
+    torch.cuda.synchronize()
+    barrier(world)
+    return max_over_ranks(ev0.elapsed_time(ev1) / steps, world), out
+
+
+def second_bound_leg(args, P, x, dims, nbytes, peak, world):
+    """512^3 at the second bound BASELINE.json names (rel 1e-4): the same
+    compress / decompress steps, bit-exact check against the oracle."""
+    import torch
+
+    eb = args.eb2
+    steps = max(5, args.steps // 2)
+    for _ in range(max(args.warmup, 1)):
+        arch = P.compress_device(P.Grid(dims, x), eb)
+        yg = P.decompress_device(arch)
+    c_ms, arch = events_ms(lambda: P.compress_device(P.Grid(dims, x), eb), steps, world)
+    d_ms, yg = events_ms(lambda: P.decompress_device(arch), steps, world)
+    n = x.numel()
+    hdr = P.archive.unpack_header(arch.header, len(arch))
+    diff = (x.double() - yg.tensor.double()).abs()
+    mse = float((diff * diff).mean().item())
+    rng = float(x.max().item()) - float(x.min().item())
+    cb, db = step_bytes_per_elem(n, 8 * hdr.sec_lens[2], sum(hdr.sec_lens), len(arch) - P.HEADER_SIZE)
+    out = {
+        "eb": eb, "steps": steps,
+        "compress_gbs": round(world * nbytes / (c_ms * 1e-3) / 1e9, 3),
+        "compress_ms_per_step": round(c_ms, 4),
+        "decompress_gbs": round(world * nbytes / (d_ms * 1e-3) / 1e9, 3),
+        "decompress_ms_per_step": round(d_ms, 4),
+        "roofline_step_frac": {"compress": round(cb * n / (c_ms * 1e-3) / 1e9 / peak, 4),
+                               "decompress": round(db * n / (d_ms * 1e-3) / 1e9 / peak, 4)},
+        "cr": round(nbytes / len(arch), 4),
+        "psnr": round(10.0 * math.log10(rng * rng / mse), 4) if mse > 0 else None,
+        "bound_ok": bool(float(diff.max().item()) <= hdr.eb_abs),
+        "n_outliers": (hdr.sec_lens[3] - 8) // 12,
+    }
+    blob = arch.to_bytes()
+    out["archive_sha256"] = hashlib.sha256(blob).hexdigest()[:16]
+    if not args.no_cpu and world == 1:
+        from oracle import oracle as O
+
+        out["parity_vs_oracle"] = bool(O.compress(x.cpu().numpy(), eb, threads=cpu_cores())
+                                       == blob)
+    return out
+
+
+RTM_SHAPE = (449, 449, 235)
+
+
+def rtm8_leg(args, P, rank, world):
+    """BASELINE configs[3]: RTM-shaped 449x449x235 x 8 snapshots (phase 2 pi k
+    / 8), z-slab sharded over the N GPUs with ONE collective per
+    stage for the whole batch (one 8 x 2R histogram all-reduce); strong
+    scaling (the 8 snapshots are the fixed total work).  Decompress: every
+    rank decodes its slabs of the 8 archives."""
+    import torch
+
+    from paper_2312_05492_b200.distributed import (SimComm, compress_sharded_batch,
+                                                   decompress_slab, slab_bounds)
+
+    shape = RTM_SHAPE
+    nz = shape[0]
+    z0, z1 = slab_bounds(nz, world)[rank]
+    xs = [smooth_field_gpu(shape, phase=2 * math.pi * k / 8, zrange=(z0, min(z1 + 1, nz)))
+          for k in range(8)]
+    comm = SimComm(1) if world == 1 else None
+    steps = max(5, args.steps // 5)
+
+    def cstep():
+        return compress_sharded_batch(xs, shape, z0, z1, args.eb, comm=comm)
+
+    for _ in range(max(args.warmup, 1)):
+        archs = cstep()
+    c_ms, archs = events_ms(cstep, steps, world)
+    # decompress: rank 0's archives are broadcast inside the step
+    import torch.distributed as dist
+
+    from paper_2312_05492_b200.pipeline import DeviceArchive
+
+    dist_on = dist.is_available() and dist.is_initialized()
+    if dist_on:
+        meta = torch.zeros(8, dtype=torch.int64, device="cuda")
+        hdrs = torch.empty(8, 112, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            for k, a in enumerate(archs):
+                meta[k] = a.payload.numel()
+                hdrs[k] = torch.frombuffer(bytearray(a.header), dtype=torch.uint8).cuda()
+        dist.broadcast(meta, 0)
+        dist.broadcast(hdrs, 0)
+        heads = [bytes(hdrs[k].cpu().numpy().tobytes()) for k in range(8)]
+        pays = [archs[k].payload if rank == 0 else
+                torch.empty(int(meta[k].item()), dtype=torch.uint8, device="cuda")
+                for k in range(8)]
+    else:
+        heads = [a.header for a in archs]
+        pays = [a.payload for a in archs]
+
+    def dstep():
+        if dist_on:
+            for p_ in pays:
+                dist.broadcast(p_, 0)
+        return [decompress_slab(DeviceArchive(header=h, payload=p_), z0, z1)
+                for h, p_ in zip(heads, pays)] if z1 > z0 else []
+
+    for _ in range(max(args.warmup, 1)):
+        ys = dstep()
+    d_ms, ys = events_ms(dstep, steps, world)
+    total = 8 * 4 * math.prod(shape)
+    out = {
+        "config": f"{shape[0]}x{shape[1]}x{shape[2]} float32 x 8 snapshots (phase 2 pi k/8), REL "
+                  f"eb {args.eb:g}, z-slab x{world}, one collective per stage for the batch",
+        "scaling": "strong", "steps": steps,
+        "compress_gbs": round(total / (c_ms * 1e-3) / 1e9, 3),
+        "compress_ms_per_step": round(c_ms, 4),
+        "decompress_gbs": round(total / (d_ms * 1e-3) / 1e9, 3),
+        "decompress_ms_per_step": round(d_ms, 4),
+    }
+    if rank == 0 and archs is not None:
+        out["cr"] = round(total / sum(len(a) for a in archs), 4)
+        if world == 1:
+            # the batch archives are the single-GPU compress archives
+            ref = [P.compress_device(P.Grid(P.Dims(shape), xk), args.eb).to_bytes() for xk in xs]
+            out["batch_equals_single_gpu"] = [a.to_bytes() for a in archs] == ref
+            s_ms, _ = events_ms(lambda: [P.compress_device(P.Grid(P.Dims(shape), xk), args.eb)
+                                         for xk in xs], steps, world)
+            out["single_gpu_api_compress_gbs"] = round(total / (s_ms * 1e-3) / 1e9, 3)
+    return out
 
 
 def run_sharded(args, rank, world, local):
@@ -545,6 +748,10 @@ def run_sharded(args, rank, world, local):
     }
     if rank == 0 and arch is not None:
         res["cr"] = round(total_bytes / len(arch), 4)
+    if not args.no_extra:
+        import paper_2312_05492_b200 as P
+
+        res["rtm8"] = rtm8_leg(args, P, rank, world)
     return res
 
 
@@ -573,9 +780,12 @@ def run_reference(args, rank, world):
         blob = O.compress(data, args.eb, threads=cores)
         times.append(time.perf_counter() - t0)
     c_s = sum(times) / len(times)
-    t0 = time.perf_counter()
-    back = O.decompress(blob, threads=cores)
-    d_s = time.perf_counter() - t0
+    dtimes = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        back = O.decompress(blob, threads=cores)
+        dtimes.append(time.perf_counter() - t0)
+    d_s = sum(dtimes) / len(dtimes)
     value = nbytes / c_s / 1e9
     return {
         "impl": "reference",
@@ -591,14 +801,14 @@ def run_reference(args, rank, world):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": {
-            "workload": f"Nyx-shaped {shape[0]}x{shape[1]}x{shape[2]} float32 smooth field "
-                        f"(SURVEY §8d), REL eb {args.eb:g}, defaults; CPU reference algorithm",
-            "shape": list(shape), "eb": args.eb, "mode": "rel",
-        },
+        "config": workload_config(shape, args.eb, 1),
+        "step": "oracle/ compress (C + OpenMP restatement of the reference algorithm) of the "
+                "host field to archive bytes; decompress leg likewise",
         "decompress_gbs": round(nbytes / d_s / 1e9, 4),
+        "decompress_ms_per_step": round(d_s * 1e3, 3),
         "cr": round(nbytes / len(blob), 4),
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": f"full field, {args.steps} timed compress runs of oracle/ "
                                    "(C+OpenMP restatement of ebcomp; the Python reference "
                                    "cannot travel to the GPU box)"},

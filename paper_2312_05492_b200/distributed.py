@@ -363,60 +363,104 @@ def compress_slabs(states: list, comm, backend=None, pass2: bool = True):
     """Run the sharded compress over this process's slabs.  Returns the
     archive (backend.assemble) on the root (the first slab's process), else
     None."""
-    backend = backend or GpuSlabBackend()
-    s0 = states[0]
-    # (1) range
-    keys = [backend.range_keys(s) for s in states]
-    comm.allreduce(keys, "min")
-    for s, k in zip(states, keys):
-        backend.set_range(s, k)
-    k0 = keys[0].cpu().numpy().astype(np.int64)
-    if int(k0[2]) != INT64_MAX:
-        raise NonFiniteValue(int(k0[2]))
-    # alpha: rel mode -> compute_alpha(eb); abs mode -> from the global range
-    if s0.mode == "rel":
-        alpha = compute_alpha(float(s0.eb))
-    else:
-        from ._keys import key_to_float
+    out = compress_slabs_batch([states], comm, backend, pass2)
+    return None if out is None else out[0]
 
-        rng = key_to_float(int(-k0[1])) - key_to_float(int(k0[0]))
-        alpha = compute_alpha(float(s0.eb) / rng if rng > 0 else float(s0.eb))
+
+def _batched(comm, per_snap, op, split_sizes=None):
+    """One collective for a batch of snapshots: per_snap[k][i] is local slab
+    i's tensor for snapshot k.  The snapshot tensors of each slab are
+    concatenated, reduced / gathered once, and split back."""
+    t = _lib.torch()
+    K = len(per_snap)
+    sizes = [x.numel() for x in per_snap[0]] if split_sizes is None else split_sizes
+    cat = [t.cat([per_snap[k][i].reshape(-1) for k in range(K)]) for i in range(len(per_snap[0]))]
+    if op == "gather":
+        res = comm.allgather(cat)[0]  # list over ranks
+        n = sizes[0]
+        return [[r[k * n:(k + 1) * n] for r in res] for k in range(K)]
+    comm.allreduce(cat, op)
+    return [[c[k * sizes[i]:(k + 1) * sizes[i]] for i, c in enumerate(cat)] for k in range(K)]
+
+
+def compress_slabs_batch(batch: list, comm, backend=None, pass2: bool = True):
+    """Sharded compress of a batch of snapshots with one collective per stage
+    for the whole batch (SURVEY §8e "Expected scaling": one K x 2R histogram
+    all-reduce instead of K).  batch[k] is the list of this process's slab
+    states of snapshot k (same slab layout for every snapshot).  Returns the
+    list of K archives on the root, else None."""
+    backend = backend or GpuSlabBackend()
+    K = len(batch)
+    # (1) range: K x 3 keys in one all-reduce
+    keys = _batched(comm, [[backend.range_keys(s) for s in states] for states in batch], "min")
+    for states, ks in zip(batch, keys):
+        for s, k in zip(states, ks):
+            backend.set_range(s, k)
+    kall = [ks[0].cpu().numpy().astype(np.int64) for ks in keys]
+    for k0 in kall:
+        if int(k0[2]) != INT64_MAX:
+            raise NonFiniteValue(int(k0[2]))
+    alphas = []
+    for states, k0 in zip(batch, kall):
+        s0 = states[0]
+        # alpha: rel mode -> compute_alpha(eb); abs mode -> from the global range
+        if s0.mode == "rel":
+            alphas.append(compute_alpha(float(s0.eb)))
+        else:
+            from ._keys import key_to_float
+
+            rng = key_to_float(int(-k0[1])) - key_to_float(int(k0[0]))
+            alphas.append(compute_alpha(float(s0.eb) / rng if rng > 0 else float(s0.eb)))
     # (2) tuner samples
-    samp = [backend.samples(s) for s in states]
-    comm.allreduce(samp, "sum")
-    for s, v in zip(states, samp):
-        backend.tune(s, v, alpha)
-    # (3) histogram -> shared codebook
-    hists = [backend.predict(s) for s in states]
+    samp = _batched(comm, [[backend.samples(s) for s in states] for states in batch], "sum")
+    for states, vs, a in zip(batch, samp, alphas):
+        for s, v in zip(states, vs):
+            backend.tune(s, v, a)
+    # (3) histograms -> shared codebooks: one K x 2R all-reduce
+    hists = [[backend.predict(s) for s in states] for states in batch]
     phased = hasattr(backend, "piece_bits")
-    local_h = [h.clone() for h in hists] if phased else None
-    comm.allreduce(hists, "sum")
-    for s, h in zip(states, hists):
-        backend.codebook(s, h)
+    local_h = [[h.clone() for h in hs] for hs in hists] if phased else None
+    hists = _batched(comm, hists, "sum")
+    for states, hs in zip(batch, hists):
+        for s, h in zip(states, hs):
+            backend.codebook(s, h)
+    ranks = _local_ranks(comm, batch[0])
     # (4) bit / outlier counts.  A phase-packing backend first exchanges each
     # slab's stream length (local histogram . code lengths, known before any
     # packing) so every slab packs at its global bit phase and the root
     # merges whole words instead of bit-shifting the pieces.
     if phased:
-        pb = [backend.piece_bits(s, h) for s, h in zip(states, local_h)]
-        allpb = [int(v.reshape(-1)[0].item()) for v in comm.allgather(pb)[0]]
-        starts = [sum(allpb[:r]) for r in range(len(allpb))]
-        counts = [backend.encode(s, bit_base=starts[r] % 32)
-                  for s, r in zip(states, _local_ranks(comm, states))]
+        pb = _batched(comm, [[backend.piece_bits(s, h) for s, h in zip(states, lh)]
+                             for states, lh in zip(batch, local_h)], "gather")
+        counts = []
+        for states, pbk in zip(batch, pb):
+            allpb = [int(v) for v in t_cat_host(pbk)]
+            starts = [sum(allpb[:r]) for r in range(len(allpb))]
+            counts.append([backend.encode(s, bit_base=starts[r] % 32)
+                           for s, r in zip(states, ranks)])
     else:
-        counts = [backend.encode(s) for s in states]
-    allc = comm.allgather(counts)[0]
-    allc = [c.cpu().numpy() for c in allc]
+        counts = [[backend.encode(s) for s in states] for states in batch]
+    allc = _batched(comm, counts, "gather")
+    allc = [[c.cpu().numpy() for c in ck] for ck in allc]
     # (5) gather pieces to the root
-    anchors = comm.gather([backend.anchors(s) for s in states])
-    pieces = [backend.pieces(s, c) for s, c in zip(states, [allc[i] for i in _local_ranks(comm, states)])]
-    bits = comm.gather([p[0] for p in pieces])
-    oidx = comm.gather([p[1] for p in pieces])
-    oval = comm.gather([p[2] for p in pieces])
-    if anchors is None:
-        return None
-    nbits = [int(c[0]) for c in allc]
-    return backend.assemble(s0, anchors, bits, nbits, oidx, oval, pass2, alpha)
+    out = []
+    for states, ck, a in zip(batch, allc, alphas):
+        anchors = comm.gather([backend.anchors(s) for s in states])
+        pieces = [backend.pieces(s, c) for s, c in zip(states, [ck[i] for i in ranks])]
+        bits = comm.gather([p[0] for p in pieces])
+        oidx = comm.gather([p[1] for p in pieces])
+        oval = comm.gather([p[2] for p in pieces])
+        if anchors is None:
+            out.append(None)
+            continue
+        nbits = [int(c[0]) for c in ck]
+        out.append(backend.assemble(states[0], anchors, bits, nbits, oidx, oval, pass2, a))
+    return None if out[0] is None else out
+
+
+def t_cat_host(parts):
+    t = _lib.torch()
+    return t.cat([p.reshape(-1) for p in parts]).cpu().numpy().tolist()
 
 
 def _local_ranks(comm, states):
@@ -432,6 +476,31 @@ def compress_sharded(local_x, extents, z0: int, z1: int, eb: float, mode: str = 
     st = SlabState(x=local_x.contiguous(), extents=tuple(int(e) for e in extents), z0=z0, z1=z1,
                    eb=float(eb), mode=mode, radius=int(quant_radius))
     return compress_slabs([st], TorchComm(group), pass2=pass2)
+
+
+def compress_sharded_batch(local_xs, extents, z0: int, z1: int, eb: float, mode: str = "rel",
+                           pass2: bool = True, quant_radius: int = 512, group=None, comm=None):
+    """torch.distributed entry point for a batch of snapshots of one shape
+    (e.g. the 8 RTM snapshots): this rank owns planes [z0, z1) of every
+    snapshot; local_xs[k] holds planes [z0, min(z1+1, nz)) of snapshot k.
+    One collective per stage for the whole batch.  -> list of archives on
+    rank 0, None elsewhere."""
+    batch = [[SlabState(x=x.contiguous(), extents=tuple(int(e) for e in extents), z0=z0, z1=z1,
+                        eb=float(eb), mode=mode, radius=int(quant_radius))] for x in local_xs]
+    return compress_slabs_batch(batch, comm if comm is not None else TorchComm(group),
+                                pass2=pass2)
+
+
+def compress_simulated_batch(xs, world: int, eb: float, mode: str = "rel", pass2: bool = True,
+                             quant_radius: int = 512):
+    """compress_sharded_batch with all ``world`` slabs in this process."""
+    batch = []
+    for x in xs:
+        nz = int(x.shape[0])
+        batch.append([SlabState(x=x[z0:min(z1 + 1, nz)].contiguous(), extents=tuple(x.shape),
+                                z0=z0, z1=z1, eb=float(eb), mode=mode, radius=int(quant_radius))
+                      for z0, z1 in slab_bounds(nz, world)])
+    return compress_slabs_batch(batch, SimComm(world), pass2=pass2)
 
 
 def compress_simulated(x, world: int, eb: float, mode: str = "rel", pass2: bool = True,

@@ -72,3 +72,83 @@ def test_phase_packed_pieces_odd_radius():
         ref = O.compress(data, 1e-3, quant_radius=R)
         for world in (2, 3, 5):
             assert compress_simulated(x, world, 1e-3, quant_radius=R).to_bytes() == ref
+
+
+def test_snapshot_batch_is_byte_identical():
+    """A batch of snapshots (RTM x 8 style: the §8d field with a phase per
+    snapshot) compressed with one collective per stage for the whole batch:
+    every archive equals single-GPU compress of that snapshot."""
+    import math
+
+    import torch
+
+    from paper_2312_05492_b200.distributed import compress_simulated_batch
+
+    shape = (45, 33, 40)
+    snaps = [O.smooth_field(shape, phase=2 * math.pi * k / 8) for k in range(8)]
+    refs = [P.compress(P.Grid(P.Dims(shape), d), 1e-3) for d in snaps]
+    xs = [torch.from_numpy(d).cuda() for d in snaps]
+    for world in (1, 2, 3, 6):
+        archs = compress_simulated_batch(xs, world, 1e-3)
+        assert [a.to_bytes() for a in archs] == refs, world
+
+
+def _torchcomm_worker(rank, world, port, data, out_path):
+    """One rank of a real torch.distributed run (gloo process group, both
+    ranks on cuda:0): GpuSlabBackend + TorchComm end to end."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2312_05492_b200.distributed import (compress_sharded, compress_sharded_batch,
+                                                   decompress_sharded, slab_bounds)
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        nz = data.shape[0]
+        z0, z1 = slab_bounds(nz, world)[rank]
+        x = torch.from_numpy(data[z0:min(z1 + 1, nz)].copy()).cuda()
+        arch = compress_sharded(x, data.shape, z0, z1, 1e-3)
+        batch = compress_sharded_batch([x, x * 2.0], data.shape, z0, z1, 1e-3)
+        blob = arch.to_bytes() if rank == 0 else None
+        # every rank decodes its slab of the one archive
+        obj = [blob]
+        dist.broadcast_object_list(obj, src=0)
+        _, _, ys = decompress_sharded(obj[0])
+        parts = [None] * world
+        dist.all_gather_object(parts, ys.cpu().numpy())
+        if rank == 0:
+            np.savez(out_path, blob=np.frombuffer(blob, dtype=np.uint8),
+                     b0=np.frombuffer(batch[0].to_bytes(), dtype=np.uint8),
+                     b1=np.frombuffer(batch[1].to_bytes(), dtype=np.uint8),
+                     dec=np.concatenate(parts, 0))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_torchcomm_gpu_backend_two_processes(tmp_path):
+    """The real combination: two processes, TorchComm over a
+    gloo group, GpuSlabBackend on the GPU -> the single-GPU archive bytes;
+    sharded decompress -> the whole-grid decompression."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    rng = np.random.default_rng(21)
+    data = noisy_field(rng, (40, 24, 64))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = str(tmp_path / "r0.npz")
+    mp.start_processes(_torchcomm_worker, args=(2, port, data, out), nprocs=2, join=True,
+                       start_method="spawn")
+    r = np.load(out)
+    ref = P.compress(P.Grid(P.Dims(data.shape), data), 1e-3)
+    assert r["blob"].tobytes() == ref
+    assert r["b0"].tobytes() == ref
+    assert r["b1"].tobytes() == P.compress(P.Grid(P.Dims(data.shape), data * np.float32(2.0)),
+                                           1e-3)
+    assert r["dec"].tobytes() == P.decompress(ref).data.tobytes()
