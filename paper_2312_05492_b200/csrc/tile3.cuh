@@ -77,7 +77,7 @@ struct Geo {
   int ni[3];         // interior tiles per axis (closing plane inside the grid)
   int R;
   int hist_smem;
-  int tma;           // 1: tensor map valid
+  int tma;           // 1: 3-D tensor map valid, 0: row-wise cp.async / load staging
   int exact;         // 1: force the true-division quantiser (tests)
   int64_t na1, na2;  // anchor lattice counts on axes 1, 2 (decompress)
 };
@@ -116,12 +116,21 @@ DEV void mbar_wait(uint64_t *mb, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-DEV void tma_load3(void *dst, const CUtensorMap *tm, int c0, int c1, int c2, uint64_t *mb) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
-      "{%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(mb))
-      : "memory");
+
+// Stage the closed box of the tile at origin o into dst (one 3-D TMA box of
+// 9 x 9 rows of BX elements) and arm mbar for it.  Called by all lanes.
+template <int BX, int ESZ>
+DEV void tile_load(uint32_t dst, const CUtensorMap *tm, const Geo &G, const int o[3],
+                   uint64_t *mb) {
+  if ((threadIdx.x & 31) == 0) {
+    mbar_expect(mb, (uint32_t)(CZ * CY * BX * ESZ));
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
+        "[%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(o[2]), "r"(o[1]), "r"(o[0] - G.z0),
+        "r"(smem_u32(mb))
+        : "memory");
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -793,30 +802,60 @@ DEV void cp_async4_zfill(uint32_t sdst, const void *gsrc, bool valid) {
                : "memory");
 }
 
-// Manual staging (no tensor map): 4-byte cp.async per element, zero-fill
-// outside the grid / the buffer's planes.  Same smem layout as the TMA box.
-DEV void stage_manual_f32(uint32_t buf, const float *x, const Geo &G, const int o[3]) {
+// Manual staging (no tensor map: the row pitch is not a multiple of 16
+// bytes, so neither a 3-D box nor a 16-byte copy can describe a tile row;
+// TMA also needs 128-byte aligned destinations, which per-row boxes of the
+// pitch-36 layout are not).  Row by row, lane l copies x = l (and 32 + l for
+// the closing columns), zero-filling outside the grid / the held planes;
+// same smem layout as the TMA box.  The float copy is asynchronous
+// (cp.async groups): it is issued for the next tile right after the passes
+// and waited for at the next tile's start, like the TMA prefetch.
+DEV void stage_rows_f32_issue(uint32_t buf, const float *x, const Geo &G, const int o[3]) {
   const int lane = threadIdx.x & 31;
   const int zl0 = o[0] - G.z0;
-  for (int i = lane; i < NBUF; i += 32) {
-    const int row = i / PX, xx = i - row * PX;
-    const int z = row / CY, y = row - z * CY;
-    const int gz = zl0 + z, gy = o[1] + y, gx = o[2] + xx;
-    const bool v = gz < G.nzl && gy < G.ext[1] && gx < G.ext[2];
-    const float *src = v ? x + ((int64_t)gz * G.ext[1] + gy) * G.ext[2] + gx : x;
-    cp_async4_zfill(buf + 4u * i, src, v);
+  const int64_t nx = G.ext[2], ny = G.ext[1];
+  const bool vx0 = o[2] + lane < nx, vx1 = lane < PX - 32 && o[2] + 32 + lane < nx;
+  const float *p = x + ((int64_t)zl0 * ny + o[1]) * nx + o[2] + lane;
+  for (int z = 0; z < CZ; ++z) {
+    const bool vz = zl0 + z < G.nzl;
+    for (int y = 0; y < CY; ++y) {
+      const bool v = vz && o[1] + y < ny;
+      const uint32_t d = buf + 4u * (uint32_t)((z * CY + y) * PX + lane);
+      cp_async4_zfill(d, v && vx0 ? p : x, v && vx0);
+      if (lane < PX - 32) cp_async4_zfill(d + 128u, v && vx1 ? p + 32 : x, v && vx1);
+      p += nx;
+    }
+    p += (ny - CY) * nx;
   }
-  asm volatile("cp.async.wait_all;" ::: "memory");
+  asm volatile("cp.async.commit_group;" ::: "memory");
 }
-DEV void stage_manual_u16(uint32_t dst, const uint16_t *sym, const Geo &G, const int o[3]) {
+DEV void stage_rows_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// symbols (2-byte elements: no 2-byte cp.async): plain loads, one z-plane
+// (9 rows) in flight per batch, then the stores
+DEV void stage_rows_u16(uint32_t dst, const uint16_t *sym, const Geo &G, const int o[3]) {
   const int lane = threadIdx.x & 31;
   const int zl0 = o[0] - G.z0;
-  for (int i = lane; i < NSYM; i += 32) {
-    const int row = i / SP, xx = i - row * SP;
-    const int z = row / CY, y = row - z * CY;
-    const int gz = zl0 + z, gy = o[1] + y, gx = o[2] + xx;
-    const bool v = gz < G.nzl && gy < G.ext[1] && gx < G.ext[2];
-    sts_u16(dst + 2u * i, v ? __ldg(sym + ((int64_t)gz * G.ext[1] + gy) * G.ext[2] + gx) : 0u);
+  const int64_t nx = G.ext[2], ny = G.ext[1];
+  const bool vx0 = o[2] + lane < nx, vx1 = lane < SP - 32 && o[2] + 32 + lane < nx;
+  const uint16_t *p = sym + ((int64_t)zl0 * ny + o[1]) * nx + o[2] + lane;
+  for (int z = 0; z < CZ; ++z) {
+    const bool vz = zl0 + z < G.nzl;
+    uint32_t a[CY], b[CY];
+#pragma unroll
+    for (int y = 0; y < CY; ++y) {
+      const bool v = vz && o[1] + y < ny;
+      const uint16_t *q = p + (int64_t)y * nx;
+      a[y] = (v && vx0) ? __ldg(q) : 0u;
+      b[y] = (v && vx1) ? __ldg(q + 32) : 0u;
+    }
+#pragma unroll
+    for (int y = 0; y < CY; ++y) {
+      const uint32_t d = dst + 2u * (uint32_t)((z * CY + y) * SP + lane);
+      sts_u16(d, a[y]);
+      if (lane < SP - 32) sts_u16(d + 64u, b[y]);
+    }
+    p += ny * nx;
   }
 }
 
@@ -876,14 +915,13 @@ __global__ void __launch_bounds__(NT, 3)
   const int ntiles = nint + tile_count<true>(G);
   unsigned int *q = g_t3_sched + 2 * slot;
   int t = next_tile(q);
-  if (lane == 0) {
-    mbar_init(&mbar[warp]);
-    if (t < ntiles && G.tma) {
-      int o[3];
-      tile_of(G, nint, t, o);
-      mbar_expect(&mbar[warp], (uint32_t)BUF_BYTES);
-      tma_load3(sm + warp * P_WARP, &tm, o[2], o[1], o[0] - G.z0, &mbar[warp]);
-    }
+  if (lane == 0) mbar_init(&mbar[warp]);
+  __syncwarp();
+  if (t < ntiles) {
+    int o[3];
+    tile_of(G, nint, t, o);
+    if (G.tma) tile_load<PX, 4>(buf, &tm, G, o, &mbar[warp]);
+    else stage_rows_f32_issue(buf, x, G, o);
   }
   if (threadIdx.x < 3) {
     const int i = threadIdx.x;
@@ -934,7 +972,7 @@ __global__ void __launch_bounds__(NT, 3)
       mbar_wait(&mbar[warp], phase);
       phase ^= 1;
     } else {
-      stage_manual_f32(buf, x, G, o);
+      stage_rows_wait();
     }
     __syncwarp();
     T3P_CLOCK(c2);
@@ -944,12 +982,16 @@ __global__ void __launch_bounds__(NT, 3)
     T3P_CLOCK(c3);
     // staging buffer free: prefetch the next tile
     const int tn = ticket_read(raw);
-    if (lane == 0 && tn < ntiles && G.tma) {
+    if (tn < ntiles) {
       int on[3];
       tile_of(G, nint, tn, on);
-      fence_proxy_async();
-      mbar_expect(&mbar[warp], (uint32_t)BUF_BYTES);
-      tma_load3(sm + warp * P_WARP, &tm, on[2], on[1], on[0] - G.z0, &mbar[warp]);
+      if (G.tma) {
+        fence_proxy_async();
+        tile_load<PX, 4>(buf, &tm, G, on, &mbar[warp]);
+      } else {
+        __syncwarp();  // every lane's pass reads of buf precede the copies
+        stage_rows_f32_issue(buf, x, G, on);
+      }
     }
     // owned codes -> global, histogram (anchors and outliers count as R)
     const int O0 = min(TZ, T.e[0]), O1 = min(TY, T.e[1]), O2 = min(TX, T.e[2]);
@@ -1003,18 +1045,25 @@ __global__ void __launch_bounds__(NT, 3)
         }
       }
     } else {
-      for (int i = lane; i < O0 * O1 * O2; i += 32) {
-        const int row = i / O2, xx = i - row * O2;
-        const int z = row / O1, y = row - z * O1;
-        const uint32_t sy = lds_u16(codea(T, z, y, xx));
-        sym[gbase + z * pz + (int64_t)y * py + xx] = (uint16_t)sy;
-        if (nzmap) {  // O2 == 32 whenever nzmap is set: one row per iteration
-          const uint32_t wd = __ballot_sync(CSZI_FULL, sy != (uint32_t)R);
-          if (lane == 0 && wd) nzmap[(gbase + z * pz + (int64_t)y * py) >> 5] = wd;
+      // row by row, lane = x: coalesced stores, no index divisions
+      for (int z = 0; z < O0; ++z) {
+        for (int y = 0; y < O1; ++y) {
+          const int64_t g0 = gbase + z * pz + (int64_t)y * py;
+          uint32_t sy = (uint32_t)R;
+          if (lane < O2) {
+            sy = lds_u16(codea(T, z, y, lane));
+            sym[g0 + lane] = (uint16_t)sy;
+          }
+          if (nzmap) {  // O2 == 32 whenever nzmap is set
+            const uint32_t wd = __ballot_sync(CSZI_FULL, sy != (uint32_t)R);
+            if (lane == 0 && wd) nzmap[g0 >> 5] = wd;
+          }
+          if (lane < O2) {
+            if (sy == (uint32_t)R || sy == 0) zeros++;
+            else if (G.hist_smem) atomicAdd(&hs[sy], 1u);
+            else atomicAdd(&hist[sy], 1ull);
+          }
         }
-        if (sy == (uint32_t)R || sy == 0) zeros++;
-        else if (G.hist_smem) atomicAdd(&hs[sy], 1u);
-        else atomicAdd(&hist[sy], 1ull);
       }
     }
     __syncwarp();  // codes read before the next tile resets them
@@ -1062,14 +1111,12 @@ __global__ void __launch_bounds__(NT, 3)
   const int ntiles = nint + tile_count<true>(G);
   unsigned int *q = g_t3_sched + 2 * slot;
   int t = next_tile(q);
-  if (lane == 0) {
-    mbar_init(&mbar[warp]);
-    if (t < ntiles && G.tma) {
-      int o[3];
-      tile_of(G, nint, t, o);
-      mbar_expect(&mbar[warp], (uint32_t)(NSYM * 2));
-      tma_load3(sm + warp * R_WARP, &tm, o[2], o[1], o[0] - G.z0, &mbar[warp]);
-    }
+  if (lane == 0) mbar_init(&mbar[warp]);
+  __syncwarp();
+  if (t < ntiles && G.tma) {
+    int o[3];
+    tile_of(G, nint, t, o);
+    tile_load<SP, 2>(syms, &tm, G, o, &mbar[warp]);
   }
   if (threadIdx.x < 3) {
     const int i = threadIdx.x;
@@ -1127,19 +1174,18 @@ __global__ void __launch_bounds__(NT, 3)
       mbar_wait(&mbar[warp], phase);
       phase ^= 1;
     } else {
-      stage_manual_u16(syms, sym, G, o);
+      stage_rows_u16(syms, sym, G, o);
     }
     __syncwarp();
     const unsigned int raw = ticket_issue(q);
     if (T.bnd) run_levels<1, true>(T, C, R, false, O);
     else run_levels_i<1>(T, C, R, O);
     const int tn = ticket_read(raw);
-    if (lane == 0 && tn < ntiles && G.tma) {
+    if (tn < ntiles && G.tma) {
       int on[3];
       tile_of(G, nint, tn, on);
       fence_proxy_async();
-      mbar_expect(&mbar[warp], (uint32_t)(NSYM * 2));
-      tma_load3(sm + warp * R_WARP, &tm, on[2], on[1], on[0] - G.z0, &mbar[warp]);
+      tile_load<SP, 2>(syms, &tm, G, on, &mbar[warp]);
     }
     const int O0 = min(TZ, T.e[0]), O1 = min(TY, T.e[1]), O2 = min(TX, T.e[2]);
     const int64_t gbase = ((int64_t)(o[0] - G.z0) * G.ext[1] + o[1]) * G.ext[2] + o[2];
@@ -1152,10 +1198,10 @@ __global__ void __launch_bounds__(NT, 3)
         __stcs(reinterpret_cast<float4 *>(yout + gbase + z * pz + (int64_t)y * py + 4 * q), v);
       }
     } else {
-      for (int i = lane; i < O0 * O1 * O2; i += 32) {
-        const int row = i / O2, xx = i - row * O2;
-        const int z = row / O1, y = row - z * O1;
-        yout[gbase + z * pz + (int64_t)y * py + xx] = lds_f(bufa(T, z, y, xx));
+      if (lane < O2) {  // row by row, lane = x
+        for (int z = 0; z < O0; ++z)
+          for (int y = 0; y < O1; ++y)
+            __stcs(yout + gbase + z * pz + (int64_t)y * py + lane, lds_f(bufa(T, z, y, lane)));
       }
     }
     __syncwarp();  // buf read before the next tile's anchors land

@@ -54,6 +54,15 @@ def test_tma_and_manual_staging_identical():
     assert out2.data.tobytes() == O.decompress(blob).tobytes()
 
 
+@pytest.mark.parametrize("shape", [(40, 33, 69), (27, 18, 235), (17, 9, 33)])
+def test_row_staging_unaligned_pitch(shape):
+    """Row pitch not a multiple of 16 bytes: row-wise asynchronous staging
+    (prefetched across tiles) against the oracle, at several eb."""
+    data = _smooth(shape, noise=0.02)
+    for eb in (1e-2, 1e-3, 1e-5):
+        _round_trip_equals_oracle(data, eb)
+
+
 def test_sparse_and_dense_huffman_packers():
     # smooth at 1e-3: almost every code is R (sparse packer); noisy at 1e-5:
     # most codes are not (dense packer)
