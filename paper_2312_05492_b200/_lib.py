@@ -240,28 +240,47 @@ def load():
 # device plumbing (torch: allocator, streams)
 # ---------------------------------------------------------------------------
 
-def torch():
-    import torch as _t
+_T = None
+_CUDA_OK = False
+_GET_RAW = None
 
-    return _t
+
+def torch():
+    global _T
+    if _T is None:
+        import torch as _t
+
+        _T = _t
+    return _T
 
 
 def require_cuda():
+    """torch, after checking once that a CUDA device is usable (every entry
+    point calls this first: there is no CPU fallback)."""
+    global _CUDA_OK, _GET_RAW
     t = torch()
-    if not t.cuda.is_available():
-        raise RuntimeError(
-            "paper_2312_05492_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists"
-        )
+    if not _CUDA_OK:
+        if not t.cuda.is_available():
+            raise RuntimeError(
+                "paper_2312_05492_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists"
+            )
+        t.cuda.init()
+        _GET_RAW = getattr(t._C, "_cuda_getCurrentRawStream", None)
+        _CUDA_OK = True
     return t
+
+
+def current_device() -> int:
+    """torch.cuda.current_device() without its per-call lazy-init checks."""
+    return require_cuda()._C._cuda_getDevice()
 
 
 def _raw_stream() -> int:
     """Handle of the current CUDA stream of the current device (the raw
     accessor is ~10x cheaper than torch.cuda.current_stream())."""
-    t = torch()
-    dev = t.cuda.current_device()
-    get = getattr(t._C, "_cuda_getCurrentRawStream", None)
-    return get(dev) if get is not None else t.cuda.current_stream(dev).cuda_stream
+    t = require_cuda()
+    dev = t._C._cuda_getDevice()
+    return _GET_RAW(dev) if _GET_RAW is not None else t.cuda.current_stream(dev).cuda_stream
 
 
 def stream_ptr():
@@ -284,7 +303,7 @@ class Workspace:
 
     def get(self, nbytes: int, key: str = "ws"):
         t = require_cuda()
-        dev = t.cuda.current_device()
+        dev = t._C._cuda_getDevice()
         k = (dev, _raw_stream(), key)
         buf = self._bufs.get(k)
         if buf is None or buf.numel() < nbytes:
@@ -310,7 +329,7 @@ class DeviceCtl:
 
     def __init__(self):
         t = require_cuda()
-        self._key = (t.cuda.current_device(), _raw_stream())
+        self._key = (t._C._cuda_getDevice(), _raw_stream())
         with DeviceCtl._pool_lock:
             free = DeviceCtl._pool.get(self._key)
             pair = free.pop() if free else None

@@ -69,6 +69,23 @@ struct Lv {
   float a32;  // interior fast path: accept |RN32(rec - o)| <= a32 (see quant_i)
 };
 
+// Division by a launch-constant divisor d (n < 2^31): q = (umulhi(n, m) + n)
+// >> s with s = ceil(log2 d), m = floor(2^32 (2^s - d) / d) + 1 (Granlund-
+// Montgomery round-up method; t + n cannot wrap because t <= n < 2^31).
+struct FDiv {
+  uint32_t m, s, d;
+};
+DEV uint32_t fdiv(uint32_t n, const FDiv &f) { return (__umulhi(n, f.m) + n) >> f.s; }
+static inline FDiv make_fdiv(uint32_t d) {
+  FDiv f;
+  f.d = d ? d : 1;
+  uint32_t s = 0;
+  while ((1ull << s) < f.d) ++s;
+  f.s = s;
+  f.m = (uint32_t)((((1ull << s) - f.d) << 32) / f.d + 1);
+  return f;
+}
+
 struct Geo {
   int ext[3];        // global extents
   int nzl;           // planes held by the input buffer (slab incl. halo)
@@ -80,6 +97,9 @@ struct Geo {
   int tma;           // 1: 3-D tensor map valid, 0: row-wise cp.async / load staging
   int exact;         // 1: force the true-division quantiser (tests)
   int64_t na1, na2;  // anchor lattice counts on axes 1, 2 (decompress)
+  // tile-index divisors: ni[2], ni[1], nt[2], nt[1], nt[1] - ni[1], nt[2] - ni[2]
+  FDiv d_ni2, d_ni1, d_nt2, d_nt1, d_wy, d_wx;
+  int shell_a, shell_b;  // edge tiles beyond ni[0] on z / beyond ni[1] on y
 };
 
 // ---------------------------------------------------------------------------
@@ -746,39 +766,35 @@ DEV int tile_count(const Geo &G) {
 }
 template <bool BND>
 DEV void tile_origin(const Geo &G, int t, int o[3]) {
-  int tz, ty, tx;
+  uint32_t tz, ty, tx;
+  const uint32_t u = (uint32_t)t;
   if (!BND) {
-    tx = t % G.ni[2];
-    const int r = t / G.ni[2];
-    ty = r % G.ni[1];
-    tz = r / G.ni[1];
-  } else {
-    const int a = (G.nt[0] - G.ni[0]) * G.nt[1] * G.nt[2];
-    const int b = G.ni[0] * (G.nt[1] - G.ni[1]) * G.nt[2];
-    if (t < a) {
-      tx = t % G.nt[2];
-      const int r = t / G.nt[2];
-      ty = r % G.nt[1];
-      tz = G.ni[0] + r / G.nt[1];
-    } else if (t < a + b) {
-      const int u = t - a;
-      tx = u % G.nt[2];
-      const int r = u / G.nt[2];
-      const int w = G.nt[1] - G.ni[1];
-      ty = G.ni[1] + r % w;
-      tz = r / w;
-    } else {
-      const int u = t - a - b;
-      const int w = G.nt[2] - G.ni[2];
-      tx = G.ni[2] + u % w;
-      const int r = u / w;
-      ty = r % G.ni[1];
-      tz = r / G.ni[1];
-    }
+    const uint32_t r = fdiv(u, G.d_ni2);
+    tx = u - r * G.d_ni2.d;
+    tz = fdiv(r, G.d_ni1);
+    ty = r - tz * G.d_ni1.d;
+  } else if (t < G.shell_a) {  // z beyond the interior box
+    const uint32_t r = fdiv(u, G.d_nt2);
+    tx = u - r * G.d_nt2.d;
+    const uint32_t q = fdiv(r, G.d_nt1);
+    ty = r - q * G.d_nt1.d;
+    tz = (uint32_t)G.ni[0] + q;
+  } else if (t < G.shell_a + G.shell_b) {  // y beyond
+    const uint32_t v = u - (uint32_t)G.shell_a;
+    const uint32_t r = fdiv(v, G.d_nt2);
+    tx = v - r * G.d_nt2.d;
+    tz = fdiv(r, G.d_wy);
+    ty = (uint32_t)G.ni[1] + (r - tz * G.d_wy.d);
+  } else {  // x beyond
+    const uint32_t v = u - (uint32_t)(G.shell_a + G.shell_b);
+    const uint32_t r = fdiv(v, G.d_wx);
+    tx = (uint32_t)G.ni[2] + (v - r * G.d_wx.d);
+    tz = fdiv(r, G.d_ni1);
+    ty = r - tz * G.d_ni1.d;
   }
-  o[0] = G.z0 + tz * TZ;
-  o[1] = ty * TY;
-  o[2] = tx * TX;
+  o[0] = G.z0 + (int)tz * TZ;
+  o[1] = (int)ty * TY;
+  o[2] = (int)tx * TX;
 }
 
 DEV void tile_of(const Geo &G, int nint, int u, int o[3]) {
@@ -813,49 +829,70 @@ DEV void cp_async4_zfill(uint32_t sdst, const void *gsrc, bool valid) {
 DEV void stage_rows_f32_issue(uint32_t buf, const float *x, const Geo &G, const int o[3]) {
   const int lane = threadIdx.x & 31;
   const int zl0 = o[0] - G.z0;
-  const int64_t nx = G.ext[2], ny = G.ext[1];
-  const bool vx0 = o[2] + lane < nx, vx1 = lane < PX - 32 && o[2] + 32 + lane < nx;
-  const float *p = x + ((int64_t)zl0 * ny + o[1]) * nx + o[2] + lane;
-  for (int z = 0; z < CZ; ++z) {
-    const bool vz = zl0 + z < G.nzl;
-    for (int y = 0; y < CY; ++y) {
-      const bool v = vz && o[1] + y < ny;
-      const uint32_t d = buf + 4u * (uint32_t)((z * CY + y) * PX + lane);
-      cp_async4_zfill(d, v && vx0 ? p : x, v && vx0);
-      if (lane < PX - 32) cp_async4_zfill(d + 128u, v && vx1 ? p + 32 : x, v && vx1);
-      p += nx;
+  const int64_t nx = G.ext[2], pzs = (int64_t)G.ext[1] * nx;
+  const int nzv = min(CZ, G.nzl - zl0), nyv = min(CY, G.ext[1] - o[1]);
+  const int nxv = G.ext[2] - o[2];  // columns held from o[2] on
+  const float *p = x + (int64_t)zl0 * pzs + (int64_t)o[1] * nx + o[2];
+  // columns 0..31 (lane = x).  Rows beyond the grid read a held row with
+  // size 0 (zero fill), so every source address stays inside the field.
+  {
+    const bool vx = lane < nxv;
+    const float *pl = p + (vx ? lane : 0);
+    uint32_t d = buf + 4u * (uint32_t)lane;
+    for (int z = 0; z < CZ; ++z) {
+      const bool vz = vx && z < nzv;
+      const float *pr = pl + (int64_t)min(z, nzv - 1) * pzs;
+#pragma unroll
+      for (int y = 0; y < CY; ++y) {
+        const bool v = vz && y < nyv;
+        cp_async4_zfill(d + 4u * (uint32_t)(y * PX), pr + (int64_t)min(y, nyv - 1) * nx, v);
+      }
+      d += 4u * PZ;
     }
-    p += (ny - CY) * nx;
+  }
+  // closing column x = 32, lane = row (z, y) of the 81.  Columns 33..35 of
+  // the pitch-36 rows are only read by the pad lines of quad 8, whose
+  // results are never stored: they are not staged.
+  for (int r = lane; r < CZ * CY; r += 32) {
+    const int z = r / CY, y = r - z * CY;
+    const bool v = nxv > 32 && z < nzv && y < nyv;
+    const float *src = p + (int64_t)min(z, nzv - 1) * pzs + (int64_t)min(y, nyv - 1) * nx +
+                       (nxv > 32 ? 32 : 0);
+    cp_async4_zfill(buf + 4u * (uint32_t)(r * PX + 32), src, v);
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 DEV void stage_rows_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // symbols (2-byte elements: no 2-byte cp.async): plain loads, one z-plane
-// (9 rows) in flight per batch, then the stores
+// (9 rows) in flight per batch, then the stores; the closing column x = 32
+// with lane = row.  Columns 33..39 feed only pad lines: not staged.
 DEV void stage_rows_u16(uint32_t dst, const uint16_t *sym, const Geo &G, const int o[3]) {
   const int lane = threadIdx.x & 31;
   const int zl0 = o[0] - G.z0;
-  const int64_t nx = G.ext[2], ny = G.ext[1];
-  const bool vx0 = o[2] + lane < nx, vx1 = lane < SP - 32 && o[2] + 32 + lane < nx;
-  const uint16_t *p = sym + ((int64_t)zl0 * ny + o[1]) * nx + o[2] + lane;
+  const int64_t nx = G.ext[2], pzs = (int64_t)G.ext[1] * nx;
+  const int nzv = min(CZ, G.nzl - zl0), nyv = min(CY, G.ext[1] - o[1]);
+  const int nxv = G.ext[2] - o[2];
+  const uint16_t *p = sym + (int64_t)zl0 * pzs + (int64_t)o[1] * nx + o[2];
+  const bool vx = lane < nxv;
+  const uint16_t *pl = p + (vx ? lane : 0);
+  uint32_t d = dst + 2u * (uint32_t)lane;
   for (int z = 0; z < CZ; ++z) {
-    const bool vz = zl0 + z < G.nzl;
-    uint32_t a[CY], b[CY];
+    const bool vz = vx && z < nzv;
+    const uint16_t *pr = pl + (int64_t)min(z, nzv - 1) * pzs;
+    uint32_t a[CY];
 #pragma unroll
-    for (int y = 0; y < CY; ++y) {
-      const bool v = vz && o[1] + y < ny;
-      const uint16_t *q = p + (int64_t)y * nx;
-      a[y] = (v && vx0) ? __ldg(q) : 0u;
-      b[y] = (v && vx1) ? __ldg(q + 32) : 0u;
-    }
+    for (int y = 0; y < CY; ++y)
+      a[y] = (vz && y < nyv) ? __ldg(pr + (int64_t)y * nx) : 0u;
 #pragma unroll
-    for (int y = 0; y < CY; ++y) {
-      const uint32_t d = dst + 2u * (uint32_t)((z * CY + y) * SP + lane);
-      sts_u16(d, a[y]);
-      if (lane < SP - 32) sts_u16(d + 64u, b[y]);
-    }
-    p += ny * nx;
+    for (int y = 0; y < CY; ++y) sts_u16(d + 2u * (uint32_t)(y * SP), a[y]);
+    d += 2u * (uint32_t)(CY * SP);
+  }
+  for (int r = lane; r < CZ * CY; r += 32) {
+    const int z = r / CY, y = r - z * CY;
+    const bool v = nxv > 32 && z < nzv && y < nyv;
+    const uint32_t w = v ? __ldg(p + (int64_t)z * pzs + (int64_t)y * nx + 32) : 0u;
+    sts_u16(dst + 2u * (uint32_t)(r * SP + 32), w);
   }
 }
 
@@ -917,8 +954,8 @@ __global__ void __launch_bounds__(NT, 3)
   int t = next_tile(q);
   if (lane == 0) mbar_init(&mbar[warp]);
   __syncwarp();
+  int o[3] = {0, 0, 0};  // origin of tile t (carried from the prefetch)
   if (t < ntiles) {
-    int o[3];
     tile_of(G, nint, t, o);
     if (G.tma) tile_load<PX, 4>(buf, &tm, G, o, &mbar[warp]);
     else stage_rows_f32_issue(buf, x, G, o);
@@ -948,8 +985,6 @@ __global__ void __launch_bounds__(NT, 3)
 #endif
   while (t < ntiles) {
     T3P_CLOCK(c0);
-    int o[3];
-    tile_of(G, nint, t, o);
     Tile T;
     T.buf = buf;
     T.codes = codes;
@@ -963,7 +998,7 @@ __global__ void __launch_bounds__(NT, 3)
     } else if (lane < 4) {
       sts_u16(codes + 2u * 8 * lane, (uint32_t)R);
     }
-    if (nzmap) {
+    if (nzmap) {  // non-R words of the tile's rows (epilogue)
       nzs[lane] = 0u;
       nzs[lane + 32] = 0u;
     }
@@ -982,8 +1017,8 @@ __global__ void __launch_bounds__(NT, 3)
     T3P_CLOCK(c3);
     // staging buffer free: prefetch the next tile
     const int tn = ticket_read(raw);
+    int on[3] = {0, 0, 0};
     if (tn < ntiles) {
-      int on[3];
       tile_of(G, nint, tn, on);
       if (G.tma) {
         fence_proxy_async();
@@ -1045,28 +1080,39 @@ __global__ void __launch_bounds__(NT, 3)
         }
       }
     } else {
-      // row by row, lane = x: coalesced stores, no index divisions
+      // row by row, lane = x: coalesced 2-byte stores, pointers stepped per
+      // row; R / outlier codes counted per lane, the histogram atomics only
+      // run for rows that hold another code
+      const bool act = lane < O2;
+      uint16_t *gz = sym + gbase + lane;
+      uint32_t cz = codea(T, 0, 0, lane);
       for (int z = 0; z < O0; ++z) {
+        uint16_t *gy = gz;
+        uint32_t cy = cz;
         for (int y = 0; y < O1; ++y) {
-          const int64_t g0 = gbase + z * pz + (int64_t)y * py;
-          uint32_t sy = (uint32_t)R;
-          if (lane < O2) {
-            sy = lds_u16(codea(T, z, y, lane));
-            sym[g0 + lane] = (uint16_t)sy;
-          }
+          const uint32_t sy = act ? lds_u16(cy) : (uint32_t)R;
+          if (act) *gy = (uint16_t)sy;
           if (nzmap) {  // O2 == 32 whenever nzmap is set
             const uint32_t wd = __ballot_sync(CSZI_FULL, sy != (uint32_t)R);
-            if (lane == 0 && wd) nzmap[g0 >> 5] = wd;
+            if (lane == 0 && wd) nzmap[(gy - sym) >> 5] = wd;
           }
-          if (lane < O2) {
-            if (sy == (uint32_t)R || sy == 0) zeros++;
-            else if (G.hist_smem) atomicAdd(&hs[sy], 1u);
+          const bool other = act && sy != (uint32_t)R && sy != 0;
+          zeros += (uint32_t)(act && !other);
+          if (__any_sync(CSZI_FULL, other) && other) {
+            if (G.hist_smem) atomicAdd(&hs[sy], 1u);
             else atomicAdd(&hist[sy], 1ull);
           }
+          gy += py;
+          cy += 2u * CP;
         }
+        gz += pz;
+        cz += 2u * TY * CP;
       }
     }
     __syncwarp();  // codes read before the next tile resets them
+    o[0] = on[0];
+    o[1] = on[1];
+    o[2] = on[2];
 #ifdef T3_PROF
     pc[0] += c1 - c0;
     pc[1] += c2 - c1;
@@ -1094,6 +1140,15 @@ __global__ void __launch_bounds__(NT, 3)
       if (hs[i]) atomicAdd(&hist[i], (u64)hs[i]);
 }
 
+// anchor value lane (< 20) seeds on an interior tile at origin o: z, y in
+// {0, 8}, x in {0, 8, 16, 24, 32} of the closed tile (lattice row-major)
+DEV float anchor_i(const float *anchors, const Geo &G, const int o[3], int lane) {
+  if (lane >= 20) return 0.f;
+  const int iz = lane / 10, iy = (lane / 5) & 1, ix = lane % 5;
+  const int64_t kz = o[0] / 8 + iz, ky = o[1] / 8 + iy, kx = o[2] / 8 + ix;
+  return __ldg(anchors + (kz * G.na1 + ky) * G.na2 + kx);
+}
+
 __global__ void __launch_bounds__(NT, 3)
     k_t3_reconstruct(const __grid_constant__ CUtensorMap tm, const uint16_t *__restrict__ sym,
                      const float *__restrict__ anchors, const u64 *out_idx,
@@ -1113,10 +1168,12 @@ __global__ void __launch_bounds__(NT, 3)
   int t = next_tile(q);
   if (lane == 0) mbar_init(&mbar[warp]);
   __syncwarp();
-  if (t < ntiles && G.tma) {
-    int o[3];
+  int o[3] = {0, 0, 0};  // origin of tile t (carried from the prefetch)
+  float apre = 0.f;      // lane < 20: interior anchor value of tile t
+  if (t < ntiles) {
     tile_of(G, nint, t, o);
-    tile_load<SP, 2>(syms, &tm, G, o, &mbar[warp]);
+    if (G.tma) tile_load<SP, 2>(syms, &tm, G, o, &mbar[warp]);
+    if (t < nint) apre = anchor_i(anchors, G, o, lane);
   }
   if (threadIdx.x < 3) {
     const int i = threadIdx.x;
@@ -1135,8 +1192,6 @@ __global__ void __launch_bounds__(NT, 3)
   const int py = G.ext[2];
   uint32_t phase = 0;
   while (t < ntiles) {
-    int o[3];
-    tile_of(G, nint, t, o);
     Tile T;
     T.buf = buf;
     T.codes = 0;
@@ -1149,12 +1204,9 @@ __global__ void __launch_bounds__(NT, 3)
     __syncwarp();
     // seed the anchors of the closed tile (multiples of 8, plus ext - 1)
     if (!T.bnd) {
-      // interior: z, y in {0, 8}, x in {0, 8, 16, 24, 32}; no closing anchors
-      if (lane < 20) {
-        const int iz = lane / 10, iy = (lane / 5) & 1, ix = lane % 5;
-        const int64_t kz = o[0] / 8 + iz, ky = o[1] / 8 + iy, kx = o[2] / 8 + ix;
-        sts_f(bufa(T, 8 * iz, 8 * iy, 8 * ix), __ldg(anchors + (kz * G.na1 + ky) * G.na2 + kx));
-      }
+      // interior: z, y in {0, 8}, x in {0, 8, 16, 24, 32}; no closing anchors.
+      // The values were loaded when this tile was prefetched (apre).
+      if (lane < 20) sts_f(bufa(T, 8 * (lane / 10), 8 * ((lane / 5) & 1), 8 * (lane % 5)), apre);
     } else {
       int az[3], ay[3], ax[6];
       const int nz = anchor_axis_local<CZ, 8>(T.e[0], az);
@@ -1181,30 +1233,49 @@ __global__ void __launch_bounds__(NT, 3)
     if (T.bnd) run_levels<1, true>(T, C, R, false, O);
     else run_levels_i<1>(T, C, R, O);
     const int tn = ticket_read(raw);
-    if (tn < ntiles && G.tma) {
-      int on[3];
+    int on[3] = {0, 0, 0};
+    if (tn < ntiles) {
       tile_of(G, nint, tn, on);
-      fence_proxy_async();
-      tile_load<SP, 2>(syms, &tm, G, on, &mbar[warp]);
+      if (G.tma) {
+        fence_proxy_async();
+        tile_load<SP, 2>(syms, &tm, G, on, &mbar[warp]);
+      }
+      if (tn < nint) apre = anchor_i(anchors, G, on, lane);
     }
     const int O0 = min(TZ, T.e[0]), O1 = min(TY, T.e[1]), O2 = min(TX, T.e[2]);
     const int64_t gbase = ((int64_t)(o[0] - G.z0) * G.ext[1] + o[1]) * G.ext[2] + o[2];
     if (O0 == TZ && O1 == TY && O2 == TX && (G.ext[2] & 3) == 0) {
-#pragma unroll 4
-      for (int i = lane; i < TZ * TY * 8; i += 32) {
-        const int row = i >> 3, q = i & 7;
-        const int z = row >> 3, y = row & 7;
-        const float4 v = lds_f4(bufa(T, z, y, 4 * q));
-        __stcs(reinterpret_cast<float4 *>(yout + gbase + z * pz + (int64_t)y * py + 4 * q), v);
+      // lane = (quad q = lane % 8, row y0 = lane / 8 and y0 + 4), z = 0..7
+      const int q4 = 4 * (lane & 7), y0 = lane >> 3;
+      const uint32_t s0 = bufa(T, 0, y0, q4);
+      float *d0 = yout + gbase + (int64_t)y0 * py + q4;
+#pragma unroll
+      for (int z = 0; z < TZ; ++z) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          __stcs(reinterpret_cast<float4 *>(d0 + 4 * h * py),
+                 lds_f4(s0 + 4u * (uint32_t)(z * PZ + 4 * h * PX)));
+        d0 += pz;
       }
-    } else {
-      if (lane < O2) {  // row by row, lane = x
-        for (int z = 0; z < O0; ++z)
-          for (int y = 0; y < O1; ++y)
-            __stcs(yout + gbase + z * pz + (int64_t)y * py + lane, lds_f(bufa(T, z, y, lane)));
+    } else if (lane < O2) {  // row by row, lane = x, pointers stepped per row
+      float *dz = yout + gbase + lane;
+      uint32_t sz = bufa(T, 0, 0, lane);
+      for (int z = 0; z < O0; ++z) {
+        float *dy = dz;
+        uint32_t sy = sz;
+        for (int y = 0; y < O1; ++y) {
+          __stcs(dy, lds_f(sy));
+          dy += py;
+          sy += 4u * PX;
+        }
+        dz += pz;
+        sz += 4u * PZ;
       }
     }
     __syncwarp();  // buf read before the next tile's anchors land
+    o[0] = on[0];
+    o[1] = on[1];
+    o[2] = on[2];
     t = tn;
   }
   sched_done(q);
@@ -1295,9 +1366,17 @@ static bool t3_geo(const cszi_geom *g, int32_t radius, Geo &G) {
       G.ni[a] = (int)(n < G.nt[a] ? n : G.nt[a]);
     }
   }
-  if ((int64_t)G.nt[0] * G.nt[1] * G.nt[2] > (int64_t)NW * 0x7fffffff) return false;
+  if ((int64_t)G.nt[0] * G.nt[1] * G.nt[2] >= 0x7fffffffll) return false;  // int tile ids
   // flat indices of the outlier lookup and of planes are int64; the
   // in-kernel (z * gs0 + ...) products need ext[1] * ext[2] < 2^62: fine.
+  G.d_ni2 = make_fdiv((uint32_t)G.ni[2]);
+  G.d_ni1 = make_fdiv((uint32_t)G.ni[1]);
+  G.d_nt2 = make_fdiv((uint32_t)G.nt[2]);
+  G.d_nt1 = make_fdiv((uint32_t)G.nt[1]);
+  G.d_wy = make_fdiv((uint32_t)(G.nt[1] - G.ni[1]));
+  G.d_wx = make_fdiv((uint32_t)(G.nt[2] - G.ni[2]));
+  G.shell_a = (G.nt[0] - G.ni[0]) * G.nt[1] * G.nt[2];
+  G.shell_b = G.ni[0] * (G.nt[1] - G.ni[1]) * G.nt[2];
   G.R = radius;
   G.hist_smem = (2 * radius <= 2048) ? 1 : 0;
   G.tma = 0;

@@ -14,6 +14,7 @@ while every grid-sized computation runs in libcszi on the GPU:
 from __future__ import annotations
 
 import ctypes
+import functools
 import math
 from dataclasses import dataclass, field
 
@@ -62,8 +63,10 @@ class ChunkLayout:
                 raise Inconsistent(f"super-chunk extent {e} is not a multiple of the anchor stride")
 
 
+@functools.lru_cache(maxsize=None)
 def default_layout(rank: int) -> ChunkLayout:
-    """Stride 8 / tiles (8,8,32) in 3D, 16 / (16,16) in 2D, 512 in 1D."""
+    """Stride 8 / tiles (8,8,32) in 3D, 16 / (16,16) in 2D, 512 in 1D
+    (frozen, so one shared instance per rank)."""
     return ChunkLayout(_DEFAULT_STRIDE[rank], rank, _DEFAULT_TILES[rank])
 
 

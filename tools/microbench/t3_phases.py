@@ -10,7 +10,8 @@ import torch
 import paper_2312_05492_b200 as P
 from paper_2312_05492_b200 import _lib
 from bench import smooth_field_gpu
-x = smooth_field_gpu((512, 512, 512))
+shape = tuple(int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "512,512,512").split(","))
+x = smooth_field_gpu(shape)
 for _ in range(2):
     P.compress_device(P.Grid(P.Dims(x.shape), x), 1e-3)
 torch.cuda.synchronize()
@@ -26,7 +27,7 @@ tot = sum(buf[i] for i in range(4))
 for i, nm in enumerate(names):
     print(f"{nm:10s} {buf[i] / n:10.0f} cycles/tile  {100 * buf[i] / tot:5.1f}%")
 print("tiles", n)
-ni = 63 * 63 * 15  # interior tiles of 512^3
+ni = ((shape[0] - 1) // 8) * ((shape[1] - 1) // 8) * ((shape[2] - 1) // 32)  # interior tiles
 for lv in range(3):
     print("level s=%d:" % (4 >> lv), " ".join(f"{buf[6 + lv * 3 + i] / ni:8.0f}" for i in range(3)))
 
