@@ -10,6 +10,7 @@ from __future__ import annotations
 import ctypes
 import os
 import subprocess
+import sys
 import threading
 
 import numpy as np
@@ -314,6 +315,39 @@ class Workspace:
 
 
 WS = Workspace()
+
+
+class PinnedPool:
+    """Pinned host buffers for results handed to the caller (decompress()
+    output grids, archive bytes).  A buffer is reused once nothing outside
+    the pool shares its storage (numpy arrays and views made from it hold
+    the storage, so a Grid still held by the caller keeps its buffer).
+    torch's caching host allocator does not reliably reuse 0.5 GB blocks,
+    and a fresh cudaHostAlloc of that size costs ~80 ms.  Reuse is safe:
+    every user synchronises its stream before handing the buffer out."""
+
+    def __init__(self, per_size: int = 4):
+        self._free = {}
+        self._per = per_size
+        self._lock = threading.Lock()
+
+    def get(self, nbytes: int):
+        t = require_cuda()
+        nbytes = max(int(nbytes), 1)
+        with self._lock:
+            bufs = self._free.setdefault(nbytes, [])
+            use = getattr(t._C, "_storage_Use_Count", None)
+            for b in bufs:
+                # the pool's tensor + the temporary storage object: nobody else
+                if use is not None and use(b.untyped_storage()._cdata) == 2:
+                    return b
+            b = t.empty(nbytes, dtype=t.uint8, pin_memory=True)
+            if len(bufs) < self._per:
+                bufs.append(b)
+            return b
+
+
+PINNED = PinnedPool()
 
 
 class DeviceCtl:

@@ -89,7 +89,7 @@ class DeviceArchive:
             return self.header + self.payload
         t = _lib.torch()
         n = self.payload.numel()
-        host = t.empty(n, dtype=t.uint8, pin_memory=True)
+        host = _lib.PINNED.get(n)
         if n:
             host.copy_(self.payload, non_blocking=True)
             t.cuda.current_stream().synchronize()
@@ -571,18 +571,78 @@ def decompress(data: bytes, threads: int = None) -> Grid:
 
     The reference wraps the result in Grid(), whose finite scan raises
     NonFiniteValue for NaN/Inf outlier or anchor values of a crafted archive;
-    that scan runs on the device here before one pinned device->host copy."""
-    g = decompress_device(data, threads)
-    t = _lib.torch()
+    that scan runs on the device here before the pinned device->host copy.
+    Large 3-D archives are reconstructed z-slab by z-slab, each slab's copy
+    to the host running on a copy stream under the next slab's kernels."""
+    thread_count(threads)
+    t = _lib.require_cuda()
+    head, d_payload, h_payload, total = _split_input(data)
+    plan = _pipeline_slabs(unpack_header(head, total)) if total >= HEADER_SIZE else None
+    if plan is None:
+        g = decompress_device(data, threads)
+        y = g.tensor.reshape(-1)
+        bounds, plane = [(0, 1)], y.numel()
+        parts = [y]
+    else:
+        # one upload of the payload, then one decompress_device per slab
+        dims, bounds, plane = plan
+        if d_payload is None:
+            d_payload = _lib.to_device_u8(h_payload)
+        arch = DeviceArchive(header=head, payload=d_payload)
+        parts = None
     lib = _lib.load()
-    y = g.tensor.reshape(-1)
     ctl = _lib.DeviceCtl()
     st = _lib.stream_ptr()
     _lib.check(lib.cszi_ctl_init(ctl.ptr, st), "ctl_init")
-    _lib.check(lib.cszi_range(_lib.ptr(y), y.numel(), ctl.ptr, st), "range")
-    host = t.empty(y.numel(), dtype=t.float32, pin_memory=True)
-    host.copy_(y, non_blocking=True)
-    c = ctl.fetch()  # synchronises the stream (covers the copy)
+    n = bounds[-1][1] * plane
+    host = _lib.PINNED.get(4 * n).view(t.float32)
+    main = t.cuda.current_stream()
+    cs = _copy_stream()
+    for i, (z0, z1) in enumerate(bounds):
+        y = parts[i] if parts is not None else \
+            decompress_device(arch, slab=(z0, z1)).reshape(-1)
+        _lib.check(lib.cszi_range(_lib.ptr(y), y.numel(), ctl.ptr, st), "range")
+        done = t.cuda.Event()
+        done.record(main)
+        cs.wait_event(done)
+        with t.cuda.stream(cs):
+            host[z0 * plane:z1 * plane].copy_(y, non_blocking=True)
+        y.record_stream(cs)
+    c = ctl.fetch()  # synchronises the compute stream
+    cs.synchronize()
     if c.first_nonfinite != 2**64 - 1:
         raise NonFiniteValue(int(c.first_nonfinite))
-    return Grid.wrap_host(g.dims, host.numpy())
+    if plan is None:
+        return Grid.wrap_host(g.dims, host.numpy())
+    return Grid.wrap_host(dims, host.numpy())
+
+
+_PIPE_MIN_VALUES = 1 << 25  # 128 MB: smaller fields copy back in well under a millisecond
+_PIPE_SLABS = 4
+_copy_streams = {}
+
+
+def _copy_stream():
+    t = _lib.torch()
+    dev = _lib.current_device()
+    s = _copy_streams.get(dev)
+    if s is None:
+        s = _copy_streams[dev] = t.cuda.Stream(device=dev)
+    return s
+
+
+def _pipeline_slabs(h):
+    """(dims, z-slab bounds, plane size) when decompress() can pipeline the
+    archive by slabs (3-D interp archive, default layout, built-in pass-2
+    codec or none, large enough), else None."""
+    if h.predictor != PREDICTOR_INTERP or h.rank != 3 or h.anchor_stride != 8:
+        return None
+    if h.pass2 and h.pass2_codec != DEFAULT_CODEC:
+        return None
+    nz, ny, nx = h.extents
+    if nz * ny * nx < _PIPE_MIN_VALUES or nz < 8 * _PIPE_SLABS:
+        return None
+    from .distributed import slab_bounds
+
+    bounds = [b for b in slab_bounds(nz, _PIPE_SLABS) if b[1] > b[0]]
+    return Dims(h.extents), bounds, ny * nx

@@ -31,3 +31,7 @@ def test_nyx_512_cube_archive_identical_to_oracle():
     # checksum of the decompressed field against the oracle's
     assert hashlib.sha256(y.data.tobytes()).digest() == \
         hashlib.sha256(O.decompress(ref).tobytes()).digest()
+    # decompress(bytes) reconstructs this field slab by slab with overlapped
+    # host copies (pipeline._pipeline_slabs): the same bytes
+    back = P.decompress(blob)
+    assert back.data.tobytes() == y.data.tobytes()
