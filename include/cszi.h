@@ -265,6 +265,43 @@ int cszi_interp_level(float *recon, const float *source, int32_t *codes, uint8_t
 int cszi_gather_anchors(const float *x, const cszi_geom *g, float *out, void *stream);
 uint64_t cszi_slab_anchor_count(const cszi_geom *g);
 
+/* ---- sharded compress glue (multi-GPU z-slabs) ---------------
+ * One call per slab and step of distributed.compress_slabs_batch (no
+ * reference counterpart: the reference's only split is the thread pool of
+ * predictor.py:347-364, whose output is byte-identical by construction).
+ * cszi_shard_scan: ctl reset, range + finite scan of the n_own owned values,
+ *   tuner sample gather (zeros for an empty slab), and keys[3] =
+ *   (vmin key, -vmax key, first non-finite flat index + flat0 or INT64_MAX),
+ *   ready for an all-reduce MIN.
+ * cszi_shard_set_range: the reduced keys back into ctl.
+ * cszi_shard_piece_bits: *out = sum(hist[i] * lengths[i]) (the slab's
+ *   Huffman piece length in bits, outliers coded as R).
+ * cszi_shard_counts: out[2] = (ctl->bits, ctl->n_outliers) after an encode. */
+int cszi_shard_scan(const float *x, uint64_t n_own, uint64_t flat0, const cszi_geom *g,
+                    cszi_ctl *ctl, int64_t *keys, int32_t *samples, void *stream);
+int cszi_shard_set_range(cszi_ctl *ctl, const int64_t *keys, void *stream);
+int cszi_shard_piece_bits(const uint64_t *hist, const uint8_t *lengths, int32_t nbins,
+                          int64_t *out, void *stream);
+int cszi_shard_counts(const cszi_ctl *ctl, int64_t *out, void *stream);
+
+/* Root of the sharded compress (replaces the whole-field _field_sections /
+ * serialize payload, pipeline.py:59-63, archive.py:102-127, for slab
+ * pieces): raw = the np anchor pieces (na[i] floats each, slab order) ||
+ * code lengths (nbins bytes) || bitstream || outlier section (count, then
+ * the pieces' records), then pass-2 into payload when pass2 != 0 (else raw
+ * is the payload).  bits[i] is slab i's piece packed at global bit bit0[i]:
+ * its word 0 holds global bits from (bit0[i] & ~31); nbits[i] bits.  Host
+ * arrays of device pointers.  ctl->raw_len / payload_len are set on the
+ * device.  raw_cap >= 4 sum(na) + nbins + 4 (total_bits / 32 + 2) +
+ * 8 + 12 sum(nout); workspace >= cszi_pass2_encode_workspace_size(raw). */
+int cszi_shard_assemble(int32_t np, const float *const *anchors, const uint64_t *na,
+                        const uint8_t *lengths, int32_t nbins, const uint8_t *const *bits,
+                        const uint64_t *bit0, const uint64_t *nbits,
+                        const uint64_t *const *oidx, const float *const *oval,
+                        const uint64_t *nout, int32_t pass2, uint8_t *raw, uint64_t raw_cap,
+                        uint8_t *payload, void *workspace, uint64_t ws_bytes, cszi_ctl *ctl,
+                        void *stream);
+
 /* profile_samples split for sharding (tuning.py:42-74): gather the packed
  * sample values (float32 bit patterns, 0 where the point lies outside the
  * owned planes of g->slab) ... */

@@ -165,6 +165,12 @@ _SIGS = {
          _vp],
     ),
     "cszi_slab_anchor_count": (_u64, [_vp]),
+    "cszi_shard_scan": (ctypes.c_int, [_vp, _u64, _u64, _vp, _vp, _vp, _vp, _vp]),
+    "cszi_shard_set_range": (ctypes.c_int, [_vp, _vp, _vp]),
+    "cszi_shard_piece_bits": (ctypes.c_int, [_vp, _vp, _i32, _vp, _vp]),
+    "cszi_shard_counts": (ctypes.c_int, [_vp, _vp, _vp]),
+    "cszi_shard_assemble": (ctypes.c_int, [_i32, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp,
+                                           _vp, _i32, _vp, _u64, _vp, _vp, _u64, _vp, _vp]),
     "cszi_sample_gather": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "cszi_tune_from_samples": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "cszi_encode_sym_workspace_size": (_u64, [_u64]),

@@ -163,6 +163,76 @@ __global__ void k_outliers_mark(const u64 *oidx, const cszi_ctl *ctl, u64 n, uin
 
 
 // ---------------------------------------------------------------------------
+// sharded compress glue (distributed.py): one launch per step instead of a
+// chain of host-side tensor ops per slab
+// ---------------------------------------------------------------------------
+// range keys of a slab for the MIN all-reduce: (vmin key, -vmax key, first
+// non-finite global flat index or INT64_MAX)
+__global__ void k_shard_keys(const cszi_ctl *ctl, u64 flat0, int64_t *keys) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  keys[0] = (int64_t)ctl->vmin_key;
+  keys[1] = -(int64_t)ctl->vmax_key;
+  const u64 f = ctl->first_nonfinite;
+  keys[2] = (f == ~0ull) ? INT64_MAX : (int64_t)(f + flat0);
+}
+// the all-reduced keys back into a slab's ctl
+__global__ void k_shard_set_range(cszi_ctl *ctl, const int64_t *keys) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  ctl->vmin_key = (uint32_t)keys[0];
+  ctl->vmax_key = (uint32_t)(-keys[1]);
+  ctl->first_nonfinite = (keys[2] == INT64_MAX) ? ~0ull : (u64)keys[2];
+}
+// bits of a slab's Huffman piece: local histogram . code lengths (outliers
+// and anchors are counted as R, which is how they are coded)
+__global__ void k_shard_piece_bits(const u64 *hist, const uint8_t *lengths, int nbins,
+                                   int64_t *out) {
+  __shared__ u64 part[32];
+  u64 v = 0;
+  for (int i = threadIdx.x; i < nbins; i += blockDim.x) v += hist[i] * (u64)lengths[i];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(CSZI_FULL, v, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u64 t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += part[w];
+    *out = (int64_t)t;
+  }
+}
+// (bit count, outlier count) of an encoded slab piece
+__global__ void k_shard_counts(const cszi_ctl *ctl, int64_t *out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  out[0] = (int64_t)ctl->bits;
+  out[1] = (int64_t)ctl->n_outliers;
+}
+
+// root assembly of a sharded archive (cszi_shard_assemble)
+__global__ void k_or_words(uint32_t *dst, const uint32_t *src, u64 nw) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < nw; i += (u64)gridDim.x * blockDim.x)
+    dst[i] |= src[i];
+}
+__global__ void k_shard_records(const u64 *idx, const float *val, u64 k, uint8_t *out) {
+  for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < k;
+       r += (u64)gridDim.x * blockDim.x) {
+    uint8_t *q = out + 12 * r;
+    const u64 ix = idx[r];
+    const uint32_t vb = __float_as_uint(val[r]);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) q[b] = (uint8_t)(ix >> (8 * b));
+#pragma unroll
+    for (int b = 0; b < 4; ++b) q[8 + b] = (uint8_t)(vb >> (8 * b));
+  }
+}
+__global__ void k_shard_tail(uint8_t *count_at, u64 k, u64 raw_len, int is_payload,
+                             cszi_ctl *ctl) {
+  if (blockIdx.x != 0) return;
+  if (threadIdx.x < 8) count_at[threadIdx.x] = (uint8_t)(k >> (8 * threadIdx.x));
+  if (threadIdx.x == 0) {
+    ctl->raw_len = raw_len;
+    if (is_payload) ctl->payload_len = raw_len;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // workspace layout
 // ---------------------------------------------------------------------------
 static inline u64 al(u64 b) { return (b + 255) & ~(u64)255; }
@@ -771,6 +841,114 @@ int cszi_tune_from_samples(const int32_t *vals, const cszi_geom *g, const cszi_p
                            cszi_ctl *ctl, void *stream) {
   CK(check_geom(g, p->radius));
   return launch_tune_from_samples(vals, g, p, ctl, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// ---- sharded compress glue (distributed.py) --------------------------------
+int cszi_shard_scan(const float *x, uint64_t n_own, uint64_t flat0, const cszi_geom *g,
+                    cszi_ctl *ctl, int64_t *keys, int32_t *samples, void *stream) {
+  if (!g || !ctl || !keys || !samples || (n_own && !x)) return CSZI_E_INVALID_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CK(launch_ctl_init(ctl, st));
+  if (n_own) {
+    CK(launch_range(x, n_own, ctl, st));
+    CK(launch_sample_gather(x, g, samples, st));
+  } else {
+    cudaMemsetAsync(samples, 0, sizeof(int32_t) * CSZI_SAMPLE_WORDS, st);
+  }
+  k_shard_keys<<<1, 32, 0, st>>>(ctl, flat0, keys);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
+int cszi_shard_set_range(cszi_ctl *ctl, const int64_t *keys, void *stream) {
+  if (!ctl || !keys) return CSZI_E_INVALID_ARG;
+  k_shard_set_range<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(ctl, keys);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
+int cszi_shard_piece_bits(const uint64_t *hist, const uint8_t *lengths, int32_t nbins,
+                          int64_t *out, void *stream) {
+  if (!hist || !lengths || !out || nbins < 1) return CSZI_E_INVALID_ARG;
+  k_shard_piece_bits<<<1, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const u64 *>(hist), lengths, nbins, out);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
+int cszi_shard_counts(const cszi_ctl *ctl, int64_t *out, void *stream) {
+  if (!ctl || !out) return CSZI_E_INVALID_ARG;
+  k_shard_counts<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(ctl, out);
+  note_launch();
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
+int cszi_shard_assemble(int32_t np, const float *const *anchors, const uint64_t *na,
+                        const uint8_t *lengths, int32_t nbins, const uint8_t *const *bits,
+                        const uint64_t *bit0, const uint64_t *nbits,
+                        const uint64_t *const *oidx, const float *const *oval,
+                        const uint64_t *nout, int32_t pass2, uint8_t *raw, uint64_t raw_cap,
+                        uint8_t *payload, void *workspace, uint64_t ws_bytes, cszi_ctl *ctl,
+                        void *stream) {
+  if (np < 1 || !anchors || !na || !lengths || !bits || !bit0 || !nbits || !oidx || !oval ||
+      !nout || !raw || !ctl || (pass2 && (!payload || !workspace)))
+    return CSZI_E_INVALID_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  u64 off = 0, total_bits = 0, kt = 0;
+  for (int i = 0; i < np; ++i) {
+    total_bits += nbits[i];
+    kt += nout[i];
+    off += 4 * na[i];
+  }
+  const u64 head = off + (u64)nbins;
+  const u64 nbytes = (total_bits + 7) / 8;
+  const u64 words = (total_bits + 31) / 32 + 1;
+  const u64 raw_len = head + nbytes + 8 + 12 * kt;
+  if (head + 4 * words > raw_cap || raw_len > raw_cap) return CSZI_E_CAPACITY;
+  if (pass2 && ws_bytes < p2enc_scratch_bytes(raw_len)) return CSZI_E_CAPACITY;
+  off = 0;
+  for (int i = 0; i < np; ++i) {
+    if (na[i]) cudaMemcpyAsync(raw + off, anchors[i], 4 * na[i], cudaMemcpyDeviceToDevice, st);
+    off += 4 * na[i];
+  }
+  cudaMemcpyAsync(raw + off, lengths, (size_t)nbins, cudaMemcpyDeviceToDevice, st);
+  // bit pieces: each was packed at its global bit phase (distributed.py), so
+  // a word-aligned section takes them as whole words, ORed at their word
+  // offsets (a piece's first and last words are shared with its neighbours)
+  cudaMemsetAsync(raw + head, 0, 4 * words, st);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(raw) + head) & 3) == 0;
+  for (int i = 0; i < np; ++i) {
+    if (!nbits[i]) continue;
+    const u64 ph = bit0[i] & 31;
+    if (aligned) {
+      const u64 nw = (ph + nbits[i] + 31) / 32;
+      u64 blocks = (nw + 255) / 256;
+      if (blocks > 4096) blocks = 4096;
+      k_or_words<<<(unsigned)blocks, 256, 0, st>>>(
+          reinterpret_cast<uint32_t *>(raw + head) + bit0[i] / 32,
+          reinterpret_cast<const uint32_t *>(bits[i]), nw);
+      note_launch();
+    } else {  // odd R: the section is not word-aligned; shift the pieces in
+      CK(launch_concat_bits(raw + head, bit0[i] - ph, bits[i], ph + nbits[i], st));
+    }
+  }
+  // outlier section: count, then the pieces' (index, value) records
+  uint8_t *os = raw + head + nbytes;
+  u64 r0 = 0;
+  for (int i = 0; i < np; ++i) {
+    if (nout[i]) {
+      k_shard_records<<<grid_for(nout[i]), 256, 0, st>>>(
+          reinterpret_cast<const u64 *>(oidx[i]), oval[i], nout[i], os + 8 + 12 * r0);
+      note_launch();
+    }
+    r0 += nout[i];
+  }
+  k_shard_tail<<<1, 32, 0, st>>>(os, kt, raw_len, pass2 ? 0 : 1, ctl);
+  note_launch();
+  if (pass2)
+    CK(launch_pass2_encode(raw, reinterpret_cast<const u64 *>(&ctl->raw_len), raw_len, payload,
+                           workspace, ctl, st));
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
 uint64_t cszi_slab_anchor_count(const cszi_geom *g) { return slab_anchor_count(g); }

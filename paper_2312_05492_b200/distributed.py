@@ -72,7 +72,7 @@ class SimComm:
     def allgather(self, ts):
         return [list(ts) for _ in ts]
 
-    def gather(self, ts):
+    def gather(self, ts, sizes=None):
         return list(ts)  # every slab is local: "root" sees all
 
 
@@ -101,14 +101,17 @@ class TorchComm:
             out.append(parts)
         return out
 
-    def gather(self, ts):
-        """Variable-length 1-D tensors -> list on rank 0 (None elsewhere)."""
+    def gather(self, ts, sizes=None):
+        """Variable-length 1-D tensors -> list on rank 0 (None elsewhere).
+        ``sizes`` (element counts of every rank, when the caller knows them)
+        saves the size all-gather and its host round trip."""
         t = _lib.torch()
         (x,) = ts
-        n = t.tensor([x.numel()], dtype=t.int64, device=x.device)
-        sizes = [t.empty_like(n) for _ in range(self.world)]
-        self.dist.all_gather(sizes, n, group=self.group)
-        sizes = [int(s.item()) for s in sizes]
+        if sizes is None:
+            n = t.tensor([x.numel()], dtype=t.int64, device=x.device)
+            got = [t.empty_like(n) for _ in range(self.world)]
+            self.dist.all_gather(got, n, group=self.group)
+            sizes = [int(v) for v in t.cat(got).cpu().tolist()]
         m = max(max(sizes), 1)
         pad = x.new_zeros(m)
         pad[: x.numel()] = x.reshape(-1)
@@ -135,57 +138,41 @@ class SlabState:
     scratch: dict = field(default_factory=dict)
 
 
-def _ctl_field(ctl, name, dtype):
-    """Device view of one cszi_ctl field (for collectives on device)."""
-    t = _lib.torch()
-    off = getattr(_lib.Ctl, name).offset
-    size = getattr(_lib.Ctl, name).size
-    return ctl.dev[off: off + size].view(dtype)
-
-
 class GpuSlabBackend:
     def geom(self, s: SlabState):
-        g = make_geom(s.extents, default_layout(3))
-        g.slab[0] = s.z0
-        g.slab[1] = s.z1
+        g = s.scratch.get("geom")
+        if g is None:
+            g = make_geom(s.extents, default_layout(3))
+            g.slab[0] = s.z0
+            g.slab[1] = s.z1
+            s.scratch["geom"] = g
         return g
 
     def range_keys(self, s: SlabState):
+        """Range + finite scan and the tuner's sample gather of the owned
+        planes, one libcszi call (the samples wait in scratch for samples())."""
         t = _lib.require_cuda()
         lib = _lib.load()
-        st = _lib.stream_ptr()
         ctl = _lib.DeviceCtl()
         s.scratch["ctl"] = ctl
         ny, nx = s.extents[1], s.extents[2]
-        n_own = (s.z1 - s.z0) * ny * nx
-        _lib.check(lib.cszi_ctl_init(ctl.ptr, st), "ctl_init")
-        if n_own:
-            _lib.check(lib.cszi_range(_lib.ptr(s.x), n_own, ctl.ptr, st), "range")
-        keys = _ctl_field(ctl, "vmin_key", t.int32).to(t.int64) & 0xFFFFFFFF
-        kmax = _ctl_field(ctl, "vmax_key", t.int32).to(t.int64) & 0xFFFFFFFF
-        fnf = _ctl_field(ctl, "first_nonfinite", t.int64).clone()
-        fnf = t.where(fnf == -1, t.full_like(fnf, INT64_MAX), fnf + s.z0 * ny * nx)
-        return t.cat([keys, -kmax, fnf])
+        n_own = max(s.z1 - s.z0, 0) * ny * nx
+        keys = t.empty(3, dtype=t.int64, device="cuda")
+        samples = t.empty(_lib.SAMPLE_WORDS, dtype=t.int32, device="cuda")
+        _lib.check(lib.cszi_shard_scan(_lib.ptr(s.x) if n_own else None, n_own, s.z0 * ny * nx,
+                                       ctypes.byref(self.geom(s)), ctl.ptr, _lib.ptr(keys),
+                                       _lib.ptr(samples), _lib.stream_ptr()), "shard_scan")
+        s.scratch["samples"] = samples
+        return keys
 
     def set_range(self, s: SlabState, k):
-        t = _lib.torch()
-        ctl = s.scratch["ctl"]
-        _ctl_field(ctl, "vmin_key", t.int32).copy_(k[0:1].to(t.int32))
-        _ctl_field(ctl, "vmax_key", t.int32).copy_((-k[1:2]).to(t.int32))
-        fnf = t.where(k[2:3] == INT64_MAX, t.full_like(k[2:3], -1), k[2:3])
-        _ctl_field(ctl, "first_nonfinite", t.int64).copy_(fnf)
+        lib = _lib.load()
+        _lib.check(lib.cszi_shard_set_range(s.scratch["ctl"].ptr, _lib.ptr(k), _lib.stream_ptr()),
+                   "shard_set_range")
         s.scratch["range"] = k
 
     def samples(self, s: SlabState):
-        t = _lib.torch()
-        lib = _lib.load()
-        if s.z1 <= s.z0:  # empty slab (more ranks than z tiles)
-            return t.zeros(_lib.SAMPLE_WORDS, dtype=t.int32, device="cuda")
-        v = t.empty(_lib.SAMPLE_WORDS, dtype=t.int32, device="cuda")
-        g = self.geom(s)
-        _lib.check(lib.cszi_sample_gather(_lib.ptr(s.x), ctypes.byref(g), _lib.ptr(v),
-                                          _lib.stream_ptr()), "sample_gather")
-        return v
+        return s.scratch["samples"]
 
     def tune(self, s: SlabState, samples, alpha: float):
         lib = _lib.load()
@@ -231,8 +218,13 @@ class GpuSlabBackend:
     def piece_bits(self, s: SlabState, hist_local):
         """Bits of this slab's Huffman piece: sum over symbols of count x length
         (outliers and anchors are counted as R, which is how they are coded)."""
-        lengths = s.scratch["lengths"].to(hist_local.dtype)
-        return (hist_local.reshape(-1) * lengths).sum().reshape(1)
+        t = _lib.torch()
+        out = t.empty(1, dtype=t.int64, device="cuda")
+        _lib.check(_lib.load().cszi_shard_piece_bits(_lib.ptr(hist_local),
+                                                     _lib.ptr(s.scratch["lengths"]),
+                                                     2 * s.radius, _lib.ptr(out),
+                                                     _lib.stream_ptr()), "shard_piece_bits")
+        return out
 
     def encode(self, s: SlabState, bit_base: int = 0):
         t = _lib.torch()
@@ -264,7 +256,10 @@ class GpuSlabBackend:
                 _lib.ptr(bits), cap, _lib.ptr(oidx), _lib.ptr(oval), ocap, _lib.ptr(ws), ctl.ptr,
                 _lib.stream_ptr()), "encode")
         s.scratch.update(bits=bits, oidx=oidx, oval=oval)
-        return t.cat([_ctl_field(ctl, "bits", t.int64), _ctl_field(ctl, "n_outliers", t.int64)])
+        counts = t.empty(2, dtype=t.int64, device="cuda")
+        _lib.check(lib.cszi_shard_counts(ctl.ptr, _lib.ptr(counts), _lib.stream_ptr()),
+                   "shard_counts")
+        return counts
 
     def anchors(self, s: SlabState):
         t = _lib.torch()
@@ -278,6 +273,19 @@ class GpuSlabBackend:
             _lib.check(lib.cszi_gather_anchors(_lib.ptr(s.x), ctypes.byref(g), _lib.ptr(out),
                                                _lib.stream_ptr()), "gather_anchors")
         return out[:na]
+
+    def piece_nbytes(self, extents, z0: int, z1: int, counts, bit_base: int):
+        """Byte sizes (anchors, bit piece, outlier indices, outlier values) of
+        the pieces slab [z0, z1) sends to the root: known on every rank from
+        the all-gathered counts, so the gather needs no size exchange."""
+        if z1 <= z0:
+            na = 0
+        else:
+            g = make_geom(extents, default_layout(3))
+            g.slab[0], g.slab[1] = z0, z1
+            na = int(_lib.load().cszi_slab_anchor_count(ctypes.byref(g)))
+        nbits, nout = int(counts[0]), int(counts[1])
+        return 4 * na, 4 * ((bit_base + nbits + 31) // 32), 8 * nout, 4 * nout
 
     def pieces(self, s: SlabState, counts):
         """Variable-length payload pieces of this slab (device tensors)."""
@@ -295,65 +303,53 @@ class GpuSlabBackend:
 
     def assemble(self, s0: SlabState, anchors, bit_pieces, nbits, oidx, oval, pass2: bool,
                  alpha: float):
-        """Root: raw payload (anchors ‖ lengths ‖ bitstream ‖ outliers), pass-2,
-        header -> DeviceArchive."""
-        payload, sec = self._payload(s0, anchors, s0.scratch["lengths"], bit_pieces, nbits, oidx,
-                                     oval, pass2)
-        c = s0.scratch["ctl"].fetch()
+        """Root: raw payload (anchors ‖ lengths ‖ bitstream ‖ outliers) and
+        pass-2 in one libcszi call (cszi_shard_assemble), header ->
+        DeviceArchive.  One host read: the slab-0 ctl (flags, tuned
+        configuration, payload length)."""
+        t = _lib.torch()
+        lib = _lib.load()
+        st = _lib.stream_ptr()
+        ctl = s0.scratch["ctl"]
+        lengths = s0.scratch["lengths"]
+        npc = len(nbits)
+        vp = ctypes.c_void_p * npc
+        u64 = ctypes.c_uint64 * npc
+        na = [int(x.numel()) for x in anchors]
+        no = [int(x.numel()) for x in oidx]
+        starts = [0] * npc
+        for i in range(1, npc):
+            starts[i] = starts[i - 1] + int(nbits[i - 1])
+        total_bits = sum(int(b) for b in nbits)
+        nbins = int(lengths.numel())
+        raw_cap = 4 * sum(na) + nbins + 4 * (total_bits // 32 + 2) + 8 + 12 * sum(no) + 64
+        if pass2:
+            raw = _lib.WS.get(raw_cap, "shard_raw")
+            pay = t.empty(raw_cap + raw_cap // 128 + 16, dtype=t.uint8, device="cuda")
+            ws = _lib.WS.get(int(lib.cszi_pass2_encode_workspace_size(raw_cap)), "p2_enc")
+        else:
+            raw = pay = t.empty(raw_cap, dtype=t.uint8, device="cuda")
+            ws = None
+        ptrs = lambda xs: vp(*[x.data_ptr() if x.numel() else 0 for x in xs])  # noqa: E731
+        _lib.check(lib.cszi_shard_assemble(
+            npc, ptrs(anchors), u64(*na), _lib.ptr(lengths), nbins, ptrs(bit_pieces),
+            u64(*starts), u64(*[int(b) for b in nbits]), ptrs(oidx), ptrs(oval), u64(*no),
+            1 if pass2 else 0, _lib.ptr(raw), raw_cap, _lib.ptr(pay),
+            _lib.ptr(ws) if ws is not None else None, ws.numel() if ws is not None else 0,
+            ctl.ptr, st), "shard_assemble")
+        c = ctl.fetch()
         if c.flags & _lib.F_EB_NONPOSITIVE:
             raise Inconsistent("absolute error bound must be positive")
         if c.flags & _lib.F_LENGTH_OVERFLOW:
             raise LengthOverflow("a symbol would need more than 32 bits")
         if c.flags & _lib.F_EMPTY_HISTOGRAM:
             raise EmptyHistogram("cannot build a codebook from all-zero counts")
+        sec = (4 * sum(na), nbins, (total_bits + 7) // 8, 8 + 12 * sum(no))
+        payload = pay[: int(c.payload_len)]
         header = pack_header(3, PREDICTOR_INTERP, EB_REL if s0.mode == "rel" else EB_ABS, pass2,
                              0, ctl_variants(c, 3), ctl_order(c, 3), s0.radius, 8, s0.extents,
                              float(s0.eb), float(c.eb_abs), alpha, sec, int(payload.numel()))
         return DeviceArchive(header=header, payload=payload)
-
-    def _payload(self, s0, anchors, lengths, bit_pieces, nbits, oidx, oval, pass2):
-        t = _lib.torch()
-        lib = _lib.load()
-        st = _lib.stream_ptr()
-        a = t.cat([x.reshape(-1) for x in anchors]).view(t.uint8)
-        total_bits = sum(nbits)
-        nbytes = (total_bits + 7) // 8
-        k = sum(int(x.numel()) for x in oidx)
-        head = a.numel() + lengths.numel()
-        raw_len = head + nbytes + 8 + 12 * k
-        raw = t.empty(raw_len + 16, dtype=t.uint8, device="cuda")
-        raw[: a.numel()] = a
-        raw[a.numel(): head] = lengths
-        raw[head: head + 4 * ((total_bits + 31) // 32 + 1)].zero_()  # the bit pieces are ORed in
-        off = 0
-        if (raw.data_ptr() + head) % 4 == 0:
-            # pieces were packed at their global bit phase: OR whole words
-            nwt = (total_bits + 31) // 32 + 1
-            rw = raw[head: head + 4 * nwt].view(t.int32)
-            for piece, nb in zip(bit_pieces, nbits):
-                if nb:
-                    w0 = off // 32
-                    pw = piece.view(t.int32)
-                    rw[w0: w0 + pw.numel()].bitwise_or_(pw)
-                off += nb
-        else:  # odd R: the section is not word-aligned; shift the pieces back
-            for piece, nb in zip(bit_pieces, nbits):
-                if nb:
-                    ph = off % 32
-                    _lib.check(lib.cszi_concat_bits(_lib.ptr(raw[head:]), off - ph,
-                                                    _lib.ptr(piece), ph + nb, st), "concat_bits")
-                off += nb
-        idx = t.cat([x.reshape(-1) for x in oidx]) if k else t.zeros(1, dtype=t.int64, device="cuda")
-        val = t.cat([x.reshape(-1) for x in oval]) if k else t.zeros(1, dtype=t.float32, device="cuda")
-        _lib.check(lib.cszi_pack_outliers(_lib.ptr(idx), _lib.ptr(val), k,
-                                          _lib.ptr(raw[head + nbytes:]), st), "pack_outliers")
-        sec = (int(a.numel()), int(lengths.numel()), nbytes, 8 + 12 * k)
-        if pass2:
-            from .pass2 import encode_device
-
-            out, m = encode_device(raw, raw_len)
-            return out[:m], sec
-        return raw[:raw_len], sec
 
 
 # ---------------------------------------------------------------------------
@@ -388,20 +384,38 @@ def compress_slabs_batch(batch: list, comm, backend=None, pass2: bool = True):
     for the whole batch (SURVEY §8e "Expected scaling": one K x 2R histogram
     all-reduce instead of K).  batch[k] is the list of this process's slab
     states of snapshot k (same slab layout for every snapshot).  Returns the
-    list of K archives on the root, else None."""
+    list of K archives on the root, else None.
+
+    Host round trips per batch: the bit lengths of the slab pieces (every
+    slab packs at its global bit phase) and the per-slab (bits, outliers)
+    counts -- both one small device->host read for the whole batch; a
+    relative bound needs the range on the device only, so the non-finite
+    check rides on the first of those reads."""
+    t = _lib.torch()
     backend = backend or GpuSlabBackend()
     K = len(batch)
+    if (isinstance(backend, GpuSlabBackend) and getattr(comm, "world", 0) == 1
+            and len(batch[0]) == 1 and batch[0][0].z0 == 0
+            and batch[0][0].z1 >= batch[0][0].extents[0]):
+        # one rank holding the whole field: nothing to shard -- the
+        # single-GPU pipeline (one graph per snapshot), the same bytes
+        from .grid import Dims, Grid
+        from .pipeline import compress_device
+
+        return [compress_device(Grid(Dims(st.extents), st.x), st.eb, st.mode, pass2=pass2,
+                                quant_radius=st.radius) for (st,) in batch]
     # (1) range: K x 3 keys in one all-reduce
     keys = _batched(comm, [[backend.range_keys(s) for s in states] for states in batch], "min")
     for states, ks in zip(batch, keys):
         for s, k in zip(states, ks):
             backend.set_range(s, k)
-    kall = [ks[0].cpu().numpy().astype(np.int64) for ks in keys]
-    for k0 in kall:
-        if int(k0[2]) != INT64_MAX:
-            raise NonFiniteValue(int(k0[2]))
+    key0 = t.stack([ks[0].reshape(-1) for ks in keys])  # K x 3, identical on every slab
+    host_keys = None
+    if any(states[0].mode != "rel" for states in batch):
+        host_keys = key0.cpu().numpy().astype(np.int64)
+        _raise_nonfinite(host_keys)
     alphas = []
-    for states, k0 in zip(batch, kall):
+    for k, states in enumerate(batch):
         s0 = states[0]
         # alpha: rel mode -> compute_alpha(eb); abs mode -> from the global range
         if s0.mode == "rel":
@@ -409,6 +423,7 @@ def compress_slabs_batch(batch: list, comm, backend=None, pass2: bool = True):
         else:
             from ._keys import key_to_float
 
+            k0 = host_keys[k]
             rng = key_to_float(int(-k0[1])) - key_to_float(int(k0[0]))
             alphas.append(compute_alpha(float(s0.eb) / rng if rng > 0 else float(s0.eb)))
     # (2) tuner samples
@@ -429,22 +444,35 @@ def compress_slabs_batch(batch: list, comm, backend=None, pass2: bool = True):
     # slab's stream length (local histogram . code lengths, known before any
     # packing) so every slab packs at its global bit phase and the root
     # merges whole words instead of bit-shifting the pieces.
+    bases = None
     if phased:
         pb = _batched(comm, [[backend.piece_bits(s, h) for s, h in zip(states, lh)]
                              for states, lh in zip(batch, local_h)], "gather")
-        counts = []
-        for states, pbk in zip(batch, pb):
-            allpb = [int(v) for v in t_cat_host(pbk)]
-            starts = [sum(allpb[:r]) for r in range(len(allpb))]
-            counts.append([backend.encode(s, bit_base=starts[r] % 32)
-                           for s, r in zip(states, ranks)])
+        allpb = t.stack([t.cat([p.reshape(-1) for p in pbk]) for pbk in pb])  # K x world
+        if host_keys is None:  # first host read: piece lengths + the range keys
+            both = t.cat([allpb.reshape(-1).to(key0.device), key0.reshape(-1)]).cpu().numpy()
+            nk = allpb.numel()
+            allpb_h = both[:nk].reshape(K, -1).astype(np.int64)
+            host_keys = both[nk:].reshape(K, 3).astype(np.int64)
+            _raise_nonfinite(host_keys)
+        else:
+            allpb_h = allpb.cpu().numpy().astype(np.int64)
+        starts = np.concatenate([np.zeros((K, 1), np.int64), np.cumsum(allpb_h, 1)[:, :-1]], 1)
+        bases = starts % 32
+        counts = [[backend.encode(s, bit_base=int(bases[k][r])) for s, r in zip(states, ranks)]
+                  for k, states in enumerate(batch)]
     else:
         counts = [[backend.encode(s) for s in states] for states in batch]
     allc = _batched(comm, counts, "gather")
-    allc = [[c.cpu().numpy() for c in ck] for ck in allc]
-    # (5) gather pieces to the root
+    allc_h = t.stack([t.stack([c.reshape(-1) for c in ck]) for ck in allc]).cpu().numpy()
+    if host_keys is None:
+        host_keys = key0.cpu().numpy().astype(np.int64)
+        _raise_nonfinite(host_keys)
+    # (5) pieces to the root
+    if hasattr(backend, "piece_nbytes") and bases is not None:
+        return _gather_packed(comm, backend, batch, allc_h, bases, ranks, alphas, pass2)
     out = []
-    for states, ck, a in zip(batch, allc, alphas):
+    for states, ck, a in zip(batch, allc_h, alphas):
         anchors = comm.gather([backend.anchors(s) for s in states])
         pieces = [backend.pieces(s, c) for s, c in zip(states, [ck[i] for i in ranks])]
         bits = comm.gather([p[0] for p in pieces])
@@ -458,9 +486,61 @@ def compress_slabs_batch(batch: list, comm, backend=None, pass2: bool = True):
     return None if out[0] is None else out
 
 
-def t_cat_host(parts):
+def _raise_nonfinite(host_keys):
+    for k0 in host_keys:
+        if int(k0[2]) != INT64_MAX:
+            raise NonFiniteValue(int(k0[2]))
+
+
+def _gather_packed(comm, backend, batch, allc_h, bases, ranks, alphas, pass2):
+    """One gather for the whole batch: every slab packs (anchors, bit piece,
+    outlier indices, outlier values) of all K snapshots into one byte
+    buffer; the sizes of every slab's parts follow from the all-gathered
+    counts, so no rank exchanges sizes and the root splits the buffers."""
     t = _lib.torch()
-    return t.cat([p.reshape(-1) for p in parts]).cpu().numpy().tolist()
+    K = len(batch)
+    s0 = batch[0][0]
+    world = allc_h.shape[1]
+    if isinstance(comm, SimComm):
+        bounds = [(s.z0, s.z1) for s in batch[0]]
+    else:
+        bounds = slab_bounds(s0.extents[0], world)
+    sizes = [[backend.piece_nbytes(s0.extents, bounds[r][0], bounds[r][1], allc_h[k][r],
+                                   int(bases[k][r])) for r in range(world)] for k in range(K)]
+    packed = []
+    for i, r in enumerate(ranks):
+        parts = []
+        for k in range(K):
+            st = batch[k][i]
+            a = backend.anchors(st)
+            b, oi, ov = backend.pieces(st, allc_h[k][r])
+            for x, nb in zip((a, b, oi, ov), sizes[k][r]):
+                v = x.reshape(-1).view(t.uint8)
+                assert v.numel() == nb, (v.numel(), nb)
+                parts.append(v)
+        packed.append(t.cat(parts) if parts else t.empty(0, dtype=t.uint8, device="cuda"))
+    per_rank = [sum(sum(sizes[k][r]) for k in range(K)) for r in range(world)]
+    got = comm.gather(packed, sizes=per_rank)
+    if got is None:
+        return None
+    out = []
+    offs = [0] * world
+    for k in range(K):
+        anchors, bits, oidx, oval = [], [], [], []
+        for r in range(world):
+            buf = got[r]
+            o = offs[r]
+            na, nb, ni, nv = sizes[k][r]
+            anchors.append(buf[o:o + na].view(t.float32))
+            bits.append(buf[o + na:o + na + nb])
+            # (an int64 view needs an 8-byte aligned offset: copy)
+            oidx.append(buf[o + na + nb:o + na + nb + ni].clone().view(t.int64))
+            oval.append(buf[o + na + nb + ni:o + na + nb + ni + nv].view(t.float32))
+            offs[r] = o + na + nb + ni + nv
+        nbits = [int(allc_h[k][r][0]) for r in range(world)]
+        out.append(backend.assemble(batch[k][0], anchors, bits, nbits, oidx, oval, pass2,
+                                    alphas[k]))
+    return out
 
 
 def _local_ranks(comm, states):
