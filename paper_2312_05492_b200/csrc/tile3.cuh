@@ -730,6 +730,7 @@ struct Cfg {  // tuned configuration (per-CTA / per-warp copy)
   Lv lv[3];
   int order[3];
   int nak[3];
+  int pc[3];  // interior pass codes (tile3i.cuh pass_codes)
 };
 
 template <int MODE, bool BND>
@@ -974,6 +975,8 @@ __global__ void __launch_bounds__(NT, 3)
   if (G.hist_smem)
     for (int i = threadIdx.x; i < 2 * R; i += NT) hs[i] = 0;
   __syncthreads();  // cfg, hist, mbarrier init visible
+  if (threadIdx.x == 0) pass_codes(C.order, C.nak, C.pc);
+  __syncthreads();
   const Out O{nullptr, nullptr, 0};
   const bool exact = G.exact != 0;
   const uint32_t rr = (uint32_t)R | ((uint32_t)R << 16);
@@ -1186,6 +1189,8 @@ __global__ void __launch_bounds__(NT, 3)
     C.order[i] = lc.order[i];
     C.nak[i] = lc.variant[i] == 0;
   }
+  __syncthreads();
+  if (threadIdx.x == 0) pass_codes(C.order, C.nak, C.pc);
   __syncthreads();
   const Out O{out_idx, out_val, nout_dev ? *nout_dev : n_out};
   const int64_t pz = (int64_t)G.ext[1] * G.ext[2];

@@ -338,6 +338,65 @@ DEV void iwalk_col(const Tile &T, double wo, double wi, const Lv &L, int R, cons
   }
 }
 
+// Pass code of the i-th pass of a level (the same at every level): axis D,
+// which other axes were passed before it, the cubic variant of D.
+//   pc = 8 D + 2 sel + nak, sel = passed & 3 for D = x, else (x passed) * 2 +
+//   (the other non-x axis passed).
+// Computed once per CTA (pass_codes), so a pass dispatches with one shared
+// load and one jump table (ipass_pc) instead of a chain of dependent tests.
+DEV void pass_codes(const int order[3], const int nak[3], int pc[3]) {
+  int passed = 0;
+  for (int i = 0; i < 3; ++i) {
+    const int D = order[i];
+    int sel;
+    if (D == 2) {
+      sel = passed & 3;
+    } else {
+      const bool xp = (passed & 4) != 0;
+      const bool ap = (passed & (D == 0 ? 2 : 1)) != 0;
+      sel = (xp ? 2 : 0) | (ap ? 1 : 0);
+    }
+    pc[i] = 8 * D + 2 * sel + (nak[D] ? 1 : 0);
+    passed |= 1 << D;
+  }
+}
+
+// One interior pass by pass code.  (wo, wi) are the variant's cubic weights
+// (the exact line redo, fix_line, evaluates the spline with them); below
+// S = 1 the y / z lines hold no cubic point, so their variant is moot.
+template <int MODE, int S>
+DEV void ipass_pc(const Tile &T, int pc, const Lv &L, int R, const Out &O) {
+  constexpr int S2 = 2 * S;
+  constexpr bool CUBIC_ZY = (S == 1);
+#define T3_X(SEL, STZ, STY)                                                                \
+  case 16 + 2 * SEL: iwalk_x<S, STZ, STY, MODE, false>(T, NAT_O, NAT_I, L, R, O); break;   \
+  case 17 + 2 * SEL: iwalk_x<S, STZ, STY, MODE, true>(T, NAK_O, NAK_I, L, R, O); break;
+#define T3_C(DD, SEL, STX, STA)                                                            \
+  case 8 * DD + 2 * SEL:                                                                    \
+    iwalk_col<S, DD, STX, STA, MODE, !CUBIC_ZY>(T, NAT_O, NAT_I, L, R, O);                 \
+    break;                                                                                  \
+  case 8 * DD + 2 * SEL + 1:                                                                \
+    iwalk_col<S, DD, STX, STA, MODE, true>(T, NAK_O, NAK_I, L, R, O);                      \
+    break;
+  switch (pc) {
+    T3_X(0, S2, S2)
+    T3_X(1, S, S2)
+    T3_X(2, S2, S)
+    T3_X(3, S, S)
+    T3_C(0, 0, S2, S2)
+    T3_C(0, 1, S2, S)
+    T3_C(0, 2, S, S2)
+    T3_C(0, 3, S, S)
+    T3_C(1, 0, S2, S2)
+    T3_C(1, 1, S2, S)
+    T3_C(1, 2, S, S2)
+    T3_C(1, 3, S, S)
+    default: break;
+  }
+#undef T3_X
+#undef T3_C
+}
+
 // One interior pass: (S, D, passed) -> walk instantiation.  passed: bit a
 // set when axis a was passed earlier at this level.
 #define T3_NAKSEL(CALL_T, CALL_F) \
@@ -395,16 +454,23 @@ DEV void ipass(const Tile &T, int D, int passed, bool nak, double wo, double wi,
 }
 #undef T3_NAKSEL
 
+// Compress dispatches by pass code (measured: predict 535 -> 525 us on
+// 512^3); the reconstructor keeps the test chain (its jump-table variant
+// measured 20 us slower).
 template <int MODE, int S>
 DEV void ilevel(const Tile &T, const Cfg &C, int lv, int R, const Out &O) {
   const Lv L = C.lv[lv];
   int passed = 0;
 #pragma unroll 1
   for (int i = 0; i < 3; ++i) {
-    const int D = C.order[i];
-    const bool nak = C.nak[D] != 0;
-    ipass<MODE, S>(T, D, passed, nak, nak ? NAK_O : NAT_O, nak ? NAK_I : NAT_I, L, R, O);
-    passed |= 1 << D;
+    if (MODE == 0) {
+      ipass_pc<MODE, S>(T, C.pc[i], L, R, O);
+    } else {
+      const int D = C.order[i];
+      const bool nak = C.nak[D] != 0;
+      ipass<MODE, S>(T, D, passed, nak, nak ? NAK_O : NAT_O, nak ? NAK_I : NAT_I, L, R, O);
+      passed |= 1 << D;
+    }
     __syncwarp();
   }
 }
