@@ -898,25 +898,47 @@ DEV void stage_rows_u16(uint32_t dst, const uint16_t *sym, const Geo &G, const i
 }
 
 // ---------------------------------------------------------------------------
-// dynamic tile queue: tiles are handed out in order by one atomic per tile
-// (edge tiles cost 2-3x an interior tile, so a static split would leave the
-// warps that own them running long after the rest).  Each launch uses one
-// slot of a ring; the last warp out resets its slot for reuse.
+// tile schedule: when interior tiles (uniform cost) make up most of the
+// grid (>= 80%: 512^3 91%, RTM 84%) they are dealt out statically, warp gw
+// taking gw, gw + nw, gw + 2 nw, ... (nw warps in the grid); the rest (the
+// edge shell: tiles cost 2-3x an interior one, and vary; or every tile of
+// an edge-heavy grid such as 33120 x 69 x 69, where the static split
+// measured 7% slower) comes from a dynamic queue, one atomic per tile,
+// requested when a tile starts and read after its passes so the round trip
+// hides under the work.  Each launch uses one slot of a ring; the last warp
+// out resets its slot for reuse.
 // ---------------------------------------------------------------------------
 constexpr int SCHED_SLOTS = 64;
 __device__ unsigned int g_t3_sched[SCHED_SLOTS * 2];
 
-DEV int next_tile(unsigned int *q) {
+struct Sched {
+  unsigned int *q;
+  int gw, nw, nint;  // nint: tiles dealt statically (the interior, or none)
+};
+DEV Sched sched_init(unsigned int *q, int nint, int ntiles) {
+  Sched S;
+  S.q = q;
+  S.gw = (int)(blockIdx.x * NW + (threadIdx.x >> 5));
+  S.nw = (int)(gridDim.x * NW);
+  S.nint = ((int64_t)nint * 5 >= (int64_t)ntiles * 4) ? nint : 0;
+  return S;
+}
+DEV int next_tile(const Sched &S) {
+  if (S.gw < S.nint) return S.gw;
   int t = 0;
-  if ((threadIdx.x & 31) == 0) t = (int)atomicAdd(q, 1u);
-  return __shfl_sync(CSZI_FULL, t, 0);
+  if ((threadIdx.x & 31) == 0) t = (int)atomicAdd(S.q, 1u);
+  return S.nint + __shfl_sync(CSZI_FULL, t, 0);
 }
-// split form: the ticket is requested when a tile starts and read after its
-// passes, so the atomic's round trip hides under the tile's work
-DEV unsigned int ticket_issue(unsigned int *q) {
-  return ((threadIdx.x & 31) == 0) ? atomicAdd(q, 1u) : 0u;
+// the tile after t: static while the interior lasts, else a queue ticket
+// (bit 31 marks a static successor)
+DEV unsigned int ticket_issue(const Sched &S, int t) {
+  if (t < S.nint && t + S.nw < S.nint) return 0x80000000u | (unsigned)(t + S.nw);
+  return ((threadIdx.x & 31) == 0) ? atomicAdd(S.q, 1u) : 0u;
 }
-DEV int ticket_read(unsigned int raw) { return (int)__shfl_sync(CSZI_FULL, raw, 0); }
+DEV int ticket_read(const Sched &S, unsigned int raw) {
+  const unsigned int v = __shfl_sync(CSZI_FULL, raw, 0);
+  return (v & 0x80000000u) ? (int)(v & 0x7fffffffu) : S.nint + (int)v;
+}
 DEV void sched_done(unsigned int *q) {
   if ((threadIdx.x & 31) == 0) {
     __threadfence();
@@ -952,7 +974,8 @@ __global__ void __launch_bounds__(NT, 3)
   const int nint = tile_count<false>(G);
   const int ntiles = nint + tile_count<true>(G);
   unsigned int *q = g_t3_sched + 2 * slot;
-  int t = next_tile(q);
+  const Sched S = sched_init(q, nint, ntiles);
+  int t = next_tile(S);
   if (lane == 0) mbar_init(&mbar[warp]);
   __syncwarp();
   int o[3] = {0, 0, 0};  // origin of tile t (carried from the prefetch)
@@ -1014,12 +1037,12 @@ __global__ void __launch_bounds__(NT, 3)
     }
     __syncwarp();
     T3P_CLOCK(c2);
-    const unsigned int raw = ticket_issue(q);
+    const unsigned int raw = ticket_issue(S, t);
     if (T.bnd || exact) run_levels<0, true>(T, C, R, exact, O);
     else run_levels_i<0>(T, C, R, O);
     T3P_CLOCK(c3);
     // staging buffer free: prefetch the next tile
-    const int tn = ticket_read(raw);
+    const int tn = ticket_read(S, raw);
     int on[3] = {0, 0, 0};
     if (tn < ntiles) {
       tile_of(G, nint, tn, on);
@@ -1168,7 +1191,8 @@ __global__ void __launch_bounds__(NT, 3)
   const int nint = tile_count<false>(G);
   const int ntiles = nint + tile_count<true>(G);
   unsigned int *q = g_t3_sched + 2 * slot;
-  int t = next_tile(q);
+  const Sched S = sched_init(q, nint, ntiles);
+  int t = next_tile(S);
   if (lane == 0) mbar_init(&mbar[warp]);
   __syncwarp();
   int o[3] = {0, 0, 0};  // origin of tile t (carried from the prefetch)
@@ -1234,10 +1258,10 @@ __global__ void __launch_bounds__(NT, 3)
       stage_rows_u16(syms, sym, G, o);
     }
     __syncwarp();
-    const unsigned int raw = ticket_issue(q);
+    const unsigned int raw = ticket_issue(S, t);
     if (T.bnd) run_levels<1, true>(T, C, R, false, O);
     else run_levels_i<1>(T, C, R, O);
-    const int tn = ticket_read(raw);
+    const int tn = ticket_read(S, raw);
     int on[3] = {0, 0, 0};
     if (tn < ntiles) {
       tile_of(G, nint, tn, on);
