@@ -55,8 +55,23 @@ constexpr int CP = 36;                          // code row pitch (u16)
 constexpr int NCODE = TZ * TY * CP;             // 2304 u16
 constexpr int SP = 40;                          // symbol row pitch (u16, TMA box x)
 constexpr int NSYM = CZ * CY * SP;              // 3240 u16
-constexpr int NW = 4;                           // warps (tiles) per CTA
+#ifndef T3R_NW
+#define T3R_NW 4
+#endif
+constexpr int NW = T3R_NW;                      // warps (tiles) per CTA (reconstruct)
 constexpr int NT = NW * 32;
+constexpr int MINB_R = (NW <= 4) ? 12 / NW : 1;
+#ifndef T3P_NW
+#define T3P_NW 12
+#endif
+constexpr int NWP = T3P_NW;                     // warps per CTA of the predictor
+constexpr int NTP = NWP * 32;
+#ifdef T3P_REGS
+#define T3P_BOUNDS __maxnreg__(T3P_REGS)
+#else
+#define T3P_BOUNDS __launch_bounds__(NTP, MINB_P)
+#endif
+constexpr int MINB_P = (NWP <= 4) ? 12 / NWP : 1;  // resident CTAs per SM (launch bounds)
 // per-warp shared regions (128-byte aligned for the TMA destinations)
 constexpr int BUF_BYTES = NBUF * 4;                              // 11664
 constexpr int NZ_BYTES = TZ * TY * 4;  // non-R bitmap words of a tile's rows
@@ -918,8 +933,8 @@ struct Sched {
 DEV Sched sched_init(unsigned int *q, int nint, int ntiles) {
   Sched S;
   S.q = q;
-  S.gw = (int)(blockIdx.x * NW + (threadIdx.x >> 5));
-  S.nw = (int)(gridDim.x * NW);
+  S.gw = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+  S.nw = (int)(gridDim.x * (blockDim.x >> 5));
   S.nint = ((int64_t)nint * 5 >= (int64_t)ntiles * 4) ? nint : 0;
   return S;
 }
@@ -942,7 +957,7 @@ DEV int ticket_read(const Sched &S, unsigned int raw) {
 DEV void sched_done(unsigned int *q) {
   if ((threadIdx.x & 31) == 0) {
     __threadfence();
-    if (atomicAdd(q + 1, 1u) == gridDim.x * NW - 1) {
+    if (atomicAdd(q + 1, 1u) == gridDim.x * (blockDim.x >> 5) - 1) {
       q[0] = 0;
       q[1] = 0;
       __threadfence();
@@ -956,18 +971,18 @@ DEV void sched_done(unsigned int *q) {
 // issued as soon as the passes release the staging buffer, so it overlaps
 // the epilogue (code store / histogram, or the float store).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT, 3)
+__global__ void T3P_BOUNDS
     k_t3_predict(const __grid_constant__ CUtensorMap tm, const float *__restrict__ x, Geo G,
                  const cszi_ctl *__restrict__ ctl, uint16_t *__restrict__ sym,
                  u64 *__restrict__ hist, uint32_t *__restrict__ nzmap, int slot) {
   extern __shared__ __align__(128) unsigned char t3_smem[];
   __shared__ Cfg C;
-  __shared__ uint64_t mbar[NW];
-  __shared__ uint32_t zero_ws[NW];
+  __shared__ uint64_t mbar[NWP];
+  __shared__ uint32_t zero_ws[NWP];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int R = G.R;
   unsigned char *sm = align128(t3_smem);
-  uint32_t *hs = reinterpret_cast<uint32_t *>(sm + NW * P_WARP);
+  uint32_t *hs = reinterpret_cast<uint32_t *>(sm + NWP * P_WARP);
   const uint32_t buf = smem_u32(sm + warp * P_WARP);
   const uint32_t codes = buf + BUF_BYTES;
   uint32_t *nzs = reinterpret_cast<uint32_t *>(sm + warp * P_WARP + BUF_BYTES + NCODE * 2);
@@ -996,7 +1011,7 @@ __global__ void __launch_bounds__(NT, 3)
     C.nak[i] = ctl->variant[i] == 0;
   }
   if (G.hist_smem)
-    for (int i = threadIdx.x; i < 2 * R; i += NT) hs[i] = 0;
+    for (int i = threadIdx.x; i < 2 * R; i += NTP) hs[i] = 0;
   __syncthreads();  // cfg, hist, mbarrier init visible
   if (threadIdx.x == 0) pass_codes(C.order, C.nak, C.pc);
   __syncthreads();
@@ -1158,11 +1173,11 @@ __global__ void __launch_bounds__(NT, 3)
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t z = 0;
-    for (int w = 0; w < NW; ++w) z += zero_ws[w];
+    for (int w = 0; w < NWP; ++w) z += zero_ws[w];
     if (z) atomicAdd(&hist[R], (u64)z);
   }
   if (G.hist_smem)
-    for (int i = threadIdx.x; i < 2 * R; i += NT)
+    for (int i = threadIdx.x; i < 2 * R; i += NTP)
       if (hs[i]) atomicAdd(&hist[i], (u64)hs[i]);
 }
 
@@ -1175,7 +1190,7 @@ DEV float anchor_i(const float *anchors, const Geo &G, const int o[3], int lane)
   return __ldg(anchors + (kz * G.na1 + ky) * G.na2 + kx);
 }
 
-__global__ void __launch_bounds__(NT, 3)
+__global__ void __launch_bounds__(NT, MINB_R)
     k_t3_reconstruct(const __grid_constant__ CUtensorMap tm, const uint16_t *__restrict__ sym,
                      const float *__restrict__ anchors, const u64 *out_idx,
                      const float *out_val, u64 n_out, const u64 *nout_dev, Geo G, LevelCfg lc,
@@ -1352,9 +1367,9 @@ static bool make_tmap(CUtensorMap *tm, const void *base, CUtensorMapDataType dt,
 }
 
 // resident CTAs x SMs, capped by the tile count
-static unsigned persistent_grid(const void *k, size_t smem, int64_t ntiles) {
-  const int sms = sm_count(), per = occupancy(k, NT, smem);
-  const int64_t need = (ntiles + NW - 1) / NW;
+static unsigned persistent_grid(const void *k, size_t smem, int64_t ntiles, int nw = NW) {
+  const int sms = sm_count(), per = occupancy(k, nw * 32, smem);
+  const int64_t need = (ntiles + nw - 1) / nw;
   const int64_t cap = (int64_t)per * sms;
   return (unsigned)(need < cap ? need : cap);
 }
@@ -1432,10 +1447,10 @@ int launch_predict_t3(const float *x, const cszi_geom *g, int32_t radius,
               : 0;
   const int64_t nall = (int64_t)G.nt[0] * G.nt[1] * G.nt[2];
   const size_t smem =
-      128 + (size_t)NW * P_WARP + (G.hist_smem ? sizeof(uint32_t) * 2 * radius : 0);
+      128 + (size_t)NWP * P_WARP + (G.hist_smem ? sizeof(uint32_t) * 2 * radius : 0);
   ensure_smem((const void *)k_t3_predict, smem);
-  const unsigned grid = persistent_grid((const void *)k_t3_predict, smem, nall);
-  k_t3_predict<<<grid, NT, smem, st>>>(tm, x, G, ctl, sym, hist, nzmap, sched_slot());
+  const unsigned grid = persistent_grid((const void *)k_t3_predict, smem, nall, NWP);
+  k_t3_predict<<<grid, NTP, smem, st>>>(tm, x, G, ctl, sym, hist, nzmap, sched_slot());
   note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
