@@ -284,6 +284,43 @@ int cszi_shard_piece_bits(const uint64_t *hist, const uint8_t *lengths, int32_t 
                           int64_t *out, void *stream);
 int cszi_shard_counts(const cszi_ctl *ctl, int64_t *out, void *stream);
 
+/* ---- sharded decompress split by Huffman chunk ranges -------
+ * The stages of cszi_decompress over one workspace of
+ * cszi_decompress_workspace_size bytes (same arguments throughout; g->slab
+ * = the rank's z-slab):
+ *   cszi_decompress_prologue: ctl reset, pass-2 decode, code tables;
+ *   cszi_huff_chunks(sec_len[2]) = M, the stream's 256-bit chunk count;
+ *   cszi_decompress_sync_range: speculative decode + synchronisation of
+ *     chunks [h0, h1) (entry: the range's first entry bit, or UINT64_MAX for
+ *     the speculative exit of chunk h0 - 1, which *entry_used receives);
+ *     writes X / K / D[h0, h1) of full-length (M) arrays of chunk exits,
+ *     symbol counts and dead flags; ctl->scratch[1] != 0: not converged;
+ *   (the caller all-gathers X / K / D and repeats a rank's range with the
+ *    true entry X[h0 - 1] when it differs from *entry_used)
+ *   cszi_decompress_write_window: counts scan, truncation check, symbols of
+ *     the slab's window;
+ *   cszi_decompress_epilogue: outlier section, reconstruction of the slab
+ *     into y ((slab[1] - slab[0]) ny nx floats).
+ * The result equals cszi_decompress with the same geometry. */
+int cszi_decompress_prologue(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
+                             const uint64_t sec_len[4], const cszi_geom *g, int32_t radius,
+                             void *workspace, uint64_t ws_bytes, cszi_ctl *ctl, void *stream);
+uint64_t cszi_huff_chunks(uint64_t nbytes);
+int cszi_decompress_sync_range(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
+                               const uint64_t sec_len[4], const cszi_geom *g, int32_t radius,
+                               uint64_t h0, uint64_t h1, uint64_t entry, uint64_t *X,
+                               uint32_t *K, uint8_t *D, uint64_t *entry_used, void *workspace,
+                               uint64_t ws_bytes, cszi_ctl *ctl, void *stream);
+int cszi_decompress_write_window(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
+                                 const uint64_t sec_len[4], const cszi_geom *g, int32_t radius,
+                                 const uint64_t *X, uint32_t *K, const uint8_t *D,
+                                 void *workspace, uint64_t ws_bytes, cszi_ctl *ctl, void *stream);
+int cszi_decompress_epilogue(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
+                             const uint64_t sec_len[4], const cszi_geom *g, int32_t radius,
+                             const double *level_eb, int32_t nlev, const int32_t variant[3],
+                             const int32_t order[3], float *y, void *workspace, uint64_t ws_bytes,
+                             cszi_ctl *ctl, void *stream);
+
 /* Root of the sharded compress (replaces the whole-field _field_sections /
  * serialize payload, pipeline.py:59-63, archive.py:102-127, for slab
  * pieces): raw = the np anchor pieces (na[i] floats each, slab order) ||

@@ -169,6 +169,15 @@ _SIGS = {
     "cszi_shard_set_range": (ctypes.c_int, [_vp, _vp, _vp]),
     "cszi_shard_piece_bits": (ctypes.c_int, [_vp, _vp, _i32, _vp, _vp]),
     "cszi_shard_counts": (ctypes.c_int, [_vp, _vp, _vp]),
+    "cszi_decompress_prologue": (ctypes.c_int, [_vp, _u64, _i32, _vp, _vp, _i32, _vp, _u64, _vp,
+                                                _vp]),
+    "cszi_huff_chunks": (_u64, [_u64]),
+    "cszi_decompress_sync_range": (ctypes.c_int, [_vp, _u64, _i32, _vp, _vp, _i32, _u64, _u64,
+                                                  _u64, _vp, _vp, _vp, _vp, _vp, _u64, _vp, _vp]),
+    "cszi_decompress_write_window": (ctypes.c_int, [_vp, _u64, _i32, _vp, _vp, _i32, _vp, _vp,
+                                                    _vp, _vp, _u64, _vp, _vp]),
+    "cszi_decompress_epilogue": (ctypes.c_int, [_vp, _u64, _i32, _vp, _vp, _i32, _vp, _i32, _vp,
+                                                _vp, _vp, _vp, _u64, _vp, _vp]),
     "cszi_shard_assemble": (ctypes.c_int, [_i32, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp,
                                            _vp, _i32, _vp, _u64, _vp, _vp, _u64, _vp, _vp]),
     "cszi_sample_gather": (ctypes.c_int, [_vp, _vp, _vp, _vp]),

@@ -59,6 +59,14 @@ u64 dec_scratch_bytes(u64 nbytes, int table_mode);
 int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *dec_tables,
                   void *out, int out_kind, void *scratch, cszi_ctl *ctl, cudaStream_t st,
                   int table_mode, int lmax, u64 w0, u64 w1);
+u64 huff_chunks(u64 nbytes);
+int launch_huff_sync_range(const uint8_t *bytes, u64 nbytes, const void *dec_tables, u64 h0,
+                           u64 h1, u64 entry, u64 *X, uint32_t *K, uint8_t *D, u64 *entry_used,
+                           void *scratch, cszi_ctl *ctl, cudaStream_t st);
+int launch_huff_write_window(const uint8_t *bytes, u64 nbytes, u64 n, int R,
+                             const void *dec_tables, const u64 *X, uint32_t *K, const uint8_t *D,
+                             u64 w0, u64 w1, uint16_t *out, void *scratch, cszi_ctl *ctl,
+                             cudaStream_t st);
 u64 p2enc_scratch_bytes(u64 n);
 int launch_pass2_encode(const uint8_t *in, const u64 *Np, u64 cap_n, uint8_t *out,
                         void *scratch, cszi_ctl *ctl, cudaStream_t st);
@@ -657,6 +665,100 @@ int cszi_decompress(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
     return decompress_body(payload, payload_len, pass2, sec_len, g, radius, level_eb, nlev,
                            variant, order, table_mode, y, workspace, ws_bytes, ctl, st);
   });
+}
+
+// ---- sharded decompress split by Huffman chunk ranges (distributed.py) ------
+// The stages of cszi_decompress over one workspace (cszi_decompress_workspace_
+// size): prologue (pass-2 decode + code tables), sync of a chunk range (the
+// caller all-gathers X / K / D between ranks), write of the z-slab's symbol
+// window, epilogue (outliers + reconstruction of the slab).
+static const uint8_t *split_raw(const uint8_t *payload, int32_t pass2, const DecompressWS &W) {
+  return pass2 ? W.raw : payload;
+}
+
+int cszi_decompress_prologue(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
+                             const uint64_t sec_len[4], const cszi_geom *g, int32_t radius,
+                             void *workspace, uint64_t ws_bytes, cszi_ctl *ctl, void *stream) {
+  if (!payload || !sec_len || !g || !ctl) return CSZI_E_INVALID_ARG;
+  CK(check_geom(g, radius));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  DecompressWS W;
+  if (ws_bytes < layout_decompress(g, radius, reinterpret_cast<const u64 *>(sec_len), payload_len,
+                                   1, workspace, &W))
+    return CSZI_E_CAPACITY;
+  const u64 nbins = 2 * (u64)radius;
+  const u64 raw_len = sec_len[0] + sec_len[1] + sec_len[2] + sec_len[3];
+  CK(launch_ctl_init(ctl, st));
+  if (pass2) CK(launch_pass2_decode(payload, payload_len, W.raw, raw_len, W.p2_scratch, ctl, st, 1));
+  if (sec_len[1] != nbins) return CSZI_E_MALFORMED;
+  const uint8_t *lengths = split_raw(payload, pass2, W) + sec_len[0];
+  CK(launch_canonical(lengths, (int)nbins, nullptr, W.dec_tables, ctl, st, pass2 ? raw_len : 0));
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
+uint64_t cszi_huff_chunks(uint64_t nbytes) { return huff_chunks(nbytes); }
+
+int cszi_decompress_sync_range(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
+                               const uint64_t sec_len[4], const cszi_geom *g, int32_t radius,
+                               uint64_t h0, uint64_t h1, uint64_t entry, uint64_t *X,
+                               uint32_t *K, uint8_t *D, uint64_t *entry_used, void *workspace,
+                               uint64_t ws_bytes, cszi_ctl *ctl, void *stream) {
+  if (!payload || !sec_len || !g || !X || !K || !D || !ctl) return CSZI_E_INVALID_ARG;
+  DecompressWS W;
+  if (ws_bytes < layout_decompress(g, radius, reinterpret_cast<const u64 *>(sec_len), payload_len,
+                                   1, workspace, &W))
+    return CSZI_E_CAPACITY;
+  const uint8_t *bits = split_raw(payload, pass2, W) + sec_len[0] + sec_len[1];
+  return launch_huff_sync_range(bits, sec_len[2], W.dec_tables, h0, h1, entry,
+                                reinterpret_cast<u64 *>(X), K, D,
+                                reinterpret_cast<u64 *>(entry_used), W.dec_scratch, ctl,
+                                reinterpret_cast<cudaStream_t>(stream));
+}
+
+int cszi_decompress_write_window(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
+                                 const uint64_t sec_len[4], const cszi_geom *g, int32_t radius,
+                                 const uint64_t *X, uint32_t *K, const uint8_t *D,
+                                 void *workspace, uint64_t ws_bytes, cszi_ctl *ctl, void *stream) {
+  if (!payload || !sec_len || !g || !X || !K || !D || !ctl) return CSZI_E_INVALID_ARG;
+  DecompressWS W;
+  if (ws_bytes < layout_decompress(g, radius, reinterpret_cast<const u64 *>(sec_len), payload_len,
+                                   1, workspace, &W))
+    return CSZI_E_CAPACITY;
+  const uint8_t *bits = split_raw(payload, pass2, W) + sec_len[0] + sec_len[1];
+  u64 w0 = 0;
+  const u64 wn = sym_window(g, &w0);
+  return launch_huff_write_window(bits, sec_len[2], grid_n(g), radius, W.dec_tables,
+                                  reinterpret_cast<const u64 *>(X), K, D, w0, w0 + wn, W.sym,
+                                  W.dec_scratch, ctl, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int cszi_decompress_epilogue(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
+                             const uint64_t sec_len[4], const cszi_geom *g, int32_t radius,
+                             const double *level_eb, int32_t nlev, const int32_t variant[3],
+                             const int32_t order[3], float *y, void *workspace, uint64_t ws_bytes,
+                             cszi_ctl *ctl, void *stream) {
+  if (!payload || !sec_len || !g || !level_eb || !variant || !order || !y || !ctl)
+    return CSZI_E_INVALID_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  DecompressWS W;
+  if (ws_bytes < layout_decompress(g, radius, reinterpret_cast<const u64 *>(sec_len), payload_len,
+                                   1, workspace, &W))
+    return CSZI_E_CAPACITY;
+  const uint8_t *raw = split_raw(payload, pass2, W);
+  const uint8_t *outl = raw + sec_len[0] + sec_len[1] + sec_len[2];
+  const u64 n = grid_n(g);
+  u64 w0 = 0;
+  const u64 wn = sym_window(g, &w0);
+  const u64 kmax = sec_len[3] >= 8 ? (sec_len[3] - 8) / 12 : 0;
+  k_outliers_parse<<<grid_for(kmax), 256, 0, st>>>(outl, sec_len[3], n, W.oidx, W.oval, W.sym,
+                                                   ctl);
+  note_launch();
+  k_outliers_mark<<<grid_for(kmax), 256, 0, st>>>(W.oidx, ctl, n, W.sym, w0, w0 + wn);
+  note_launch();
+  CK(launch_reconstruct(W.sym, reinterpret_cast<const float *>(raw), W.oidx, W.oval, kmax,
+                        reinterpret_cast<const u64 *>(&ctl->n_outliers), g, radius, level_eb,
+                        nlev, variant, order, y, st));
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
 // ---- Lorenzo predictor (pipeline.py:123-150, 202-203) ----------------------

@@ -1143,12 +1143,14 @@ struct SmemReader {
 DEV bool zrun_tables(const DecTables *G) { return G->counts[1] == 1 && G->first_code[1] == 0; }
 
 // Phase 1: speculative decode of chunk j from its first bit.
+// (chunks jbase + blockIdx * DEC_NT + threadIdx < M: a range of the stream)
 __global__ void __launch_bounds__(DEC_NT) k_dec_spec(Stream s, const DecTables *G,
                                                     const uint16_t *sorted, u64 M, u64 *spec_exit,
-                                                    uint32_t *spec_cnt, uint8_t *spec_dead) {
+                                                    uint32_t *spec_cnt, uint8_t *spec_dead,
+                                                    u64 jbase) {
   __shared__ DecSmem T;
   __shared__ uint32_t sw[DEC_SW];
-  const u64 j0 = (u64)blockIdx.x * DEC_NT;
+  const u64 j0 = jbase + (u64)blockIdx.x * DEC_NT;
   SmemStream ss;
   stage_words(sw, s, j0, ss);
   load_dec_smem(T, G, sorted);  // ends with __syncthreads()
@@ -1190,18 +1192,22 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_spec(Stream s, const DecTables *
 // walked in lockstep with its speculative decode until both chains meet.
 // it == 0: entry = 0 (j == 0) or spec_exit[j-1]; it > 0: entry = X_prev[j-1]
 // for chunks whose entry changed in the previous iteration.
+// (chunks [jbase, M): a range of the stream whose first chunk enters at
+// *entry_dev -- 0 for the stream start, a neighbour's true exit, or the
+// speculative exit of chunk jbase - 1)
 __global__ void __launch_bounds__(256) k_dec_sync(Stream s, const DecTables *G,
                                                  const uint16_t *sorted, u64 M, int it,
                                                  const u64 *spec_exit, const uint32_t *spec_cnt,
                                                  const uint8_t *spec_dead, const u64 *X_prev,
                                                  const uint8_t *chg_prev, u64 *X, uint32_t *K,
-                                                 uint8_t *D, uint8_t *chg, uint32_t *nchg) {
+                                                 uint8_t *D, uint8_t *chg, uint32_t *nchg,
+                                                 u64 jbase, const u64 *entry_dev) {
   __shared__ DecSmem T;
-  const u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+  const u64 j = jbase + blockIdx.x * (u64)blockDim.x + threadIdx.x;
   // iterations > 0: only chunks whose predecessor moved re-walk; blocks
   // without one skip the table load (most of them once the chains meet)
   bool need = j < M;
-  if (need && it > 0 && (j == 0 || !chg_prev[j - 1])) {
+  if (need && it > 0 && (j == jbase || !chg_prev[j - 1])) {
     X[j] = X_prev[j];
     chg[j] = 0;
     need = false;
@@ -1209,7 +1215,7 @@ __global__ void __launch_bounds__(256) k_dec_sync(Stream s, const DecTables *G,
   if (!__syncthreads_or(need)) return;
   load_dec_smem(T, G, sorted);
   if (!need) return;
-  const u64 e = (it == 0) ? ((j == 0) ? 0 : spec_exit[j - 1]) : X_prev[j - 1];
+  const u64 e = (j == jbase) ? *entry_dev : (it == 0) ? spec_exit[j - 1] : X_prev[j - 1];
   const u64 end = min((j + 1) * DEC_C, s.nb);
   BitReader ba, bb;
   ba.init();
@@ -1280,7 +1286,7 @@ __global__ void __launch_bounds__(256) k_dec_sync(Stream s, const DecTables *G,
   const u64 prev_est = (it == 0) ? spec_exit[j] : X_prev[j];
   const uint8_t c = (xo != prev_est) ? 1 : 0;
   chg[j] = c;
-  if (c && j + 1 < M) atomicAdd(nchg, 1u);
+  if (c && j + 1 < M) atomicAdd(nchg, 1u);  // (M: the range end)
 }
 
 // Phase 3 (after the generic exclusive scan of K into off): truncation
@@ -1712,10 +1718,13 @@ int launch_chain_resolve(const uint8_t *tab, u64 M, int D, int e0, uint8_t *entr
                          void *scratch, cudaStream_t st);
 
 static u64 dec_chunks(u64 nbytes) { return nbytes ? (nbytes * 8 + DEC_C - 1) / DEC_C : 1; }
+// bytes of the speculative / synchronisation scratch over M chunks (SyncScratch)
+static u64 sync_scratch_bytes(u64 M) { return M * (8 + 8 + 4 + 3) + 64 + 16 + 8 * 16; }  // nchg: 16 u32
 
 u64 dec_scratch_bytes(u64 nbytes, int table_mode) {
   const u64 M = dec_chunks(nbytes);
-  u64 b = M * (8 * 4 + 4 * 2 + 4) + 256 + scan_scratch_bytes(M) + 64;
+  u64 b = M * (8 + 4 + 1) + 3 * 16 + sync_scratch_bytes(M) + M * 8 + 64 + scan_scratch_bytes(M) +
+          256;
   if (table_mode) b += M * 32 * (1 + 4 + 1) + M + chain_scratch_bytes(M, 32) + 256;
   return b;
 }
@@ -1729,55 +1738,142 @@ static unsigned char *carve(unsigned char *&p, u64 bytes) {
 // Decode exactly n symbols.  out_kind 0: uint16 symbols, 1: int32 codes.
 // table_mode != 0 selects the exact transfer-table path (lmax = longest code
 // length), used when the speculative path reports non-convergence.
-int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *dec_tables,
-                  void *out, int out_kind, void *scratch, cszi_ctl *ctl, cudaStream_t st,
-                  int table_mode, int lmax, u64 w0, u64 w1) {
-  if (n == 0) return CSZI_OK;
+__global__ void k_set_u64(u64 *p, u64 v) { *p = v; }
+
+static Stream make_stream(const uint8_t *bytes, u64 nbytes) {
   Stream s;
   const uintptr_t addr = reinterpret_cast<uintptr_t>(bytes);
   s.w = reinterpret_cast<const uint32_t *>(addr & ~(uintptr_t)3);
   s.b0 = 8 * (addr & 3);
   s.nb = nbytes * 8;
   s.nwords = (s.b0 + s.nb + 31) / 32;
+  return s;
+}
+
+// Scratch of the speculative / synchronisation phases over M chunks.
+struct SyncScratch {
+  u64 *spec_exit, *X1, *entry;
+  uint32_t *spec_cnt, *nchg;
+  uint8_t *spec_dead, *chg0, *chg1;
+};
+static SyncScratch carve_sync(unsigned char *&p, u64 M) {
+  SyncScratch S;
+  S.spec_exit = reinterpret_cast<u64 *>(carve(p, M * 8));
+  S.X1 = reinterpret_cast<u64 *>(carve(p, M * 8));
+  S.spec_cnt = reinterpret_cast<uint32_t *>(carve(p, M * 4));
+  S.nchg = reinterpret_cast<uint32_t *>(carve(p, 64));
+  S.entry = reinterpret_cast<u64 *>(carve(p, 16));
+  S.spec_dead = carve(p, M);
+  S.chg0 = carve(p, M);
+  S.chg1 = carve(p, M);
+  return S;
+}
+
+// Phases 1-2 over the chunk range [h0, h1) of a stream of M chunks: the
+// speculative decode (of h0 - 1 as well, whose exit is the range's assumed
+// entry unless `entry` is given) and three synchronisation iterations.
+// X / K / D (full-length arrays) receive the range's true exits, symbol
+// counts and dead flags; *entry_used the entry the range assumed;
+// ctl->scratch[1] the number of chains still moving (0: converged).
+static void huff_sync_range(const Stream &s, const DecTables *G, const uint16_t *sorted, u64 M,
+                            u64 h0, u64 h1, u64 entry, u64 *X, uint32_t *K, uint8_t *D,
+                            u64 *entry_used, const SyncScratch &S, cszi_ctl *ctl,
+                            cudaStream_t st, int iters = 3) {
+  // iters is odd: the last iteration writes X (even iterations write X,
+  // odd ones the scratch copy)
+  cudaMemsetAsync(S.nchg, 0, 64, st);
+  if (h1 <= h0) {
+    cudaMemcpyAsync(&ctl->scratch[1], S.nchg, 4, cudaMemcpyDeviceToDevice, st);
+    return;
+  }
+  const u64 sb = (h0 > 0 && entry == ~0ull) ? h0 - 1 : h0;  // speculate h0 - 1 for the entry
+  k_dec_spec<<<(unsigned)((h1 - sb + DEC_NT - 1) / DEC_NT), DEC_NT, 0, st>>>(
+      s, G, sorted, h1, S.spec_exit, S.spec_cnt, S.spec_dead, sb);
+  note_launch();
+  // the range's entry: 0 at the stream start, else the given one, else the
+  // speculative exit of chunk h0 - 1 (device-resident: read by k_dec_sync)
+  const u64 e0 = (h0 == 0) ? 0ull : entry;
+  if (e0 != ~0ull) {
+    k_set_u64<<<1, 1, 0, st>>>(S.entry, e0);
+    note_launch();
+  } else {
+    cudaMemcpyAsync(S.entry, S.spec_exit + (h0 - 1), 8, cudaMemcpyDeviceToDevice, st);
+  }
+  if (entry_used) cudaMemcpyAsync(entry_used, S.entry, 8, cudaMemcpyDeviceToDevice, st);
+  const unsigned blocks = (unsigned)((h1 - h0 + 255) / 256);
+  // iteration 0 verifies every chunk; later iterations repair chunks whose
+  // predecessor did not synchronise (blocks without one exit at once)
+  for (int it = 0; it < iters; ++it) {
+    u64 *Xo = (it & 1) ? S.X1 : X;
+    const u64 *Xp = it ? ((it & 1) ? X : S.X1) : nullptr;
+    uint8_t *co = (it & 1) ? S.chg1 : S.chg0;
+    const uint8_t *cp = it ? ((it & 1) ? S.chg0 : S.chg1) : nullptr;
+    k_dec_sync<<<blocks, 256, 0, st>>>(s, G, sorted, h1, it, S.spec_exit, S.spec_cnt,
+                                       S.spec_dead, Xp, cp, Xo, K, D, co, S.nchg + it, h0,
+                                       S.entry);
+    note_launch();
+  }
+  cudaMemcpyAsync(&ctl->scratch[1], S.nchg + iters - 1, 4, cudaMemcpyDeviceToDevice, st);
+}
+
+// Phase 3-4 over all M chunks: exclusive scan of the symbol counts,
+// truncation check, and the write of the symbol window [w0, w1).
+static void huff_write(const Stream &s, const DecTables *G, const uint16_t *sorted, u64 M,
+                       const u64 *X, uint32_t *K, const uint8_t *D, u64 n, int R, void *out,
+                       int out_kind, u64 w0, u64 w1, unsigned char *p, cszi_ctl *ctl,
+                       cudaStream_t st) {
+  u64 *off = reinterpret_cast<u64 *>(carve(p, M * 8));
+  u64 *misc = reinterpret_cast<u64 *>(carve(p, 64));
+  u64 *first_dead = misc + 2;
+  u64 *total = misc + 3;
+  void *scan_ws = carve(p, scan_scratch_bytes(M));
+  cudaMemsetAsync(first_dead, 0xff, 8, st);
+  const unsigned blocks = (unsigned)((M + 255) / 256);
+  const unsigned dblocks = (unsigned)((M + DEC_NT - 1) / DEC_NT);
+  launch_excl_scan_u32(K, M, off, total, scan_ws, st);
+  k_dec_first_dead<<<blocks, 256, 0, st>>>(M, D, first_dead);
+  note_launch();
+  const DecCheck C{first_dead, total, ctl};
+  if (out_kind == 0) {
+    k_dec_write<uint16_t><<<dblocks, DEC_NT, 0, st>>>(s, G, sorted, M, X, off, K, n, R,
+                                                      reinterpret_cast<uint16_t *>(out), w0, w1,
+                                                      C);
+    k_dec_write_zr<uint16_t><<<dblocks, DEC_NT, 0, st>>>(
+        s, G, sorted, M, X, off, K, n, R, reinterpret_cast<uint16_t *>(out), w0, w1, C);
+  } else {
+    k_dec_write<int32_t><<<dblocks, DEC_NT, 0, st>>>(s, G, sorted, M, X, off, K, n, R,
+                                                     reinterpret_cast<int32_t *>(out), w0, w1, C);
+    k_dec_write_zr<int32_t><<<dblocks, DEC_NT, 0, st>>>(
+        s, G, sorted, M, X, off, K, n, R, reinterpret_cast<int32_t *>(out), w0, w1, C);
+  }
+  note_launch(2);
+}
+
+u64 huff_split_scratch_bytes(u64 nbytes) {
+  const u64 M = dec_chunks(nbytes);
+  return sync_scratch_bytes(M) + M * 8 + 64 + scan_scratch_bytes(M) + 1024;
+}
+
+// table_mode != 0 selects the exact transfer-table path (lmax = longest code
+// length), used when the speculative path reports non-convergence.
+int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *dec_tables,
+                  void *out, int out_kind, void *scratch, cszi_ctl *ctl, cudaStream_t st,
+                  int table_mode, int lmax, u64 w0, u64 w1) {
+  if (n == 0) return CSZI_OK;
+  const Stream s = make_stream(bytes, nbytes);
   const DecTables *G = reinterpret_cast<const DecTables *>(dec_tables);
   const uint16_t *sorted = reinterpret_cast<const uint16_t *>(G + 1);
   const u64 M = dec_chunks(nbytes);
   unsigned char *p = reinterpret_cast<unsigned char *>(scratch);
-  u64 *spec_exit = reinterpret_cast<u64 *>(carve(p, M * 8));
   u64 *X0 = reinterpret_cast<u64 *>(carve(p, M * 8));
-  u64 *X1 = reinterpret_cast<u64 *>(carve(p, M * 8));
-  u64 *off = reinterpret_cast<u64 *>(carve(p, M * 8));
-  uint32_t *spec_cnt = reinterpret_cast<uint32_t *>(carve(p, M * 4));
   uint32_t *K = reinterpret_cast<uint32_t *>(carve(p, M * 4));
-  u64 *misc = reinterpret_cast<u64 *>(carve(p, 64));  // nchg[4] (u32), first_dead, total
-  uint32_t *nchg = reinterpret_cast<uint32_t *>(misc);
-  u64 *first_dead = misc + 2;
-  u64 *total = misc + 3;
-  uint8_t *spec_dead = carve(p, M);
   uint8_t *D = carve(p, M);
-  uint8_t *chg0 = carve(p, M);
-  uint8_t *chg1 = carve(p, M);
-  void *scan_ws = carve(p, scan_scratch_bytes(M));
-  cudaMemsetAsync(misc, 0, 16, st);
-  cudaMemsetAsync(first_dead, 0xff, 8, st);
-  const unsigned blocks = (unsigned)((M + 255) / 256);
-  const unsigned dblocks = (unsigned)((M + DEC_NT - 1) / DEC_NT);
   if (!table_mode) {
-    k_dec_spec<<<dblocks, DEC_NT, 0, st>>>(s, G, sorted, M, spec_exit, spec_cnt, spec_dead);
-    note_launch();
-    // iteration 0 verifies every chunk; two more iterations repair chunks
-    // whose predecessor did not synchronise.  A chain still moving after
-    // that is reported in ctl->scratch[1]; the caller reruns in table mode.
-    k_dec_sync<<<blocks, 256, 0, st>>>(s, G, sorted, M, 0, spec_exit, spec_cnt, spec_dead,
-                                       nullptr, nullptr, X0, K, D, chg0, nchg + 0);
-    note_launch();
-    k_dec_sync<<<blocks, 256, 0, st>>>(s, G, sorted, M, 1, spec_exit, spec_cnt, spec_dead, X0,
-                                       chg0, X1, K, D, chg1, nchg + 1);
-    note_launch();
-    k_dec_sync<<<blocks, 256, 0, st>>>(s, G, sorted, M, 2, spec_exit, spec_cnt, spec_dead, X1,
-                                       chg1, X0, K, D, chg0, nchg + 2);
-    note_launch();
-    cudaMemcpyAsync(&ctl->scratch[1], nchg + 2, 4, cudaMemcpyDeviceToDevice, st);
+    const SyncScratch S = carve_sync(p, M);
+    // the whole stream is one range entering at bit 0; a chain still moving
+    // after three iterations is reported in ctl->scratch[1] and the caller
+    // reruns in table mode
+    huff_sync_range(s, G, sorted, M, 0, M, 0, X0, K, D, nullptr, S, ctl, st);
   } else {
     if (lmax < 1 || lmax > 32) lmax = 32;
     uint8_t *tab = carve(p, M * lmax);
@@ -1786,6 +1882,7 @@ int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *de
     uint8_t *E = carve(p, M);
     void *chain_ws = carve(p, chain_scratch_bytes(M, lmax));
     const u64 work = M * (u64)lmax;
+    const unsigned blocks = (unsigned)((M + 255) / 256);
     k_dec_table<<<(unsigned)((work + 255) / 256), 256, 0, st>>>(s, G, sorted, M, lmax, tab,
                                                                ktab, dtab);
     note_launch();
@@ -1793,23 +1890,41 @@ int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *de
     k_dec_from_tab<<<blocks, 256, 0, st>>>(M, lmax, E, ktab, dtab, X0, K, D);
     note_launch();
   }
-  launch_excl_scan_u32(K, M, off, total, scan_ws, st);
-  k_dec_first_dead<<<blocks, 256, 0, st>>>(M, D, first_dead);
-  note_launch();
-  const DecCheck C{first_dead, total, ctl};
-  if (out_kind == 0) {
-    k_dec_write<uint16_t><<<dblocks, DEC_NT, 0, st>>>(s, G, sorted, M, X0, off, K, n, R,
-                                                      reinterpret_cast<uint16_t *>(out), w0, w1,
-                                                      C);
-    k_dec_write_zr<uint16_t><<<dblocks, DEC_NT, 0, st>>>(
-        s, G, sorted, M, X0, off, K, n, R, reinterpret_cast<uint16_t *>(out), w0, w1, C);
-  } else {
-    k_dec_write<int32_t><<<dblocks, DEC_NT, 0, st>>>(s, G, sorted, M, X0, off, K, n, R,
-                                                     reinterpret_cast<int32_t *>(out), w0, w1, C);
-    k_dec_write_zr<int32_t><<<dblocks, DEC_NT, 0, st>>>(
-        s, G, sorted, M, X0, off, K, n, R, reinterpret_cast<int32_t *>(out), w0, w1, C);
-  }
-  note_launch(2);
+  huff_write(s, G, sorted, M, X0, K, D, n, R, out, out_kind, w0, w1, p, ctl, st);
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
+// ---- split decode (sharded decompress): ranges of chunks per rank --------
+u64 huff_chunks(u64 nbytes) { return dec_chunks(nbytes); }
+
+int launch_huff_sync_range(const uint8_t *bytes, u64 nbytes, const void *dec_tables, u64 h0,
+                           u64 h1, u64 entry, u64 *X, uint32_t *K, uint8_t *D, u64 *entry_used,
+                           void *scratch, cszi_ctl *ctl, cudaStream_t st) {
+  const Stream s = make_stream(bytes, nbytes);
+  const DecTables *G = reinterpret_cast<const DecTables *>(dec_tables);
+  const uint16_t *sorted = reinterpret_cast<const uint16_t *>(G + 1);
+  const u64 M = dec_chunks(nbytes);
+  if (h1 > M) h1 = M;
+  unsigned char *p = reinterpret_cast<unsigned char *>(scratch);
+  const SyncScratch S = carve_sync(p, M);
+  // more repair iterations than the whole-stream decode (which falls back to
+  // the exact table path): a range has no second chance at that
+  huff_sync_range(s, G, sorted, M, h0, h1, entry, X, K, D, entry_used, S, ctl, st, 11);
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
+int launch_huff_write_window(const uint8_t *bytes, u64 nbytes, u64 n, int R,
+                             const void *dec_tables, const u64 *X, uint32_t *K, const uint8_t *D,
+                             u64 w0, u64 w1, uint16_t *out, void *scratch, cszi_ctl *ctl,
+                             cudaStream_t st) {
+  if (n == 0) return CSZI_OK;
+  const Stream s = make_stream(bytes, nbytes);
+  const DecTables *G = reinterpret_cast<const DecTables *>(dec_tables);
+  const uint16_t *sorted = reinterpret_cast<const uint16_t *>(G + 1);
+  const u64 M = dec_chunks(nbytes);
+  unsigned char *p = reinterpret_cast<unsigned char *>(scratch);
+  carve_sync(p, M);  // (the same scratch block as the range phase)
+  huff_write(s, G, sorted, M, X, K, D, n, R, out, 0, w0, w1, p, ctl, st);
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 

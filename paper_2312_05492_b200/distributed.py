@@ -607,9 +607,180 @@ def decompress_slab(data, z0: int, z1: int):
     return decompress_device(data, slab=(z0, z1))
 
 
+class _SplitSlab:
+    """One slab's split-decompress state (workspace, ctl, chunk range)."""
+
+    def __init__(self, plan, z0: int, z1: int, h0: int, h1: int):
+        t = _lib.torch()
+        lib = _lib.load()
+        self.z0, self.z1, self.h0, self.h1 = z0, z1, h0, h1
+        self.geom = make_geom(plan["extents"], default_layout(3))
+        self.geom.slab[0], self.geom.slab[1] = z0, z1
+        self.ctl = _lib.DeviceCtl()
+        self.ws = t.empty(int(lib.cszi_decompress_workspace_size(
+            ctypes.byref(self.geom), plan["R"], plan["sec"], plan["plen"])),
+            dtype=t.uint8, device="cuda")
+        self.entry_used = t.zeros(1, dtype=t.int64, device="cuda")
+
+
+def _split_plan(data):
+    """Header checks and launch arguments shared by every slab, or None when
+    the archive must take the single-rank path (host-side errors raise
+    there, in the reference's order; other codecs / layouts / predictors)."""
+    from .archive import HEADER_SIZE, PREDICTOR_INTERP, unpack_header
+    from .pass2 import DEFAULT_CODEC
+    from .pipeline import _host_checks, _split_input
+    from .grid import Dims
+    from .predictor import plan_levels
+
+    head, d_payload, h_payload, total = _split_input(data)
+    if total < HEADER_SIZE:
+        return None
+    h = unpack_header(head, total)
+    if h.predictor != PREDICTOR_INTERP or h.rank != 3 or h.anchor_stride != 8:
+        return None
+    if h.pass2 and h.pass2_codec != DEFAULT_CODEC:
+        return None
+    err, layout = _host_checks(h, Dims(h.extents))
+    if err is not None or h.sec_lens[1] != 2 * h.quant_radius:
+        return None
+    if d_payload is None:
+        d_payload = _lib.to_device_u8(h_payload)
+    if h.pass2 and sum(h.sec_lens) > 128 * d_payload.numel():
+        return None
+    if not h.pass2 and d_payload.numel() != sum(h.sec_lens):
+        return None
+    lp = plan_levels(layout.anchor_stride, h.eb_abs, h.alpha)
+    return dict(h=h, payload=d_payload, plen=int(d_payload.numel()), pass2=1 if h.pass2 else 0,
+                extents=tuple(h.extents), R=h.quant_radius,
+                sec=(ctypes.c_uint64 * 4)(*h.sec_lens),
+                leb=(ctypes.c_double * _lib.MAX_LEVELS)(*[v.eb for v in lp.levels]),
+                nlev=len(lp.levels), var=(ctypes.c_int32 * 3)(*h.variants),
+                order=(ctypes.c_int32 * 3)(*h.dim_order))
+
+
+# The split saves each rank (1 - 1/world) of the whole-stream synchronisation
+# (~80 us per 535K chunks on a B200) and costs a few host round trips and
+# one all-gather (~150 us): worth it for long streams only.
+SPLIT_MIN_SAVED_CHUNKS = 1 << 20
+
+
+def split_pays(data, world: int) -> bool:
+    """Whether decompress_sharded splits the Huffman synchronisation for
+    this archive over `world` ranks."""
+    from .archive import HEADER_SIZE, unpack_header
+
+    if world < 2:
+        return False
+    head = data.header if isinstance(data, DeviceArchive) else bytes(data[:HEADER_SIZE])
+    try:
+        h = unpack_header(head, len(data))
+    except Exception:
+        return False
+    M = (h.sec_lens[2] * 8 + 255) // 256
+    return M * (world - 1) // world >= SPLIT_MIN_SAVED_CHUNKS
+
+
+def decompress_slabs_split(data, slabs, comm, world: int):
+    """Sharded decompress with the Huffman synchronisation split by chunk
+    ranges: this process's slabs [(rank, z0, z1), ...] each synchronise
+    1/world of the stream's 256-bit chunks, the (exit, count, dead) records
+    are all-gathered (one collective), a range whose assumed entry differs
+    from its predecessor's true exit re-synchronises (rare: chains meet
+    within a few codewords), then every slab writes its own symbol window
+    and reconstructs its planes.  Returns [(z0, z1, tensor), ...] or None
+    when the archive needs the single-rank path.  Bit-identical to
+    decompress_device(slab=...) (tests/test_gpu_distributed.py)."""
+    t = _lib.require_cuda()
+    lib = _lib.load()
+    st = _lib.stream_ptr()
+    plan = _split_plan(data)
+    if plan is None:
+        return None
+    M = int(lib.cszi_huff_chunks(plan["h"].sec_lens[2]))
+    per = -(-M // world)
+    S = [_SplitSlab(plan, z0, z1, min(M, r * per), min(M, (r + 1) * per)) for r, z0, z1 in slabs]
+    pay = _lib.ptr(plan["payload"])
+    args = lambda s: (pay, plan["plen"], plan["pass2"], plan["sec"], ctypes.byref(s.geom),  # noqa
+                      plan["R"])
+    X = [t.zeros(M, dtype=t.int64, device="cuda") for _ in S]
+    K = [t.zeros(M, dtype=t.int32, device="cuda") for _ in S]
+    D = [t.zeros(M, dtype=t.uint8, device="cuda") for _ in S]
+    for s, x, k, d in zip(S, X, K, D):
+        _lib.check(lib.cszi_decompress_prologue(*args(s), _lib.ptr(s.ws), s.ws.numel(), s.ctl.ptr,
+                                                st), "decompress_prologue")
+    entries = [None] * len(S)  # None: speculative entry
+    for _round in range(world + 1):
+        for i, (s, x, k, d) in enumerate(zip(S, X, K, D)):
+            if _round == 0 or entries[i] is not None:
+                e = (1 << 64) - 1 if entries[i] is None else int(entries[i])
+                _lib.check(lib.cszi_decompress_sync_range(
+                    *args(s), s.h0, s.h1, e, _lib.ptr(x), _lib.ptr(k), _lib.ptr(d),
+                    _lib.ptr(s.entry_used), _lib.ptr(s.ws), s.ws.numel(), s.ctl.ptr, st),
+                    "decompress_sync_range")
+        # one all-gather of every range's records: (exit, count | dead << 32) per chunk
+        shares = []
+        for s, x, k, d in zip(S, X, K, D):
+            rec = t.zeros(2 * per, dtype=t.int64, device="cuda")
+            nrec = s.h1 - s.h0
+            if nrec:
+                rec[0:2 * nrec:2] = x[s.h0:s.h1]
+                rec[1:2 * nrec:2] = (k[s.h0:s.h1].to(t.int64) & 0xFFFFFFFF) | \
+                    (d[s.h0:s.h1].to(t.int64) << 32)
+            shares.append(rec)
+        got = comm.allgather(shares)[0]  # list over ranks
+        xa = t.cat([g[0::2] for g in got])[:M]
+        kd = t.cat([g[1::2] for g in got])[:M]
+        ka = (kd & 0xFFFFFFFF).to(t.int32)
+        da = (kd >> 32).to(t.uint8)
+        for x, k, d in zip(X, K, D):
+            x.copy_(xa)
+            k.copy_(ka)
+            d.copy_(da)
+        # ranges whose assumed entry is not their predecessor's true exit
+        flags = []
+        for s in S:
+            if s.h0 == 0 or s.h1 <= s.h0:
+                flags.append(t.zeros(1, dtype=t.int64, device="cuda"))
+            else:
+                flags.append((xa[s.h0 - 1:s.h0] != s.entry_used).to(t.int64))
+        moved = [f.clone() for f in flags]
+        comm.allreduce(moved, "max")
+        if int(t.stack(moved).max().item()) == 0:
+            break
+        entries = [int(xa[s.h0 - 1].item()) if int(f.item()) else None for s, f in zip(S, flags)]
+    out = []
+    for s, x, k, d in zip(S, X, K, D):
+        c = s.ctl.fetch()
+        if c.scratch[1] != 0:
+            return None  # a range did not synchronise: the single-rank path (table mode)
+        _lib.check(lib.cszi_decompress_write_window(*args(s), _lib.ptr(x), _lib.ptr(k),
+                                                    _lib.ptr(d), _lib.ptr(s.ws), s.ws.numel(),
+                                                    s.ctl.ptr, st), "decompress_write_window")
+        ny, nx = plan["extents"][1], plan["extents"][2]
+        y = t.empty((max(s.z1 - s.z0, 0), ny, nx), dtype=t.float32, device="cuda")
+        if s.z1 > s.z0:
+            _lib.check(lib.cszi_decompress_epilogue(*args(s), plan["leb"], plan["nlev"],
+                                                    plan["var"], plan["order"], _lib.ptr(y),
+                                                    _lib.ptr(s.ws), s.ws.numel(), s.ctl.ptr,
+                                                    st), "decompress_epilogue")
+        c = s.ctl.fetch()
+        from .pipeline import _raise_device_flags
+
+        _raise_device_flags(c, int(np.prod(plan["extents"])))
+        if c.flags & _lib.F_OUTLIER_INDEX:
+            raise IndexError("outlier index out of bounds for the grid")
+        out.append((s.z0, s.z1, y))
+    return out
+
+
 def decompress_sharded(data, nz: int = None, group=None):
     """torch.distributed entry point: this rank's slab of the decompressed
-    field -> (z0, z1, tensor).  ``nz`` defaults to the archive's extent."""
+    field -> (z0, z1, tensor).  ``nz`` defaults to the archive's extent.
+    The Huffman synchronisation is split across the ranks
+    (decompress_slabs_split); archives that need the single-rank path
+    (other codecs, non-converging streams, host-side errors) decode the slab
+    on each rank."""
     import torch.distributed as dist
 
     from .archive import HEADER_SIZE, unpack_header
@@ -617,7 +788,12 @@ def decompress_sharded(data, nz: int = None, group=None):
     if nz is None:
         head = data[:HEADER_SIZE] if not isinstance(data, DeviceArchive) else data.header
         nz = unpack_header(bytes(head), len(data)).extents[0]
-    z0, z1 = slab_bounds(nz, dist.get_world_size(group))[dist.get_rank(group)]
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    z0, z1 = slab_bounds(nz, world)[rank]
+    if split_pays(data, world):
+        got = decompress_slabs_split(data, [(rank, z0, z1)], TorchComm(group), world)
+        if got is not None:
+            return got[0]
     if z1 <= z0:  # more ranks than z tiles: this rank owns no planes
         t = _lib.require_cuda()
         head = data.header if isinstance(data, DeviceArchive) else bytes(data[:HEADER_SIZE])
@@ -626,13 +802,20 @@ def decompress_sharded(data, nz: int = None, group=None):
     return z0, z1, decompress_slab(data, z0, z1)
 
 
-def decompress_simulated(data, world: int):
+def decompress_simulated(data, world: int, split: bool = False):
     """All ``world`` slabs in this process, concatenated (GPU-count
-    determinism check on one device)."""
+    determinism check on one device); ``split`` runs the chunk-range split
+    of decompress_sharded over SimComm."""
     from .archive import HEADER_SIZE, unpack_header
 
     t = _lib.torch()
     head = data.header if isinstance(data, DeviceArchive) else bytes(data[:HEADER_SIZE])
     nz = unpack_header(head, len(data)).extents[0]
-    parts = [decompress_slab(data, z0, z1) for z0, z1 in slab_bounds(nz, world) if z1 > z0]
+    bounds = slab_bounds(nz, world)
+    if split:
+        got = decompress_slabs_split(data, [(r, z0, z1) for r, (z0, z1) in enumerate(bounds)],
+                                     SimComm(world), world)
+        if got is not None:
+            return t.cat([y for z0, z1, y in got if z1 > z0], 0)
+    parts = [decompress_slab(data, z0, z1) for z0, z1 in bounds if z1 > z0]
     return t.cat(parts, 0)
