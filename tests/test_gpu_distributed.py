@@ -128,8 +128,9 @@ def _torchcomm_worker(rank, world, port, data, out_path):
     import torch
     import torch.distributed as dist
 
-    from paper_2312_05492_b200.distributed import (compress_sharded, compress_sharded_batch,
-                                                   decompress_sharded, slab_bounds)
+    from paper_2312_05492_b200.distributed import (TorchComm, compress_sharded,
+                                                   compress_sharded_batch, decompress_sharded,
+                                                   decompress_slabs_split, slab_bounds)
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
@@ -147,6 +148,9 @@ def _torchcomm_worker(rank, world, port, data, out_path):
         _, _, ys = decompress_sharded(obj[0])
         parts = [None] * world
         dist.all_gather_object(parts, ys.cpu().numpy())
+        # the chunk-range split of the Huffman synchronisation over TorchComm
+        got = decompress_slabs_split(obj[0], [(rank, z0, z1)], TorchComm(), world)
+        assert got is not None and torch.equal(got[0][2], ys)
         if rank == 0:
             np.savez(out_path, blob=np.frombuffer(blob, dtype=np.uint8),
                      b0=np.frombuffer(batch[0].to_bytes(), dtype=np.uint8),
