@@ -284,6 +284,14 @@ int cszi_shard_piece_bits(const uint64_t *hist, const uint8_t *lengths, int32_t 
                           int64_t *out, void *stream);
 int cszi_shard_counts(const cszi_ctl *ctl, int64_t *out, void *stream);
 
+/* Distributed pass-2 encode (sharded compress): out[0] / out[1] = the first /
+ * last index i in [lo + 2, hi) of bytes where a run of >= 2 zero bytes ends
+ * (bytes[i-2] == bytes[i-1] == 0 != bytes[i]), -1 if none.  The zero-run
+ * codec (pass2.py:30-67) has a segment boundary there whatever precedes the
+ * run, so a stream cut at such points encodes piecewise to the same bytes.
+ * out must hold 4 int64 (out[2..3] is scratch). */
+int cszi_find_cuts(const uint8_t *bytes, uint64_t lo, uint64_t hi, int64_t *out, void *stream);
+
 /* ---- sharded decompress split by Huffman chunk ranges -------
  * The stages of cszi_decompress over one workspace of
  * cszi_decompress_workspace_size bytes (same arguments throughout; g->slab

@@ -172,6 +172,7 @@ _SIGS = {
     "cszi_decompress_prologue": (ctypes.c_int, [_vp, _u64, _i32, _vp, _vp, _i32, _vp, _u64, _vp,
                                                 _vp]),
     "cszi_huff_chunks": (_u64, [_u64]),
+    "cszi_find_cuts": (ctypes.c_int, [_vp, _u64, _u64, _vp, _vp]),
     "cszi_decompress_sync_range": (ctypes.c_int, [_vp, _u64, _i32, _vp, _vp, _i32, _u64, _u64,
                                                   _u64, _vp, _vp, _vp, _vp, _vp, _u64, _vp, _vp]),
     "cszi_decompress_write_window": (ctypes.c_int, [_vp, _u64, _i32, _vp, _vp, _i32, _vp, _vp,

@@ -240,6 +240,25 @@ __global__ void k_shard_tail(uint8_t *count_at, u64 k, u64 raw_len, int is_paylo
   }
 }
 
+// Cut points for the distributed pass-2 encode: positions i in [lo + 2, hi)
+// where a run of >= 2 zero bytes ends (b[i-2] == b[i-1] == 0, b[i] != 0):
+// the zero-run codec's segmentation has a boundary there whatever precedes
+// the run (pass2.py:30-67), so the stream can be encoded piecewise.
+__global__ void k_find_cuts(const uint8_t *__restrict__ b, u64 lo, u64 hi,
+                            unsigned long long *first, unsigned long long *last) {
+  for (u64 i = lo + 2 + blockIdx.x * (u64)blockDim.x + threadIdx.x; i < hi;
+       i += (u64)gridDim.x * blockDim.x) {
+    if (b[i] != 0 && b[i - 1] == 0 && b[i - 2] == 0) {
+      atomicMin(first, (unsigned long long)i);
+      atomicMax(last, (unsigned long long)i);
+    }
+  }
+}
+__global__ void k_cuts_out(const unsigned long long *fl, int64_t *out) {
+  out[0] = fl[0] == ~0ull ? -1 : (int64_t)fl[0];
+  out[1] = fl[1] == 0 ? -1 : (int64_t)fl[1];
+}
+
 // ---------------------------------------------------------------------------
 // workspace layout
 // ---------------------------------------------------------------------------
@@ -1050,6 +1069,21 @@ int cszi_shard_assemble(int32_t np, const float *const *anchors, const uint64_t 
   if (pass2)
     CK(launch_pass2_encode(raw, reinterpret_cast<const u64 *>(&ctl->raw_len), raw_len, payload,
                            workspace, ctl, st));
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
+int cszi_find_cuts(const uint8_t *bytes, uint64_t lo, uint64_t hi, int64_t *out, void *stream) {
+  if (!bytes || !out) return CSZI_E_INVALID_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  unsigned long long *fl = reinterpret_cast<unsigned long long *>(out + 2);  // scratch
+  const unsigned long long init[2] = {~0ull, 0ull};
+  cudaMemcpyAsync(fl, init, sizeof(init), cudaMemcpyHostToDevice, st);
+  if (hi > lo + 2) {
+    k_find_cuts<<<grid_for(hi - lo), 256, 0, st>>>(bytes, lo, hi, fl, fl + 1);
+    note_launch();
+  }
+  k_cuts_out<<<1, 1, 0, st>>>(fl, out);
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 

@@ -469,6 +469,11 @@ def compress_slabs_batch(batch: list, comm, backend=None, pass2: bool = True):
         host_keys = key0.cpu().numpy().astype(np.int64)
         _raise_nonfinite(host_keys)
     # (5) pieces to the root
+    if (pass2 and isinstance(backend, GpuSlabBackend) and allc_h.shape[1] > 1
+            and _pass2_split_pays(allc_h)):
+        got = _pass2_split(comm, backend, batch, allc_h, ranks, alphas)
+        if got != "fallback":
+            return got
     if hasattr(backend, "piece_nbytes") and bases is not None:
         return _gather_packed(comm, backend, batch, allc_h, bases, ranks, alphas, pass2)
     out = []
@@ -484,6 +489,195 @@ def compress_slabs_batch(batch: list, comm, backend=None, pass2: bool = True):
         nbits = [int(c[0]) for c in ck]
         out.append(backend.assemble(states[0], anchors, bits, nbits, oidx, oval, pass2, a))
     return None if out[0] is None else out
+
+
+# Distributed pass-2 pays once the bitstream is long enough that the root's
+# pass-2 encode (and the gather of raw pieces) outweighs a few host round
+# trips; PASS2_SPLIT_MIN_BYTES = 0 forces it (tests).
+PASS2_SPLIT_MIN_BYTES = 48 << 20
+
+
+def _pass2_split_pays(allc_h) -> bool:
+    bits = int(allc_h[:, :, 0].sum(axis=1).max())
+    return bits // 8 >= PASS2_SPLIT_MIN_BYTES
+
+
+def _pass2_split(comm, backend, batch, allc_h, ranks, alphas):
+    """Pass-2 encoded where the pieces live (pass2.py:30-67).
+
+    The zero-run codec has a segment boundary right after every run of >= 2
+    zero bytes that is followed by a nonzero byte, whatever precedes the run,
+    so the raw payload encodes piecewise to the same bytes when cut there.
+    Every slab r >= 1 finds the first such cut c_r in the bytes of its bit
+    piece that no neighbour shares (the last slab also the last cut e); slab
+    r encodes [c_r, c_{r+1}) (slab 0 from the payload start, with the anchor
+    and code-length sections in front; slab r borrows slab r+1's piece bytes
+    up to c_{r+1}, ORing the shared word), the root encodes the last slab's
+    bytes after e plus the outlier section, and concatenates.  Collectives
+    per batch: an all-gather of the cuts, an all-gather of the borrowed
+    prefixes, a gather of the anchors and a gather of the encoded pieces.
+    Returns the archives on the root, None elsewhere, or "fallback" (on every
+    rank alike) when a slab has no cut."""
+    t = _lib.torch()
+    lib = _lib.load()
+    st = _lib.stream_ptr()
+    from .pass2 import encode_device
+
+    K = len(batch)
+    W = allc_h.shape[1]
+    geo = []
+    for k in range(K):
+        nb = [int(allc_h[k][r][0]) for r in range(W)]
+        starts = [sum(nb[:r]) for r in range(W)]
+        total = sum(nb)
+        nbytes = (total + 7) // 8
+        gb = [4 * (starts[r] // 32) for r in range(W)]
+        ge = [gb[r] + 4 * ((starts[r] % 32 + nb[r] + 31) // 32) for r in range(W)]
+        geo.append((nb, total, nbytes, gb, ge))
+    # (1) cuts in the bytes no neighbour shares: the first word of a piece
+    # holds the previous piece's last bits, the last word the next piece's first
+    cuts = []
+    for k in range(K):
+        nb, total, nbytes, gb, ge = geo[k]
+        row = []
+        for i, r in enumerate(ranks):
+            out = t.full((4,), -1, dtype=t.int64, device="cuda")
+            if r > 0:
+                hi = (min(ge[r], nbytes) if r == W - 1 else ge[r] - 4) - gb[r]
+                bits = batch[k][i].scratch["bits"]
+                _lib.check(lib.cszi_find_cuts(_lib.ptr(bits), 4, max(hi, 4), _lib.ptr(out), st),
+                           "find_cuts")
+            row.append(out[:2])
+        cuts.append(row)
+    allcut = _batched(comm, cuts, "gather")
+    cut_h = t.stack([t.stack([c.reshape(-1) for c in ck]) for ck in allcut]).cpu().numpy()
+    c = [[0] * (W + 1) for _ in range(K)]
+    for k in range(K):
+        nb, total, nbytes, gb, ge = geo[k]
+        for r in range(1, W):
+            if cut_h[k][r][0] < 0:
+                return "fallback"
+            c[k][r] = gb[r] + int(cut_h[k][r][0])
+        last = int(cut_h[k][W - 1][1])
+        if last < 0 or gb[W - 1] + last < c[k][W - 1]:
+            return "fallback"
+        c[k][W] = gb[W - 1] + last  # the root encodes from here to the end
+    # (2) borrowed prefixes: slab r >= 1 lends bytes [gb_r, c_r) of its piece
+    plen = [[c[k][r] - geo[k][3][r] if r > 0 else 0 for r in range(W)] for k in range(K)]
+    pmax = max(max(p) for p in plen) or 1
+    lend = []
+    for i, r in enumerate(ranks):
+        buf = t.zeros(K * pmax, dtype=t.uint8, device="cuda")
+        for k in range(K):
+            if plen[k][r]:
+                buf[k * pmax:k * pmax + plen[k][r]] = batch[k][i].scratch["bits"][:plen[k][r]]
+        lend.append(buf)
+    lent = comm.allgather(lend)[0]  # list over ranks
+    # (3) anchors to the root (the root's piece carries the anchor section)
+    anc_local = [t.cat([backend.anchors(batch[k][i]).reshape(-1).view(t.uint8)
+                        for k in range(K)]) for i in range(len(ranks))]
+    na_b = [[backend.piece_nbytes(batch[0][0].extents, *_slab_of(batch, comm, r, W),
+                                  allc_h[k][r], 0)[0] for r in range(W)] for k in range(K)]
+    anc_got = comm.gather(anc_local, sizes=[sum(na_b[k][r] for k in range(K)) for r in range(W)])
+    # (4) each slab encodes its cut range
+    enc = []
+    for i, r in enumerate(ranks):
+        parts = []
+        for k in range(K):
+            nb, total, nbytes, gb, ge = geo[k]
+            s_ = batch[k][i]
+            a, e = c[k][r], c[k][r + 1]
+            seg = t.zeros(max(e - a, 0) + 8, dtype=t.uint8, device="cuda")
+            bits = s_.scratch["bits"]
+            lo, hi = max(a, gb[r]), min(e, ge[r])
+            if hi > lo:
+                seg[lo - a:hi - a] = bits[lo - gb[r]:hi - gb[r]]
+            if r + 1 < W and plen[k][r + 1]:
+                q0 = gb[r + 1]
+                pre = lent[r + 1][k * pmax:k * pmax + plen[k][r + 1]]
+                seg[q0 - a:q0 - a + pre.numel()].bitwise_or_(pre)
+            seg = seg[:max(e - a, 0)]
+            if r == 0:  # anchor section (every slab, lattice order) + code lengths in front
+                pieces = []
+                for rr in range(W):
+                    o = sum(na_b[kk][rr] for kk in range(k))
+                    pieces.append(anc_got[rr][o:o + na_b[k][rr]])
+                seg = t.cat(pieces + [s_.scratch["lengths"], seg])
+            out, m = encode_device(seg, int(seg.numel()))
+            parts.append(out[:m])
+        enc.append(parts)
+    # (5) encoded pieces, the last slab's tail bytes and the outliers to the root
+    packed = []
+    meta = []
+    for i, r in enumerate(ranks):
+        chunks = []
+        row = []
+        for k in range(K):
+            nb, total, nbytes, gb, ge = geo[k]
+            s_ = batch[k][i]
+            tail = s_.scratch["bits"][c[k][W] - gb[r]:nbytes - gb[r]] if r == W - 1 else \
+                s_.scratch["bits"][:0]
+            _, oi, ov = backend.pieces(s_, allc_h[k][r])
+            for x in (enc[i][k], tail, oi.reshape(-1).view(t.uint8), ov.reshape(-1).view(t.uint8)):
+                chunks.append(x)
+            row += [enc[i][k].numel(), tail.numel(), oi.numel()]
+        meta.append(t.tensor(row, dtype=t.int64, device="cuda").view(t.uint8))
+        packed.append(t.cat([meta[-1]] + chunks))
+    got = comm.gather(packed)
+    if got is None:
+        return None
+    out = []
+    for k in range(K):
+        s0 = batch[k][0]
+        nb, total, nbytes, gb, ge = geo[k]
+        encs, oidx, oval, tail = [], [], [], None
+        for r in range(W):
+            buf = got[r]
+            m = buf[:24 * K].clone().view(t.int64).cpu().numpy().reshape(K, 3)
+            o = 24 * K
+            for kk in range(K):
+                le, lt, no = (int(v) for v in m[kk])
+                if kk == k:
+                    encs.append(buf[o:o + le])
+                    if r == W - 1:
+                        tail = buf[o + le:o + le + lt]
+                    oidx.append(buf[o + le + lt:o + le + lt + 8 * no].clone().view(t.int64))
+                    oval.append(buf[o + le + lt + 8 * no:o + le + lt + 12 * no].clone()
+                                .view(t.float32))
+                o += le + lt + 12 * no
+        kt = sum(int(x.numel()) for x in oidx)
+        osec = t.empty(8 + 12 * kt, dtype=t.uint8, device="cuda")
+        idx = t.cat(oidx) if kt else t.zeros(1, dtype=t.int64, device="cuda")
+        val = t.cat(oval) if kt else t.zeros(1, dtype=t.float32, device="cuda")
+        _lib.check(lib.cszi_pack_outliers(_lib.ptr(idx), _lib.ptr(val), kt, _lib.ptr(osec), st),
+                   "pack_outliers")
+        last = t.cat([tail, osec])
+        tout, tm = encode_device(last, int(last.numel()))
+        payload = t.cat(encs + [tout[:tm]])
+        ctl = s0.scratch["ctl"]
+        cc = ctl.fetch()
+        if cc.flags & _lib.F_EB_NONPOSITIVE:
+            raise Inconsistent("absolute error bound must be positive")
+        if cc.flags & _lib.F_LENGTH_OVERFLOW:
+            raise LengthOverflow("a symbol would need more than 32 bits")
+        if cc.flags & _lib.F_EMPTY_HISTOGRAM:
+            raise EmptyHistogram("cannot build a codebook from all-zero counts")
+        na_total = sum(na_b[k][r] for r in range(W))
+        nbins = int(s0.scratch["lengths"].numel())
+        sec = (na_total, nbins, nbytes, 8 + 12 * kt)
+        header = pack_header(3, PREDICTOR_INTERP, EB_REL if s0.mode == "rel" else EB_ABS, True,
+                             0, ctl_variants(cc, 3), ctl_order(cc, 3), s0.radius, 8, s0.extents,
+                             float(s0.eb), float(cc.eb_abs), alphas[k], sec,
+                             int(payload.numel()))
+        out.append(DeviceArchive(header=header, payload=payload))
+    return out
+
+
+def _slab_of(batch, comm, r, W):
+    if isinstance(comm, SimComm):
+        s = batch[0][r]
+        return s.z0, s.z1
+    return slab_bounds(batch[0][0].extents[0], W)[r]
 
 
 def _raise_nonfinite(host_keys):

@@ -183,3 +183,30 @@ def test_torchcomm_gpu_backend_two_processes(tmp_path):
     assert r["b1"].tobytes() == P.compress(P.Grid(P.Dims(data.shape), data * np.float32(2.0)),
                                            1e-3)
     assert r["dec"].tobytes() == P.decompress(ref).data.tobytes()
+
+
+@pytest.mark.parametrize("shape,world", [((64, 48, 64), 2), ((100, 64, 96), 8), ((41, 30, 40), 3),
+                                         ((256, 96, 128), 4)])
+def test_distributed_pass2_is_byte_identical(shape, world, monkeypatch):
+    """Pass-2 encoded where the pieces live (cut after zero runs, prefixes
+    borrowed from the next slab, root tail + outliers): the archive equals
+    single-GPU compress, single snapshots and a batch."""
+    import torch
+
+    from paper_2312_05492_b200 import distributed as D
+
+    monkeypatch.setattr(D, "PASS2_SPLIT_MIN_BYTES", 0)
+    calls = []
+    orig = D._pass2_split
+    monkeypatch.setattr(D, "_pass2_split", lambda *a: calls.append(1) or orig(*a))
+    rng = np.random.default_rng(5)
+    for eb in (1e-3, 1e-5):
+        data = smooth_field(rng, shape) if eb == 1e-3 else noisy_field(rng, shape)
+        x = torch.from_numpy(data).cuda()
+        ref = P.compress(P.Grid(P.Dims(shape), data), eb)
+        assert D.compress_simulated(x, world, eb).to_bytes() == ref
+        batch = D.compress_simulated_batch([x, x * 1.5], world, eb)
+        assert batch[0].to_bytes() == ref
+        assert batch[1].to_bytes() == P.compress(P.Grid(P.Dims(shape), data * np.float32(1.5)),
+                                                 eb)
+    assert calls
