@@ -140,6 +140,14 @@ def _torchcomm_worker(rank, world, port, data, out_path):
         z0, z1 = slab_bounds(nz, world)[rank]
         x = torch.from_numpy(data[z0:min(z1 + 1, nz)].copy()).cuda()
         arch = compress_sharded(x, data.shape, z0, z1, 1e-3)
+        # the same with pass-2 encoded per slab (forced on this small field)
+        from paper_2312_05492_b200 import distributed as D
+
+        D.PASS2_SPLIT_MIN_BYTES = 0
+        arch_p2 = compress_sharded(x, data.shape, z0, z1, 1e-3)
+        D.PASS2_SPLIT_MIN_BYTES = 48 << 20
+        if rank == 0:
+            assert arch_p2.to_bytes() == arch.to_bytes()
         batch = compress_sharded_batch([x, x * 2.0], data.shape, z0, z1, 1e-3)
         blob = arch.to_bytes() if rank == 0 else None
         # every rank decodes its slab of the one archive
