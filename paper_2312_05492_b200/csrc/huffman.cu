@@ -9,6 +9,7 @@
 #include "common.cuh"
 
 namespace cszi {
+void launch_zero16(void *p, u64 bytes, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 // histogram of int32 codes (fine-grained API; the compress path bins inside
@@ -1645,7 +1646,7 @@ int launch_encode(int mode, const void *src, u64 n, int R, const uint8_t *length
   S.ch_out = S.ch_bits + nc;
   S.lane_pre = reinterpret_cast<uint16_t *>(S.ch_out + nc);
   S.nz_lane = reinterpret_cast<uint32_t *>(S.lane_pre + 32 * nc);
-  cudaMemsetAsync(p, 0, (size_t)(nt * 16 + 16), st);
+  launch_zero16(p, (u64)(nt * 16 + 16), st);  // (a kernel: no memset node in the graph)
   const int nbins = 2 * R;
   int sms = sm_count(), per_sm = 1;
   const size_t smem_c = sizeof(uint32_t) * (nbins + 2) + 16;
@@ -1781,7 +1782,7 @@ static void huff_sync_range(const Stream &s, const DecTables *G, const uint16_t 
                             cudaStream_t st, int iters = 3) {
   // iters is odd: the last iteration writes X (even iterations write X,
   // odd ones the scratch copy)
-  cudaMemsetAsync(S.nchg, 0, 64, st);
+  launch_zero16(S.nchg, 64, st);
   if (h1 <= h0) {
     cudaMemcpyAsync(&ctl->scratch[1], S.nchg, 4, cudaMemcpyDeviceToDevice, st);
     return;
@@ -1827,7 +1828,8 @@ static void huff_write(const Stream &s, const DecTables *G, const uint16_t *sort
   u64 *first_dead = misc + 2;
   u64 *total = misc + 3;
   void *scan_ws = carve(p, scan_scratch_bytes(M));
-  cudaMemsetAsync(first_dead, 0xff, 8, st);
+  k_set_u64<<<1, 1, 0, st>>>(first_dead, ~0ull);  // (a kernel: no memset node)
+  note_launch();
   const unsigned blocks = (unsigned)((M + 255) / 256);
   const unsigned dblocks = (unsigned)((M + DEC_NT - 1) / DEC_NT);
   launch_excl_scan_u32(K, M, off, total, scan_ws, st);

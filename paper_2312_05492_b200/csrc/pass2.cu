@@ -18,6 +18,7 @@
 #include "common.cuh"
 
 namespace cszi {
+void launch_zero16(void *p, u64 bytes, cudaStream_t st);
 
 u64 scan_scratch_bytes(u64 m);
 int launch_excl_scan_u32(const uint32_t *in, u64 m, u64 *out, u64 *total, void *scratch,
@@ -343,7 +344,7 @@ int launch_pass2_encode(const uint8_t *in, const u64 *Np, u64 cap_n, uint8_t *ou
   S.fs = reinterpret_cast<uint32_t *>(S.out_off + nc);
   S.rest = S.fs + nc;
   S.lit0 = reinterpret_cast<uint8_t *>(S.rest + nc);
-  cudaMemsetAsync(p, 0, (size_t)(nt * 16 + 16), st);
+  launch_zero16(p, (u64)(nt * 16 + 16), st);  // (a kernel: no memset node in the graph)
   int sms = sm_count(), per_sm = 1;
   per_sm = occupancy((const void *)k_p2_emit, P2_NT, 0);
   if (per_sm < 1) per_sm = 1;
