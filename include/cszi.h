@@ -323,6 +323,29 @@ int cszi_decompress_write_window(const uint8_t *payload, uint64_t payload_len, i
                                  const uint64_t sec_len[4], const cszi_geom *g, int32_t radius,
                                  const uint64_t *X, uint32_t *K, const uint8_t *D,
                                  void *workspace, uint64_t ws_bytes, cszi_ctl *ctl, void *stream);
+/* Pass-2 decode split by 1 KiB chunks of the encoded payload (sharded
+ * decompress): tables of chunks [c0, c1) into full-length arrays (M =
+ * cszi_p2d_chunks(n); tab: M x 129 bytes, ctab: M x 129 uint32); the caller
+ * all-gathers them; cszi_p2d_resolve (every rank: chain, counts, scan ->
+ * E, cnt, off of M entries, ctl->raw_len); cszi_p2d_expand writes the raw
+ * bytes of chunks [c0, c1) at their offsets (only the ranges a rank needs).
+ * cszi_decompress_raw_offset: where the workspace's raw buffer starts;
+ * cszi_decompress_prologue_raw: the prologue for a raw payload already
+ * expanded there (ctl reset + code tables). */
+uint64_t cszi_p2d_chunks(uint64_t n);
+uint64_t cszi_p2d_resolve_scratch_size(uint64_t n);
+int cszi_p2d_tables(const uint8_t *in, uint64_t n, uint64_t c0, uint64_t c1, uint8_t *tab,
+                    uint32_t *ctab, void *stream);
+int cszi_p2d_resolve(const uint8_t *tab, const uint32_t *ctab, uint64_t n, uint8_t *E,
+                     uint32_t *cnt, uint64_t *off, void *scratch, cszi_ctl *ctl, void *stream);
+int cszi_p2d_expand(const uint8_t *in, uint64_t n, const uint8_t *E, const uint64_t *off,
+                    const uint32_t *cnt, uint64_t c0, uint64_t c1, uint8_t *out, uint64_t cap,
+                    cszi_ctl *ctl, void *stream);
+uint64_t cszi_decompress_raw_offset(const cszi_geom *g, int32_t radius,
+                                    const uint64_t sec_len[4], uint64_t payload_len);
+int cszi_decompress_prologue_raw(uint64_t payload_len, const uint64_t sec_len[4],
+                                 const cszi_geom *g, int32_t radius, void *workspace,
+                                 uint64_t ws_bytes, cszi_ctl *ctl, void *stream);
 int cszi_decompress_epilogue(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
                              const uint64_t sec_len[4], const cszi_geom *g, int32_t radius,
                              const double *level_eb, int32_t nlev, const int32_t variant[3],

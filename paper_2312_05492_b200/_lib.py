@@ -172,6 +172,14 @@ _SIGS = {
     "cszi_decompress_prologue": (ctypes.c_int, [_vp, _u64, _i32, _vp, _vp, _i32, _vp, _u64, _vp,
                                                 _vp]),
     "cszi_huff_chunks": (_u64, [_u64]),
+    "cszi_p2d_chunks": (_u64, [_u64]),
+    "cszi_p2d_resolve_scratch_size": (_u64, [_u64]),
+    "cszi_p2d_tables": (ctypes.c_int, [_vp, _u64, _u64, _u64, _vp, _vp, _vp]),
+    "cszi_p2d_resolve": (ctypes.c_int, [_vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "cszi_p2d_expand": (ctypes.c_int, [_vp, _u64, _vp, _vp, _vp, _u64, _u64, _vp, _u64, _vp,
+                                       _vp]),
+    "cszi_decompress_raw_offset": (_u64, [_vp, _i32, _vp, _u64]),
+    "cszi_decompress_prologue_raw": (ctypes.c_int, [_u64, _vp, _vp, _i32, _vp, _u64, _vp, _vp]),
     "cszi_find_cuts": (ctypes.c_int, [_vp, _u64, _u64, _vp, _vp]),
     "cszi_decompress_sync_range": (ctypes.c_int, [_vp, _u64, _i32, _vp, _vp, _i32, _u64, _u64,
                                                   _u64, _vp, _vp, _vp, _vp, _vp, _u64, _vp, _vp]),

@@ -60,6 +60,15 @@ int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *de
                   void *out, int out_kind, void *scratch, cszi_ctl *ctl, cudaStream_t st,
                   int table_mode, int lmax, u64 w0, u64 w1);
 u64 huff_chunks(u64 nbytes);
+u64 p2d_chunks(u64 n);
+u64 p2d_resolve_scratch_bytes(u64 n);
+int launch_p2d_tables_range(const uint8_t *in, u64 n, u64 c0, u64 c1, uint8_t *tab,
+                            uint32_t *ctab, cudaStream_t st);
+int launch_p2d_resolve(const uint8_t *tab, const uint32_t *ctab, u64 n, uint8_t *E,
+                       uint32_t *cnt, u64 *off, void *scratch, cszi_ctl *ctl, cudaStream_t st);
+int launch_p2d_expand_range(const uint8_t *in, u64 n, const uint8_t *E, const u64 *off,
+                            const uint32_t *cnt, u64 c0, u64 c1, uint8_t *out, u64 cap,
+                            cszi_ctl *ctl, cudaStream_t st);
 int launch_huff_sync_range(const uint8_t *bytes, u64 nbytes, const void *dec_tables, u64 h0,
                            u64 h1, u64 entry, u64 *X, uint32_t *K, uint8_t *D, u64 *entry_used,
                            void *scratch, cszi_ctl *ctl, cudaStream_t st);
@@ -716,6 +725,57 @@ int cszi_decompress_prologue(const uint8_t *payload, uint64_t payload_len, int32
 }
 
 uint64_t cszi_huff_chunks(uint64_t nbytes) { return huff_chunks(nbytes); }
+
+// the prologue for a raw payload already expanded into the workspace (the
+// pass-2 decode split across ranks): ctl reset + code tables
+int cszi_decompress_prologue_raw(uint64_t payload_len, const uint64_t sec_len[4],
+                                 const cszi_geom *g, int32_t radius, void *workspace,
+                                 uint64_t ws_bytes, cszi_ctl *ctl, void *stream) {
+  if (!sec_len || !g || !ctl) return CSZI_E_INVALID_ARG;
+  CK(check_geom(g, radius));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  DecompressWS W;
+  if (ws_bytes < layout_decompress(g, radius, reinterpret_cast<const u64 *>(sec_len), payload_len,
+                                   1, workspace, &W))
+    return CSZI_E_CAPACITY;
+  const u64 nbins = 2 * (u64)radius;
+  if (sec_len[1] != nbins) return CSZI_E_MALFORMED;
+  CK(launch_ctl_init(ctl, st));
+  CK(launch_canonical(W.raw + sec_len[0], (int)nbins, nullptr, W.dec_tables, ctl, st, 0));
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
+uint64_t cszi_decompress_raw_offset(const cszi_geom *g, int32_t radius,
+                                    const uint64_t sec_len[4], uint64_t payload_len) {
+  DecompressWS W;
+  unsigned char *base = reinterpret_cast<unsigned char *>((uintptr_t)4096);
+  layout_decompress(g, radius, reinterpret_cast<const u64 *>(sec_len), payload_len, 1, base, &W);
+  return (uint64_t)(W.raw - base);
+}
+
+uint64_t cszi_p2d_chunks(uint64_t n) { return p2d_chunks(n); }
+uint64_t cszi_p2d_resolve_scratch_size(uint64_t n) { return p2d_resolve_scratch_bytes(n); }
+
+int cszi_p2d_tables(const uint8_t *in, uint64_t n, uint64_t c0, uint64_t c1, uint8_t *tab,
+                    uint32_t *ctab, void *stream) {
+  if (!in || !tab || !ctab) return CSZI_E_INVALID_ARG;
+  return launch_p2d_tables_range(in, n, c0, c1, tab, ctab, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int cszi_p2d_resolve(const uint8_t *tab, const uint32_t *ctab, uint64_t n, uint8_t *E,
+                     uint32_t *cnt, uint64_t *off, void *scratch, cszi_ctl *ctl, void *stream) {
+  if (!tab || !ctab || !E || !cnt || !off || !scratch || !ctl) return CSZI_E_INVALID_ARG;
+  return launch_p2d_resolve(tab, ctab, n, E, cnt, reinterpret_cast<u64 *>(off), scratch, ctl,
+                            reinterpret_cast<cudaStream_t>(stream));
+}
+
+int cszi_p2d_expand(const uint8_t *in, uint64_t n, const uint8_t *E, const uint64_t *off,
+                    const uint32_t *cnt, uint64_t c0, uint64_t c1, uint8_t *out, uint64_t cap,
+                    cszi_ctl *ctl, void *stream) {
+  if (!in || !E || !off || !cnt || !out || !ctl) return CSZI_E_INVALID_ARG;
+  return launch_p2d_expand_range(in, n, E, reinterpret_cast<const u64 *>(off), cnt, c0, c1, out,
+                                 cap, ctl, reinterpret_cast<cudaStream_t>(stream));
+}
 
 int cszi_decompress_sync_range(const uint8_t *payload, uint64_t payload_len, int32_t pass2,
                                const uint64_t sec_len[4], const cszi_geom *g, int32_t radius,

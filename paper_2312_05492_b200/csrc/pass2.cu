@@ -367,11 +367,13 @@ constexpr int P2D_D = 129;           // entry offsets 0..128
 constexpr int P2D_P = P2D_C + 130;   // local positions incl. spill
 constexpr uint32_t OVR = 0x80000000u;
 
+// (chunk jbase + blockIdx.x: a range of the stream's chunks)
 __global__ void __launch_bounds__(256) k_p2d_tables(const uint8_t *__restrict__ in, u64 n,
-                                                    uint8_t *tab, uint32_t *ctab) {
+                                                    uint8_t *tab, uint32_t *ctab, u64 jbase) {
   __shared__ uint16_t nx[2][P2D_P];
   __shared__ uint32_t ct[2][P2D_P];
-  const u64 c0 = (u64)blockIdx.x * P2D_C;
+  const u64 jb = jbase + blockIdx.x;
+  const u64 c0 = jb * P2D_C;
   const int clen = (int)min((u64)P2D_C, n - c0);
   for (int p = threadIdx.x; p < P2D_P; p += blockDim.x) {
     uint16_t x;
@@ -412,8 +414,8 @@ __global__ void __launch_bounds__(256) k_p2d_tables(const uint8_t *__restrict__ 
   }
   for (int e = threadIdx.x; e < P2D_D; e += blockDim.x) {
     const int x = nx[cur][e];
-    tab[(u64)blockIdx.x * P2D_D + e] = (uint8_t)(x >= P2D_C ? x - P2D_C : 0);
-    ctab[(u64)blockIdx.x * P2D_D + e] = ct[cur][e];
+    tab[jb * P2D_D + e] = (uint8_t)(x >= P2D_C ? x - P2D_C : 0);
+    ctab[jb * P2D_D + e] = ct[cur][e];
   }
 }
 
@@ -441,9 +443,9 @@ __global__ void __launch_bounds__(P2X_WPB * 32) k_p2d_expand(const uint8_t *__re
                                                             const u64 *off,
                                                             const uint32_t *cnt,
                                                             uint8_t *__restrict__ out, u64 cap,
-                                                            u64 M, cszi_ctl *ctl) {
+                                                            u64 M, cszi_ctl *ctl, u64 jbase) {
   const int lane = threadIdx.x & 31;
-  const u64 j = (u64)blockIdx.x * P2X_WPB + (threadIdx.x >> 5);
+  const u64 j = jbase + (u64)blockIdx.x * P2X_WPB + (threadIdx.x >> 5);
   if (j >= M) return;
   const u64 c0 = j * P2D_C;
   const u64 cend = min(c0 + P2D_C, n);  // controls start below cend
@@ -579,7 +581,7 @@ int launch_pass2_decode(const uint8_t *in, u64 n, uint8_t *out, u64 cap, void *s
   u64 *off = reinterpret_cast<u64 *>(carve2(p, M * 8));
   void *chain_ws = carve2(p, chain_scratch_bytes(M, P2D_D));
   void *scan_ws = carve2(p, scan_scratch_bytes(M));
-  k_p2d_tables<<<(unsigned)M, 256, 0, st>>>(in, n, tab, ctab);
+  k_p2d_tables<<<(unsigned)M, 256, 0, st>>>(in, n, tab, ctab, 0);
   note_launch();
   launch_chain_resolve(tab, M, P2D_D, 0, E, chain_ws, st);
   k_p2d_counts<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(M, E, ctab, cnt, ctl);
@@ -587,7 +589,55 @@ int launch_pass2_decode(const uint8_t *in, u64 n, uint8_t *out, u64 cap, void *s
   launch_excl_scan_u32(cnt, M, off, reinterpret_cast<u64 *>(&ctl->raw_len), scan_ws, st);
   if (expand) {
     k_p2d_expand<<<(unsigned)((M + P2X_WPB - 1) / P2X_WPB), P2X_WPB * 32, 0, st>>>(
-        in, n, E, off, cnt, out, cap, M, ctl);
+        in, n, E, off, cnt, out, cap, M, ctl, 0);
+    note_launch();
+  }
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
+// ---- split decode (sharded decompress): chunk ranges per rank -------------
+u64 p2d_chunks(u64 n) { return n ? (n + P2D_C - 1) / P2D_C : 0; }
+u64 p2d_resolve_scratch_bytes(u64 n) {
+  const u64 M = p2d_chunks(n) + 1;
+  return chain_scratch_bytes(M, P2D_D) + scan_scratch_bytes(M) + 512;
+}
+
+int launch_p2d_tables_range(const uint8_t *in, u64 n, u64 c0, u64 c1, uint8_t *tab,
+                            uint32_t *ctab, cudaStream_t st) {
+  const u64 M = p2d_chunks(n);
+  if (c1 > M) c1 = M;
+  if (c1 > c0) {
+    k_p2d_tables<<<(unsigned)(c1 - c0), 256, 0, st>>>(in, n, tab, ctab, c0);
+    note_launch();
+  }
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
+int launch_p2d_resolve(const uint8_t *tab, const uint32_t *ctab, u64 n, uint8_t *E,
+                       uint32_t *cnt, u64 *off, void *scratch, cszi_ctl *ctl, cudaStream_t st) {
+  const u64 M = p2d_chunks(n);
+  if (M == 0) {
+    cudaMemsetAsync(&ctl->raw_len, 0, 8, st);
+    return CSZI_OK;
+  }
+  unsigned char *p = reinterpret_cast<unsigned char *>(scratch);
+  void *chain_ws = carve2(p, chain_scratch_bytes(M, P2D_D));
+  void *scan_ws = carve2(p, scan_scratch_bytes(M));
+  launch_chain_resolve(tab, M, P2D_D, 0, E, chain_ws, st);
+  k_p2d_counts<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(M, E, ctab, cnt, ctl);
+  note_launch();
+  launch_excl_scan_u32(cnt, M, off, reinterpret_cast<u64 *>(&ctl->raw_len), scan_ws, st);
+  return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
+}
+
+int launch_p2d_expand_range(const uint8_t *in, u64 n, const uint8_t *E, const u64 *off,
+                            const uint32_t *cnt, u64 c0, u64 c1, uint8_t *out, u64 cap,
+                            cszi_ctl *ctl, cudaStream_t st) {
+  const u64 M = p2d_chunks(n);
+  if (c1 > M) c1 = M;
+  if (c1 > c0) {
+    k_p2d_expand<<<(unsigned)((c1 - c0 + P2X_WPB - 1) / P2X_WPB), P2X_WPB * 32, 0, st>>>(
+        in, n, E, off, cnt, out, cap, c1, ctl, c0);
     note_launch();
   }
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;

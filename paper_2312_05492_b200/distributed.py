@@ -875,6 +875,129 @@ def split_pays(data, world: int) -> bool:
     return M * (world - 1) // world >= SPLIT_MIN_SAVED_CHUNKS
 
 
+# The pass-2 decode of the payload splits as well once the payload is long
+# (each rank: 1/world of the chunk tables, one all-gather, the chain resolve,
+# and only the raw ranges it reads); PASS2 decode of a 2.7 MB payload takes
+# ~100 us on one B200.
+P2D_SPLIT_MIN_BYTES = 8 << 20
+
+
+class _SplitPass2:
+    """Pass-2 decode split by the encoded payload's 1 KiB chunks: tables of
+    this rank's chunks, all-gathered; the chain resolve and the count scan on
+    every rank; then each slab expands only the raw byte ranges it reads
+    (its anchor planes, the code lengths, the bitstream of its Huffman chunk
+    range and later of its symbol window, the outlier section)."""
+
+    def __init__(self, plan, S, slabs, comm, world, hper):
+        t = _lib.torch()
+        lib = self.lib = _lib.load()
+        st = _lib.stream_ptr()
+        self.plan = plan
+        n = plan["plen"]
+        self.n = n
+        Mp = self.Mp = int(lib.cszi_p2d_chunks(n))
+        perp = -(-Mp // world)
+        D = 129
+        tab = t.empty(Mp * D, dtype=t.uint8, device="cuda")
+        ctab = t.empty(Mp * D, dtype=t.int32, device="cuda")
+        pay = _lib.ptr(plan["payload"])
+        shares = []
+        for (r, _, _) in slabs:
+            p0, p1 = min(Mp, r * perp), min(Mp, (r + 1) * perp)
+            _lib.check(lib.cszi_p2d_tables(pay, n, p0, p1, _lib.ptr(tab), _lib.ptr(ctab), st),
+                       "p2d_tables")
+            # share: the uint32 table first (4-byte aligned views), then the bytes
+            sh = t.zeros(perp * 5 * D, dtype=t.uint8, device="cuda")
+            if p1 > p0:
+                sh[:(p1 - p0) * 4 * D] = ctab[p0 * D:p1 * D].view(t.uint8)
+                sh[perp * 4 * D:perp * 4 * D + (p1 - p0) * D] = tab[p0 * D:p1 * D]
+            shares.append(sh)
+        got = comm.allgather(shares)[0]
+        for r, g in enumerate(got):
+            p0, p1 = min(Mp, r * perp), min(Mp, (r + 1) * perp)
+            if p1 > p0:
+                ctab[p0 * D:p1 * D] = g[:(p1 - p0) * 4 * D].view(t.int32)
+                tab[p0 * D:p1 * D] = g[perp * 4 * D:perp * 4 * D + (p1 - p0) * D]
+        self.E = t.empty(Mp, dtype=t.uint8, device="cuda")
+        self.cnt = t.empty(Mp, dtype=t.int32, device="cuda")
+        self.off = t.empty(Mp, dtype=t.int64, device="cuda")
+        ws = t.empty(int(lib.cszi_p2d_resolve_scratch_size(n)), dtype=t.uint8, device="cuda")
+        ctl = S[0].ctl
+        _lib.check(lib.cszi_ctl_init(ctl.ptr, st), "ctl_init")
+        _lib.check(lib.cszi_p2d_resolve(_lib.ptr(tab), _lib.ptr(ctab), n, _lib.ptr(self.E),
+                                        _lib.ptr(self.cnt), _lib.ptr(self.off), _lib.ptr(ws),
+                                        ctl.ptr, st), "p2d_resolve")
+        c = ctl.fetch()
+        h = plan["h"]
+        self.raw_len = sum(h.sec_lens)
+        self.ok = (int(c.raw_len) == self.raw_len and not (c.flags & _lib.F_P2_CORRUPT))
+        self.off_h = self.off.cpu().numpy().tolist()
+        sec = h.sec_lens
+        self.head = sec[0] + sec[1]
+        if not self.ok:
+            return
+        ny, nx = plan["extents"][1], plan["extents"][2]
+        nz = plan["extents"][0]
+        na1 = (ny - 1) // 8 + 1 + (1 if (ny - 1) % 8 else 0)
+        na2 = (nx - 1) // 8 + 1 + (1 if (nx - 1) % 8 else 0)
+        zl = list(range(0, nz, 8)) + ([nz - 1] if (nz - 1) % 8 else [])
+        for s in S:
+            rngs = [(sec[0], self.head),                                     # code lengths
+                    (self.head + sec[2], self.raw_len)]                      # outlier section
+            if s.z1 > s.z0:  # the anchor planes of the slab and its closing plane
+                top = min(s.z1, nz - 1)
+                k0 = s.z0 // 8
+                k1 = max(i for i, zc in enumerate(zl) if zc <= top)
+                rngs.append((4 * k0 * na1 * na2, 4 * (k1 + 1) * na1 * na2))
+            if s.h1 > s.h0:  # the bitstream of the Huffman range (+ one chunk each side)
+                rngs.append((self.head + max(0, (s.h0 - 1) * 32 - 8),
+                             self.head + min(sec[2], (s.h1 + 1) * 32 + 16)))
+            self._expand(s, rngs)
+
+    def _expand(self, s, rngs):
+        import bisect
+
+        lib = self.lib
+        raw = s.ws[int(lib.cszi_decompress_raw_offset(ctypes.byref(s.geom), self.plan["R"],
+                                                      self.plan["sec"], self.n)):]
+        cap = self.raw_len + 64
+        for lo, hi in rngs:
+            if hi <= lo:
+                continue
+            ja = max(0, bisect.bisect_right(self.off_h, lo) - 1)
+            jb = bisect.bisect_left(self.off_h, hi)
+            _lib.check(lib.cszi_p2d_expand(_lib.ptr(self.plan["payload"]), self.n,
+                                           _lib.ptr(self.E), _lib.ptr(self.off),
+                                           _lib.ptr(self.cnt), ja, jb, _lib.ptr(raw), cap,
+                                           s.ctl.ptr, _lib.stream_ptr()), "p2d_expand")
+
+    def expand_windows(self, S, X, K, plan):
+        """The bitstream bytes of the chunks holding each slab's symbol window
+        (plus its halo plane), known once the chunk records are gathered."""
+        t = _lib.torch()
+        ny, nx = plan["extents"][1], plan["extents"][2]
+        nz = plan["extents"][0]
+        nb = plan["h"].sec_lens[2]
+        for s, x, k in zip(S, X, K):
+            if s.z1 <= s.z0:
+                continue
+            w0, w1 = s.z0 * ny * nx, min(s.z1 + 1, nz) * ny * nx
+            cum = t.cumsum(k.to(t.int64), 0)
+            ja = int(t.searchsorted(cum, t.tensor([w0], device=cum.device), right=True).item())
+            jb = int(t.searchsorted(cum - k.to(t.int64), t.tensor([w1], device=cum.device)).item())
+            jb = max(jb - 1, ja)
+            b_lo = int(x[ja - 1].item()) if ja > 0 else 0
+            b_hi = int(x[min(jb, x.numel() - 1)].item())
+            self._expand(s, [(self.head + max(0, b_lo // 8 - 8),
+                              self.head + min(nb, b_hi // 8 + 16))])
+
+
+def _split_pass2_decode(plan, S, slabs, comm, world, hper):
+    p2 = _SplitPass2(plan, S, slabs, comm, world, hper)
+    return p2 if p2.ok else None
+
+
 def decompress_slabs_split(data, slabs, comm, world: int):
     """Sharded decompress with the Huffman synchronisation split by chunk
     ranges: this process's slabs [(rank, z0, z1), ...] each synchronise
@@ -900,9 +1023,20 @@ def decompress_slabs_split(data, slabs, comm, world: int):
     X = [t.zeros(M, dtype=t.int64, device="cuda") for _ in S]
     K = [t.zeros(M, dtype=t.int32, device="cuda") for _ in S]
     D = [t.zeros(M, dtype=t.uint8, device="cuda") for _ in S]
+    p2 = None
+    if plan["pass2"] and plan["plen"] >= P2D_SPLIT_MIN_BYTES:
+        p2 = _split_pass2_decode(plan, S, slabs, comm, world, per)
+        if p2 is None:
+            return None  # raw length mismatch: the single-rank path raises it
     for s, x, k, d in zip(S, X, K, D):
-        _lib.check(lib.cszi_decompress_prologue(*args(s), _lib.ptr(s.ws), s.ws.numel(), s.ctl.ptr,
-                                                st), "decompress_prologue")
+        if p2 is None:
+            _lib.check(lib.cszi_decompress_prologue(*args(s), _lib.ptr(s.ws), s.ws.numel(),
+                                                    s.ctl.ptr, st), "decompress_prologue")
+        else:
+            _lib.check(lib.cszi_decompress_prologue_raw(plan["plen"], plan["sec"],
+                                                        ctypes.byref(s.geom), plan["R"],
+                                                        _lib.ptr(s.ws), s.ws.numel(), s.ctl.ptr,
+                                                        st), "decompress_prologue_raw")
     entries = [None] * len(S)  # None: speculative entry
     for _round in range(world + 1):
         for i, (s, x, k, d) in enumerate(zip(S, X, K, D)):
@@ -943,6 +1077,8 @@ def decompress_slabs_split(data, slabs, comm, world: int):
         if int(t.stack(moved).max().item()) == 0:
             break
         entries = [int(xa[s.h0 - 1].item()) if int(f.item()) else None for s, f in zip(S, flags)]
+    if p2 is not None:  # the bit ranges of each slab's symbol window
+        p2.expand_windows(S, X, K, plan)
     out = []
     for s, x, k, d in zip(S, X, K, D):
         c = s.ctl.fetch()

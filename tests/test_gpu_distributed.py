@@ -218,3 +218,28 @@ def test_distributed_pass2_is_byte_identical(shape, world, monkeypatch):
         assert batch[1].to_bytes() == P.compress(P.Grid(P.Dims(shape), data * np.float32(1.5)),
                                                  eb)
     assert calls
+
+
+@pytest.mark.parametrize("shape,world,eb", [((64, 64, 64), 2, 1e-3), ((96, 40, 64), 8, 1e-5),
+                                            ((256, 128, 128), 4, 1e-4), ((41, 30, 37), 3, 1e-3)])
+def test_split_decompress_with_split_pass2(shape, world, eb, monkeypatch):
+    """The pass-2 decode split as well (tables per rank, all-gathered; each
+    slab expands only the raw ranges it reads): still bit-identical."""
+    import torch
+
+    from paper_2312_05492_b200 import distributed as D
+
+    monkeypatch.setattr(D, "P2D_SPLIT_MIN_BYTES", 0)
+    made = []
+    orig = D._split_pass2_decode
+    monkeypatch.setattr(D, "_split_pass2_decode", lambda *a: made.append(1) or orig(*a))
+    rng = np.random.default_rng(13)
+    data = noisy_field(rng, shape)
+    arch = P.compress_device(P.Grid(P.Dims(shape), torch.from_numpy(data).cuda()), eb)
+    whole = P.decompress_device(arch).tensor
+    bounds = D.slab_bounds(shape[0], world)
+    got = D.decompress_slabs_split(arch, [(r, z0, z1) for r, (z0, z1) in enumerate(bounds)],
+                                   D.SimComm(world), world)
+    assert got is not None and made
+    for (z0, z1, y), (b0, b1) in zip(got, bounds):
+        assert torch.equal(y.reshape(-1), whole[z0:z1].reshape(-1))
