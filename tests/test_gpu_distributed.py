@@ -159,6 +159,9 @@ def _torchcomm_worker(rank, world, port, data, out_path):
         # the chunk-range split of the Huffman synchronisation over TorchComm
         got = decompress_slabs_split(obj[0], [(rank, z0, z1)], TorchComm(), world)
         assert got is not None and torch.equal(got[0][2], ys)
+        D.P2D_SPLIT_MIN_BYTES = 0  # and with the pass-2 decode split too
+        got = decompress_slabs_split(obj[0], [(rank, z0, z1)], TorchComm(), world)
+        assert got is not None and torch.equal(got[0][2], ys)
         if rank == 0:
             np.savez(out_path, blob=np.frombuffer(blob, dtype=np.uint8),
                      b0=np.frombuffer(batch[0].to_bytes(), dtype=np.uint8),
