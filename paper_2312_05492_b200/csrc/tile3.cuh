@@ -380,7 +380,7 @@ DEV double chain4(double w0, double w1, double w2, double w3, double a, double b
 
 // interior lines: compile-time case pattern; edge tiles: case from the true
 // extent (warp-uniform), weights from c_w.  cs < 0: interior.
-template <int NP, bool BND>
+template <int NP, bool BND, bool SW = false>
 DEV double pred_k(int k, int cs, double wo, double wi, double a, double b, double c, double d) {
   if (!BND) {
     if (NP == 1) return p_lin(b, c);
@@ -389,6 +389,19 @@ DEV double pred_k(int k, int cs, double wo, double wi, double a, double b, doubl
     return chain4(wo, wi, wi, wo, a, b, c, d);
   }
   if (cs == 0) return chain4(wo, wi, wi, wo, a, b, c, d);
+  if (SW) {
+    // compress edge tiles: the case is warp-uniform; its weights are
+    // compile-time per branch (the c_w rows, with the zero-weight terms
+    // dropped: they only change the sign of an exact zero, as in the
+    // interior walks).  (Measured: predict -8 us on 512^3; the reconstructor
+    // is faster with the table.)
+    switch (cs) {
+      case 1: return p_m3(a, b, c);
+      case 2: return p_p3(b, c, d);
+      case 3: return p_lin(b, c);
+      default: return b;
+    }
+  }
   return chain4(c_w[cs][0], c_w[cs][1], c_w[cs][2], c_w[cs][3], a, b, c, d);
 }
 
@@ -475,8 +488,8 @@ DEV void walk_x(const Tile &T, int stz, int sty, double wo, double wi, const Lv 
         cs = case_of(pd, S, TX, T.e[2]);
         if (row_anchor && pd == T.e[2] - 1) keep |= 1u << k;
       }
-      const double pr = pred_k<NP, BND>(k, cs, wo, wi, k > 0 ? ev[k - 1] : 0.0, ev[k], ev[k + 1],
-                                   k + 2 <= NP ? ev[k + 2] : 0.0);
+      const double pr = pred_k<NP, BND, MODE == 0>(k, cs, wo, wi, k > 0 ? ev[k - 1] : 0.0, ev[k],
+                                                   ev[k + 1], k + 2 <= NP ? ev[k + 2] : 0.0);
       if (MODE == 0) {
         if (!quant_fast(pr, pt[k], L, Rd, R, rec[k], code[k])) fail |= 1u << k;
       } else {
@@ -624,8 +637,9 @@ DEV void walk_col(const Tile &T, int sta, double wo, double wi, const Lv &L, int
       }
 #pragma unroll
       for (int e = 0; e < NE; ++e) {
-        const double pr = pred_k<NP, BND>(k, cs, wo, wi, k > 0 ? ev[e][k - 1] : 0.0, ev[e][k],
-                                     ev[e][k + 1], k + 2 <= NP ? ev[e][k + 2] : 0.0);
+        const double pr = pred_k<NP, BND, MODE == 0>(k, cs, wo, wi, k > 0 ? ev[e][k - 1] : 0.0,
+                                                     ev[e][k], ev[e][k + 1],
+                                                     k + 2 <= NP ? ev[e][k + 2] : 0.0);
         if (MODE == 0) {
           if (!quant_fast(pr, pt[e][k], L, Rd, R, rec[e][k], code[e][k]))
             fail |= 1u << (e * NP + k);
@@ -758,14 +772,10 @@ DEV void run_levels(const Tile &T, const Cfg &C, int R, bool exact, const Out &O
 #pragma unroll 1
     for (int i = 0; i < 3; ++i) {
       const int D = C.order[i];
-      T3P_CLOCK(q0);
       run_pass<MODE, BND>(T, s, D, passed, C.nak[D] != 0, L, R, exact, O);
       passed |= 1 << D;
       __syncwarp();
-#ifdef T3_PROF
-      if (MODE == 0 && !BND && (threadIdx.x & 31) == 0)
-        atomicAdd(&g_t3_prof[6 + lv * 3 + i], (unsigned long long)(clock64() - q0));
-#endif
+
     }
   }
 }

@@ -463,6 +463,9 @@ DEV void ilevel(const Tile &T, const Cfg &C, int lv, int R, const Out &O) {
   int passed = 0;
 #pragma unroll 1
   for (int i = 0; i < 3; ++i) {
+#ifdef T3_PROF
+    const long long q0 = clock64();
+#endif
     if (MODE == 0) {
       ipass_pc<MODE, S>(T, C.pc[i], L, R, O);
     } else {
@@ -472,6 +475,10 @@ DEV void ilevel(const Tile &T, const Cfg &C, int lv, int R, const Out &O) {
       passed |= 1 << D;
     }
     __syncwarp();
+#ifdef T3_PROF
+    if (MODE == 0 && (threadIdx.x & 31) == 0)
+      atomicAdd(&g_t3_prof[6 + lv * 3 + i], (unsigned long long)(clock64() - q0));
+#endif
   }
 }
 
