@@ -223,6 +223,11 @@ DEV uint32_t lds_u16(uint32_t a) {
 DEV void sts_u16(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
 }
+DEV uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
 DEV uint2 lds_u2(uint32_t a) {
   uint2 v;
   asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
@@ -1066,6 +1071,12 @@ __global__ void T3P_BOUNDS
     if (T.bnd || exact) run_levels<0, true>(T, C, R, exact, O);
     else run_levels_i<0>(T, C, R, O);
     T3P_CLOCK(c3);
+#ifdef T3_PROF
+    if (T.bnd && lane == 0) {  // [5] edge tiles, [15] their pass cycles
+      atomicAdd(&g_t3_prof[5], 1ull);
+      atomicAdd(&g_t3_prof[15], (unsigned long long)(c3 - c2));
+    }
+#endif
     // staging buffer free: prefetch the next tile
     const int tn = ticket_read(S, raw);
     int on[3] = {0, 0, 0};
@@ -1128,6 +1139,42 @@ __global__ void T3P_BOUNDS
           const int row = lane + 32 * h;
           const uint32_t wd = nzs[row];
           if (wd) nzmap[(gbase + (row >> 3) * pz + (int64_t)(row & 7) * py) >> 5] = wd;
+        }
+      }
+    } else if (!nzmap) {
+      // (rows not 16-byte aligned, e.g. nx = 235 / 69) two rows per step:
+      // half-warp h takes row (z, y0 + h), lane pair x = 2 (lane % 16) + {0, 1};
+      // one 4-byte store when the pair is 4-byte aligned in global memory
+      // (the row base parity), two 2-byte stores otherwise
+      const int h = lane >> 4, xl = 2 * (lane & 15);
+      const bool a0 = xl < O2, a1 = xl + 1 < O2;
+      for (int z = 0; z < O0; ++z) {
+        const int64_t gz = gbase + (int64_t)z * pz + xl;
+        for (int y0 = 0; y0 < O1; y0 += 2) {
+          const int y = y0 + h;
+          const bool v0 = a0 && y < O1, v1 = a1 && y < O1;
+          const uint32_t w = v0 ? lds_u32(codea(T, z, y, xl)) : rr;
+          const uint32_t s0 = w & 0xffffu, s1 = w >> 16;
+          uint16_t *g = sym + gz + (int64_t)y * py;
+          if (v1 && !(reinterpret_cast<uintptr_t>(g) & 3)) {
+            *reinterpret_cast<uint32_t *>(g) = w;
+          } else {
+            if (v0) g[0] = (uint16_t)s0;
+            if (v1) g[1] = (uint16_t)s1;
+          }
+          const bool o0 = v0 && s0 != (uint32_t)R && s0 != 0;
+          const bool o1 = v1 && s1 != (uint32_t)R && s1 != 0;
+          zeros += (uint32_t)(v0 && !o0) + (uint32_t)(v1 && !o1);
+          if (__any_sync(CSZI_FULL, o0 || o1)) {
+            if (o0) {
+              if (G.hist_smem) atomicAdd(&hs[s0], 1u);
+              else atomicAdd(&hist[s0], 1ull);
+            }
+            if (o1) {
+              if (G.hist_smem) atomicAdd(&hs[s1], 1u);
+              else atomicAdd(&hist[s1], 1ull);
+            }
+          }
         }
       }
     } else {
