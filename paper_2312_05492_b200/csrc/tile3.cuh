@@ -260,7 +260,7 @@ struct QS {
 
 // Exact scalar quantiser (predictor.py:327-339): the rare points the fast
 // path cannot decide, and every point under G.exact.
-__device__ __noinline__ QS quant_slow(double pred, float o32, double leb, double e2, double inv,
+static __device__ __noinline__ QS quant_slow(double pred, float o32, double leb, double e2, double inv,
                                       int R) {
   QS q;
   q.sym = quantize<true>(pred, o32, leb, e2, inv, R, q.rec);
@@ -271,7 +271,7 @@ __device__ __noinline__ QS quant_slow(double pred, float o32, double leb, double
 // (a pass never writes them), so the walk keeps no predictions live.
 // cs: spline case (0 cubic, 1 no +3, 2 no -3, 3 linear), st: neighbour
 // distance in bytes.
-__device__ __noinline__ QS fix_point(uint32_t a, uint32_t st, int cs, double wo, double wi,
+static __device__ __noinline__ QS fix_point(uint32_t a, uint32_t st, int cs, double wo, double wi,
                                      float o32, double leb, double e2, double inv, int R) {
   float v[4];
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[1]) : "r"(a - st));
@@ -316,7 +316,7 @@ struct Out {  // decompress outlier list
   u64 n;
 };
 
-__device__ __noinline__ float outlier_at(const u64 *idx, const float *val, u64 n, u64 flat) {
+static __device__ __noinline__ float outlier_at(const u64 *idx, const float *val, u64 n, u64 flat) {
   return outlier_value(idx, val, n, flat);
 }
 
@@ -372,7 +372,7 @@ DEV int case_interior(int k) {
 // ((w0 a + w1 b) + w2 c) + w3 d is the reference expression (predictor.py
 // :325, missing neighbours enter with weight 0); finite staged data stands
 // in for missing neighbours, which only changes the sign of a zero term.
-__constant__ double c_w[5][4] = {{0.0, 0.0, 0.0, 0.0},
+static __constant__ double c_w[5][4] = {{0.0, 0.0, 0.0, 0.0},
                                  {QO, QN, QF, 0.0},
                                  {0.0, QF, QN, QO},
                                  {0.0, 0.5, 0.5, 0.0},
@@ -755,7 +755,7 @@ DEV void run_pass(const Tile &T, int s, int D, int passed, bool nak, const Lv &L
 // per-phase cycle counters (tools/microbench/t3_phases.py; build with
 // make EXTRA=-DT3_PROF OUT=...): [0] setup [1] TMA wait [2] passes
 // [3] epilogue [4] tiles [6 + 3 lv + i] interior pass (lv, i)
-__device__ unsigned long long g_t3_prof[16];
+static __device__ unsigned long long g_t3_prof[16];
 #define T3P_CLOCK(v) const long long v = clock64()
 #else
 #define T3P_CLOCK(v)
@@ -939,7 +939,7 @@ DEV void stage_rows_u16(uint32_t dst, const uint16_t *sym, const Geo &G, const i
 // out resets its slot for reuse.
 // ---------------------------------------------------------------------------
 constexpr int SCHED_SLOTS = 64;
-__device__ unsigned int g_t3_sched[SCHED_SLOTS * 2];
+static __device__ unsigned int g_t3_sched[SCHED_SLOTS * 2];
 
 struct Sched {
   unsigned int *q;
@@ -981,11 +981,38 @@ DEV void sched_done(unsigned int *q) {
 }
 
 // ---------------------------------------------------------------------------
+// Exact-fit edge tiles (tile3i.cuh fit_mask), per kernel: 0 generic walks,
+// 1 interior walks + FK walks, 3 one FK walk set for interior and exact-fit
+// tiles (fit = 0 on interior tiles).  Measured (r02g, 512^3 / 256x384x384):
+// predict 1: +10% / -4%, 3: -2% / -18%; reconstruct 1: -6% / -8%, 3: -2% /
+// -7% against 0.  The kernels sit at their register caps, so the choice
+// moves the register allocation of the whole kernel, not just edge tiles.
+#ifndef T3_FIT_P
+#define T3_FIT_P 3
+#endif
+#ifndef T3_FIT_R
+#define T3_FIT_R 1
+#endif
+template <int MODE, int FM>
+DEV void run_tile(const Tile &T, const Cfg &C, int R, bool exact, const Out &O) {
+  const int fit = (FM == 0 || !T.bnd) ? 0 : fit_mask(T);
+  if ((MODE == 0 && exact) || (T.bnd && (FM == 0 || fit < 0))) {
+    run_levels<MODE, true>(T, C, R, exact, O);
+  } else if (FM == 3) {
+    run_levels_i<MODE, 1>(T, C, R, O, fit);
+  } else if (!T.bnd) {
+    run_levels_i<MODE, FM == 0 ? 0 : 2>(T, C, R, O);
+  } else {
+    run_levels_i<MODE, 1>(T, C, R, O, fit);
+  }
+}
+
 // kernels: persistent warps take tiles from one queue, interior tiles first
 // (their code has no edge logic), then the edge shell; one tile at a time; the next tile's TMA load is
 // issued as soon as the passes release the staging buffer, so it overlaps
 // the epilogue (code store / histogram, or the float store).
 // ---------------------------------------------------------------------------
+template <int FM>
 __global__ void T3P_BOUNDS
     k_t3_predict(const __grid_constant__ CUtensorMap tm, const float *__restrict__ x, Geo G,
                  const cszi_ctl *__restrict__ ctl, uint16_t *__restrict__ sym,
@@ -1068,8 +1095,9 @@ __global__ void T3P_BOUNDS
     __syncwarp();
     T3P_CLOCK(c2);
     const unsigned int raw = ticket_issue(S, t);
-    if (T.bnd || exact) run_levels<0, true>(T, C, R, exact, O);
-    else run_levels_i<0>(T, C, R, O);
+    // edge tiles whose axes all end on the tile boundary or beyond run the
+    // interior walks with their end cases (FK); the rest the generic walks
+    run_tile<0, FM>(T, C, R, exact, O);
     T3P_CLOCK(c3);
 #ifdef T3_PROF
     if (T.bnd && lane == 0) {  // [5] edge tiles, [15] their pass cycles
@@ -1247,6 +1275,7 @@ DEV float anchor_i(const float *anchors, const Geo &G, const int o[3], int lane)
   return __ldg(anchors + (kz * G.na1 + ky) * G.na2 + kx);
 }
 
+template <int FM>
 __global__ void __launch_bounds__(NT, MINB_R)
     k_t3_reconstruct(const __grid_constant__ CUtensorMap tm, const uint16_t *__restrict__ sym,
                      const float *__restrict__ anchors, const u64 *out_idx,
@@ -1331,8 +1360,7 @@ __global__ void __launch_bounds__(NT, MINB_R)
     }
     __syncwarp();
     const unsigned int raw = ticket_issue(S, t);
-    if (T.bnd) run_levels<1, true>(T, C, R, false, O);
-    else run_levels_i<1>(T, C, R, O);
+    run_tile<1, FM>(T, C, R, false, O);
     const int tn = ticket_read(S, raw);
     int on[3] = {0, 0, 0};
     if (tn < ntiles) {
@@ -1488,9 +1516,10 @@ static bool t3_geo(const cszi_geom *g, int32_t radius, Geo &G) {
   return true;
 }
 
-int launch_predict_t3(const float *x, const cszi_geom *g, int32_t radius,
-                             const cszi_ctl *ctl, uint16_t *sym, u64 *hist, bool exact,
-                             cudaStream_t st, uint32_t *nzmap, bool *nz_done) {
+template <int FM>
+static int predict_t3_impl(const float *x, const cszi_geom *g, int32_t radius,
+                           const cszi_ctl *ctl, uint16_t *sym, u64 *hist, bool exact,
+                           cudaStream_t st, uint32_t *nzmap, bool *nz_done) {
   Geo G;
   if (!t3_geo(g, radius, G)) return CSZI_E_UNSUPPORTED;
   // the non-R bitmap needs every tile row to be one aligned 32-code word
@@ -1505,16 +1534,17 @@ int launch_predict_t3(const float *x, const cszi_geom *g, int32_t radius,
   const int64_t nall = (int64_t)G.nt[0] * G.nt[1] * G.nt[2];
   const size_t smem =
       128 + (size_t)NWP * P_WARP + (G.hist_smem ? sizeof(uint32_t) * 2 * radius : 0);
-  ensure_smem((const void *)k_t3_predict, smem);
-  const unsigned grid = persistent_grid((const void *)k_t3_predict, smem, nall, NWP);
-  k_t3_predict<<<grid, NTP, smem, st>>>(tm, x, G, ctl, sym, hist, nzmap, sched_slot());
+  ensure_smem((const void *)k_t3_predict<FM>, smem);
+  const unsigned grid = persistent_grid((const void *)k_t3_predict<FM>, smem, nall, NWP);
+  k_t3_predict<FM><<<grid, NTP, smem, st>>>(tm, x, G, ctl, sym, hist, nzmap, sched_slot());
   note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
-int launch_recon_t3(const uint16_t *sym, const float *anchors, const u64 *oidx,
-                           const float *oval, u64 nout, const u64 *nout_dev, const cszi_geom *g,
-                           int32_t radius, const LevelCfg &lc, float *y, cudaStream_t st) {
+template <int FM>
+static int recon_t3_impl(const uint16_t *sym, const float *anchors, const u64 *oidx,
+                         const float *oval, u64 nout, const u64 *nout_dev, const cszi_geom *g,
+                         int32_t radius, const LevelCfg &lc, float *y, cudaStream_t st) {
   Geo G;
   if (!t3_geo(g, radius, G) || lc.nlev != 3) return CSZI_E_UNSUPPORTED;
   CUtensorMap tm;
@@ -1523,22 +1553,98 @@ int launch_recon_t3(const uint16_t *sym, const float *anchors, const u64 *oidx,
               : 0;
   const int64_t nall = (int64_t)G.nt[0] * G.nt[1] * G.nt[2];
   const size_t smem = 128 + (size_t)NW * R_WARP;
-  ensure_smem((const void *)k_t3_reconstruct, smem);
-  const unsigned grid = persistent_grid((const void *)k_t3_reconstruct, smem, nall);
-  k_t3_reconstruct<<<grid, NT, smem, st>>>(tm, sym, anchors, oidx, oval, nout, nout_dev, G, lc,
+  ensure_smem((const void *)k_t3_reconstruct<FM>, smem);
+  const unsigned grid = persistent_grid((const void *)k_t3_reconstruct<FM>, smem, nall);
+  k_t3_reconstruct<FM><<<grid, NT, smem, st>>>(tm, sym, anchors, oidx, oval, nout, nout_dev, G, lc,
                                            y, sched_slot());
   note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
+#ifdef T3_PROF
+// read and reset this translation unit's profile counters
+static void t3_prof_take(unsigned long long *out) {
+  unsigned long long v[16];
+  cudaMemcpyFromSymbol(v, g_t3_prof, sizeof(v));
+  for (int i = 0; i < 16; ++i) out[i] += v[i];
+  const unsigned long long z[16] = {0};
+  cudaMemcpyToSymbol(g_t3_prof, z, sizeof(z));
+}
+void t3_prof_fit(unsigned long long *out);
+#endif
+
+// The kernels come in two builds (run_tile's FM): FM = 0 runs every edge
+// tile through the generic walks, the fit build (T3_FIT_P / T3_FIT_R, in
+// t3f.cu) runs exact-fit edge tiles through the interior walks.  Each build
+// is its own register allocation: the fit build is faster where exact-fit
+// tiles are common (512^3: predict -2%, reconstruct -6%) and slower where
+// there are none (449 x 449 x 235: +3%, +8%), so the launch picks per grid.
+int launch_predict_t3_fit(const float *x, const cszi_geom *g, int32_t radius,
+                          const cszi_ctl *ctl, uint16_t *sym, u64 *hist, bool exact,
+                          cudaStream_t st, uint32_t *nzmap, bool *nz_done);
+int launch_recon_t3_fit(const uint16_t *sym, const float *anchors, const u64 *oidx,
+                        const float *oval, u64 nout, const u64 *nout_dev, const cszi_geom *g,
+                        int32_t radius, const LevelCfg &lc, float *y, cudaStream_t st);
+
+#ifdef T3_FIT_TU
+int launch_predict_t3_fit(const float *x, const cszi_geom *g, int32_t radius,
+                          const cszi_ctl *ctl, uint16_t *sym, u64 *hist, bool exact,
+                          cudaStream_t st, uint32_t *nzmap, bool *nz_done) {
+  return predict_t3_impl<T3_FIT_P>(x, g, radius, ctl, sym, hist, exact, st, nzmap, nz_done);
+}
+int launch_recon_t3_fit(const uint16_t *sym, const float *anchors, const u64 *oidx,
+                        const float *oval, u64 nout, const u64 *nout_dev, const cszi_geom *g,
+                        int32_t radius, const LevelCfg &lc, float *y, cudaStream_t st) {
+  return recon_t3_impl<T3_FIT_R>(sym, anchors, oidx, oval, nout, nout_dev, g, radius, lc, y, st);
+}
+#ifdef T3_PROF
+void t3_prof_fit(unsigned long long *out) { t3_prof_take(out); }
+#endif
+#else
+// exact-fit edge tiles (every axis closed or ending on the tile boundary, at
+// least one of the latter) against the other edge tiles (some axis ends
+// inside the tile)
+static bool t3_fit_pays(const cszi_geom *g, int32_t radius) {
+  Geo G;
+  if (!t3_geo(g, radius, G)) return false;
+  const int T3[3] = {TZ, TY, TX};
+  int64_t all = 1, inner = 1, closed = 1;
+  for (int a = 0; a < 3; ++a) {
+    const int64_t o_last = (a == 0 ? G.z0 : 0) + (int64_t)(G.nt[a] - 1) * T3[a];
+    const bool fit = G.nt[a] > G.ni[a] && G.ext[a] - o_last == T3[a];
+    all *= G.nt[a];
+    inner *= G.ni[a] + (fit ? 1 : 0);
+    closed *= G.ni[a];
+  }
+  const int64_t nfit = inner - closed, npart = all - inner;
+  return nfit > 0 && nfit >= npart;
+}
+
+int launch_predict_t3(const float *x, const cszi_geom *g, int32_t radius, const cszi_ctl *ctl,
+                      uint16_t *sym, u64 *hist, bool exact, cudaStream_t st, uint32_t *nzmap,
+                      bool *nz_done) {
+  if (!exact && t3_fit_pays(g, radius))
+    return launch_predict_t3_fit(x, g, radius, ctl, sym, hist, exact, st, nzmap, nz_done);
+  return predict_t3_impl<0>(x, g, radius, ctl, sym, hist, exact, st, nzmap, nz_done);
+}
+
+int launch_recon_t3(const uint16_t *sym, const float *anchors, const u64 *oidx,
+                    const float *oval, u64 nout, const u64 *nout_dev, const cszi_geom *g,
+                    int32_t radius, const LevelCfg &lc, float *y, cudaStream_t st) {
+  if (t3_fit_pays(g, radius))
+    return launch_recon_t3_fit(sym, anchors, oidx, oval, nout, nout_dev, g, radius, lc, y, st);
+  return recon_t3_impl<0>(sym, anchors, oidx, oval, nout, nout_dev, g, radius, lc, y, st);
+}
+#endif
+
 }  // namespace t3
 }  // namespace cszi
 
-#ifdef T3_PROF
-extern "C" int cszi_t3_prof(unsigned long long *out) {  // read and reset
-  cudaMemcpyFromSymbol(out, cszi::t3::g_t3_prof, sizeof(unsigned long long) * 16);
-  const unsigned long long z[16] = {0};
-  cudaMemcpyToSymbol(cszi::t3::g_t3_prof, z, sizeof(z));
+#if defined(T3_PROF) && !defined(T3_FIT_TU)
+extern "C" int cszi_t3_prof(unsigned long long *out) {  // read and reset (both builds)
+  for (int i = 0; i < 16; ++i) out[i] = 0;
+  cszi::t3::t3_prof_take(out);
+  cszi::t3::t3_prof_fit(out);
   return 0;
 }
 #endif

@@ -71,6 +71,45 @@ def test_irregular_3d_shapes_vs_oracle():
             assert P.decompress(blob).data.tobytes() == O.decompress(blob).tobytes()
 
 
+def test_exact_fit_edge_tiles_vs_oracle():
+    """Edge tiles whose axes end exactly on the tile boundary (z, y = 8,
+    x = 32: tile3i.cuh fit_mask) run the interior walks with the end cases;
+    every fit mask, pass order and cubic variant, with outliers and exact
+    redos (noisy data at tight bounds) and the closing anchors they keep."""
+    rng = np.random.default_rng(23)
+    shapes = ((8, 8, 32), (16, 16, 64), (8, 24, 96), (24, 8, 33), (9, 16, 64), (16, 9, 32),
+              (8, 8, 65), (17, 16, 64))
+    for si, shape in enumerate(shapes):
+        for kind in (smooth_field, noisy_field):
+            data = kind(rng, shape)
+            g = P.Grid(P.Dims(shape), data)
+            opts = [dict(eb=1e-3), dict(eb=1e-5), dict(eb=3e-2, mode="abs", quant_radius=4)]
+            order = [(0, 1, 2), (2, 0, 1), (1, 2, 0), (2, 1, 0)][si % 4]
+            variants = [(1, 0, 1), (0, 1, 0)][si % 2]
+            opts.append(dict(eb=1e-4, dim_order=order, variants=variants, alpha=1.25))
+            for o in opts:
+                o = dict(o)
+                eb = o.pop("eb")
+                blob = P.compress(g, eb, **o)
+                assert blob == O.compress(data, eb, **o), (shape, kind.__name__, eb, o)
+                assert P.decompress(blob).data.tobytes() == O.decompress(blob).tobytes(), \
+                    (shape, kind.__name__, eb, o)
+
+
+def test_exact_fit_tiles_match_generic_walks():
+    """The same fields through the generic (exact) walks: byte-identical
+    archives at sizes the oracle would take minutes on."""
+    rng = np.random.default_rng(29)
+    for shape in ((64, 48, 128), (40, 72, 96)):
+        for kind in (smooth_field, noisy_field):
+            data = kind(rng, shape)
+            g = P.Grid(P.Dims(shape), data)
+            for eb in (1e-3, 1e-5):
+                a = P.compress_device(g, eb).to_bytes()
+                b = P.compress_device(g, eb, exact=True).to_bytes()
+                assert a == b, (shape, kind.__name__, eb)
+
+
 def test_compress_predict_matches_oracle():
     rng = np.random.default_rng(5)
     for shape in ((40, 33, 47), (64, 64), (5000,)):

@@ -31,3 +31,4 @@ ni = ((shape[0] - 1) // 8) * ((shape[1] - 1) // 8) * ((shape[2] - 1) // 32)  # i
 for lv in range(3):
     print("level s=%d:" % (4 >> lv), " ".join(f"{buf[6 + lv * 3 + i] / ni:8.0f}" for i in range(3)))
 
+print("edge tiles", buf[5], "pass cycles per edge tile", buf[15] / max(buf[5], 1))
