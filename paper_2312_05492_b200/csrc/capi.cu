@@ -468,7 +468,7 @@ struct GraphEntry {
 };
 static std::mutex g_graph_mu;
 static std::vector<GraphEntry> g_graphs;  // most recently used last
-constexpr size_t GRAPH_CACHE = 16;
+constexpr size_t GRAPH_CACHE = 64;  // batches of snapshots cycle through (x, payload) pairs
 
 static cudaStream_t capture_stream(int dev) {
   static cudaStream_t cs[64] = {};

@@ -362,60 +362,103 @@ int launch_pass2_encode(const uint8_t *in, const u64 *Np, u64 cap_n, uint8_t *ou
 // ---------------------------------------------------------------------------
 // decode
 // ---------------------------------------------------------------------------
-constexpr int P2D_C = 1024;
+#ifndef P2D_CHUNK
+#define P2D_CHUNK 256
+#endif
+constexpr int P2D_C = P2D_CHUNK;  // bytes of the stream per decode chunk
 constexpr int P2D_D = 129;           // entry offsets 0..128
 constexpr int P2D_P = P2D_C + 130;   // local positions incl. spill
 constexpr uint32_t OVR = 0x80000000u;
 
-// (chunk jbase + blockIdx.x: a range of the stream's chunks)
-__global__ void __launch_bounds__(256) k_p2d_tables(const uint8_t *__restrict__ in, u64 n,
-                                                    uint8_t *tab, uint32_t *ctab, u64 jbase) {
-  __shared__ uint16_t nx[2][P2D_P];
-  __shared__ uint32_t ct[2][P2D_P];
-  const u64 jb = jbase + blockIdx.x;
+// Transfer tables by a backward pass over the chunk, one warp per chunk.
+// Every control's successor lies at most 129 bytes ahead (a literal header
+// p jumps to p + b + 2 <= p + 129), so (exit, count) of a position follows
+// from its successor's: X[p] = X[next(p)], C[p] = c(p) + C[next(p)], with
+// positions >= clen terminal (X = p, C = 0).  The warp walks the chunk in
+// 32-byte windows from its end: successors past the window are read from a
+// 256-entry ring in shared memory (they are at most 160 positions ahead),
+// successors inside the window are resolved by pointer jumping over the
+// lanes (<= 5 shuffle rounds).  The windows over positions 0..128 are the
+// table.  (Replaces pointer doubling over all 1154 positions: 4x fewer
+// instructions.)
+constexpr int P2T_WPB = 8;    // warps (chunks) per block
+constexpr int P2T_RING = 256;
+// chunks [jbase, jend) of the stream
+__global__ void __launch_bounds__(P2T_WPB * 32) k_p2d_tables(const uint8_t *__restrict__ in,
+                                                            u64 n, uint8_t *tab, uint32_t *ctab,
+                                                            u64 jbase, u64 jend) {
+  __shared__ uint16_t rx[P2T_WPB][P2T_RING];
+  __shared__ uint32_t rc[P2T_WPB][P2T_RING];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const u64 jb = jbase + (u64)blockIdx.x * P2T_WPB + w;
+  if (jb >= jend) return;
   const u64 c0 = jb * P2D_C;
   const int clen = (int)min((u64)P2D_C, n - c0);
-  for (int p = threadIdx.x; p < P2D_P; p += blockDim.x) {
-    uint16_t x;
-    uint32_t c;
-    if (p < clen) {
-      const uint32_t b = __ldg(in + c0 + p);
-      if (b < 128) {
-        x = (uint16_t)min(p + (int)b + 2, P2D_P - 1);
-        c = b + 1;
-        if (c0 + p + 1 + b + 1 > n) c |= OVR;  // literal overruns the stream
-      } else {
-        x = (uint16_t)(p + 1);
-        c = b - 127;
-      }
+  uint16_t *RX = rx[w];
+  uint32_t *RC = rc[w];
+  const int wtop = ((clen - 1) >> 5) << 5;  // window holding the last control
+  uint32_t bnext = (c0 + wtop + lane < n) ? (uint32_t)__ldg(in + c0 + wtop + lane) : 0u;
+  for (int w0 = wtop; w0 >= 0; w0 -= 32) {
+    const int p = w0 + lane;
+    const uint32_t b = bnext;
+    if (w0 >= 32) bnext = __ldg(in + c0 + w0 - 32 + lane);  // prefetch (always in range)
+    int X;
+    uint32_t acc;
+    int ptr = lane;
+    bool res = true;
+    if (p >= clen) {
+      X = p;
+      acc = 0;
     } else {
-      x = (uint16_t)p;
-      c = 0;
+      int nx;
+      if (b < 128) {
+        nx = p + (int)b + 2;
+        acc = b + 1;
+        if (c0 + p + 1 + b + 1 > n) acc |= OVR;  // literal overruns the stream
+      } else {
+        nx = p + 1;
+        acc = b - 127;
+      }
+      if (nx >= clen) {
+        X = nx;
+      } else if (nx >= w0 + 32) {
+        X = RX[nx & (P2T_RING - 1)];
+        const uint32_t c2 = RC[nx & (P2T_RING - 1)];
+        acc = ((acc & ~OVR) + (c2 & ~OVR)) | ((acc | c2) & OVR);
+      } else {
+        X = 0;
+        ptr = nx - w0;
+        res = false;
+      }
     }
-    nx[0][p] = x;
-    ct[0][p] = c;
-  }
-  __syncthreads();
-  // pointer doubling until every entry walk sits on a terminal (positions
-  // >= clen loop on themselves with count 0, so nothing changes after):
-  // literal-heavy chunks need 4-5 rounds, all-run chunks 10
-  int cur = 0;
-  for (int r = 0; r < 12; ++r) {
-    const bool open = threadIdx.x < P2D_D && nx[cur][threadIdx.x] < clen;
-    if (!__syncthreads_or(open)) break;
-    for (int p = threadIdx.x; p < P2D_P; p += blockDim.x) {
-      const int a = nx[cur][p];
-      nx[cur ^ 1][p] = nx[cur][a];
-      const uint32_t c1 = ct[cur][p], c2 = ct[cur][a];
-      ct[cur ^ 1][p] = ((c1 & ~OVR) + (c2 & ~OVR)) | ((c1 | c2) & OVR);
+    while (!__all_sync(CSZI_FULL, res)) {
+      const int q = ptr;
+      const bool tr = __shfl_sync(CSZI_FULL, res, q);
+      const uint32_t ta = __shfl_sync(CSZI_FULL, acc, q);
+      const int tx = __shfl_sync(CSZI_FULL, X, q);
+      const int tp = __shfl_sync(CSZI_FULL, ptr, q);
+      if (!res) {
+        acc = ((acc & ~OVR) + (ta & ~OVR)) | ((acc | ta) & OVR);
+        if (tr) {
+          X = tx;
+          res = true;
+        } else {
+          ptr = tp;
+        }
+      }
     }
-    __syncthreads();
-    cur ^= 1;
+    RX[p & (P2T_RING - 1)] = (uint16_t)X;
+    RC[p & (P2T_RING - 1)] = acc;
+    if (p < P2D_D) {
+      tab[jb * P2D_D + p] = (uint8_t)(X >= P2D_C ? X - P2D_C : 0);
+      ctab[jb * P2D_D + p] = acc;
+    }
+    __syncwarp();
   }
-  for (int e = threadIdx.x; e < P2D_D; e += blockDim.x) {
-    const int x = nx[cur][e];
-    tab[jb * P2D_D + e] = (uint8_t)(x >= P2D_C ? x - P2D_C : 0);
-    ctab[jb * P2D_D + e] = ct[cur][e];
+  // entries past the last window (clen < 129: the stream's short tail)
+  for (int e = wtop + 32 + lane; e < P2D_D; e += 32) {
+    tab[jb * P2D_D + e] = (uint8_t)(e >= P2D_C ? e - P2D_C : 0);
+    ctab[jb * P2D_D + e] = 0;
   }
 }
 
@@ -581,7 +624,8 @@ int launch_pass2_decode(const uint8_t *in, u64 n, uint8_t *out, u64 cap, void *s
   u64 *off = reinterpret_cast<u64 *>(carve2(p, M * 8));
   void *chain_ws = carve2(p, chain_scratch_bytes(M, P2D_D));
   void *scan_ws = carve2(p, scan_scratch_bytes(M));
-  k_p2d_tables<<<(unsigned)M, 256, 0, st>>>(in, n, tab, ctab, 0);
+  k_p2d_tables<<<(unsigned)((M + P2T_WPB - 1) / P2T_WPB), P2T_WPB * 32, 0, st>>>(in, n, tab,
+                                                                                 ctab, 0, M);
   note_launch();
   launch_chain_resolve(tab, M, P2D_D, 0, E, chain_ws, st);
   k_p2d_counts<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(M, E, ctab, cnt, ctl);
@@ -607,7 +651,8 @@ int launch_p2d_tables_range(const uint8_t *in, u64 n, u64 c0, u64 c1, uint8_t *t
   const u64 M = p2d_chunks(n);
   if (c1 > M) c1 = M;
   if (c1 > c0) {
-    k_p2d_tables<<<(unsigned)(c1 - c0), 256, 0, st>>>(in, n, tab, ctab, c0);
+    k_p2d_tables<<<(unsigned)((c1 - c0 + P2T_WPB - 1) / P2T_WPB), P2T_WPB * 32, 0, st>>>(
+        in, n, tab, ctab, c0, c1);
     note_launch();
   }
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
