@@ -1183,6 +1183,11 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_spec(Stream s, const DecTables *
     }
     p += len;
     cnt++;
+    if (zr && len < 32) {  // the "0" codewords after it in the same window
+      const uint32_t adv = min(min((uint32_t)__clz(w << len), 32u - len), pend - p);
+      p += adv;
+      cnt += adv;
+    }
   }
   spec_exit[j] = pos0 + p;
   spec_cnt[j] = cnt;
@@ -1520,6 +1525,12 @@ __global__ void __launch_bounds__(DEC_NT) k_dec_write_zr(Stream s, const DecTabl
       p += len;
       if (kk >= kskip) o[kk] = (sizeof(OutT) == 4) ? (OutT)((int32_t)sym - R) : (OutT)sym;
       ++kk;
+      if (len < 32) {  // the "0" codewords after it in the same window (run fill wrote them)
+        const uint32_t adv =
+            min(min(min((uint32_t)__clz(w << len), 32u - len), pend - p), kend - kk);
+        p += adv;
+        kk += adv;
+      }
     }
     return;
   }
