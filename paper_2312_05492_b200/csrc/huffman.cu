@@ -1207,8 +1207,12 @@ __global__ void __launch_bounds__(256) k_dec_sync(Stream s, const DecTables *G,
                                                  const uint8_t *spec_dead, const u64 *X_prev,
                                                  const uint8_t *chg_prev, u64 *X, uint32_t *K,
                                                  uint8_t *D, uint8_t *chg, uint32_t *nchg,
-                                                 u64 jbase, const u64 *entry_dev) {
+                                                 u64 jbase, u64 *entry_dev, u64 e0) {
   __shared__ DecSmem T;
+  // nothing moved in iteration 0 (the common case): every later iteration
+  // is a no-op and X already holds the result (the last iteration, `iters`
+  // odd, writes X as iteration 0 did)
+  if (it > 0 && *(nchg - it) == 0) return;
   const u64 j = jbase + blockIdx.x * (u64)blockDim.x + threadIdx.x;
   // iterations > 0: only chunks whose predecessor moved re-walk; blocks
   // without one skip the table load (most of them once the chains meet)
@@ -1221,7 +1225,15 @@ __global__ void __launch_bounds__(256) k_dec_sync(Stream s, const DecTables *G,
   if (!__syncthreads_or(need)) return;
   load_dec_smem(T, G, sorted);
   if (!need) return;
-  const u64 e = (j == jbase) ? *entry_dev : (it == 0) ? spec_exit[j - 1] : X_prev[j - 1];
+  // the range's entry (iteration 0 only: later ones copy chunk jbase): e0,
+  // or ~0 for the speculative exit of chunk jbase - 1; recorded in *entry_dev
+  u64 e;
+  if (j == jbase) {
+    e = (e0 != ~0ull) ? e0 : spec_exit[j - 1];
+    *entry_dev = e;
+  } else {
+    e = (it == 0) ? spec_exit[j - 1] : X_prev[j - 1];
+  }
   const u64 end = min((j + 1) * DEC_C, s.nb);
   BitReader ba, bb;
   ba.init();
@@ -1804,14 +1816,7 @@ static void huff_sync_range(const Stream &s, const DecTables *G, const uint16_t 
   note_launch();
   // the range's entry: 0 at the stream start, else the given one, else the
   // speculative exit of chunk h0 - 1 (device-resident: read by k_dec_sync)
-  const u64 e0 = (h0 == 0) ? 0ull : entry;
-  if (e0 != ~0ull) {
-    k_set_u64<<<1, 1, 0, st>>>(S.entry, e0);
-    note_launch();
-  } else {
-    cudaMemcpyAsync(S.entry, S.spec_exit + (h0 - 1), 8, cudaMemcpyDeviceToDevice, st);
-  }
-  if (entry_used) cudaMemcpyAsync(entry_used, S.entry, 8, cudaMemcpyDeviceToDevice, st);
+  const u64 e0 = (h0 == 0) ? 0ull : entry;  // ~0: k_dec_sync takes spec_exit[h0 - 1]
   const unsigned blocks = (unsigned)((h1 - h0 + 255) / 256);
   // iteration 0 verifies every chunk; later iterations repair chunks whose
   // predecessor did not synchronise (blocks without one exit at once)
@@ -1822,9 +1827,10 @@ static void huff_sync_range(const Stream &s, const DecTables *G, const uint16_t 
     const uint8_t *cp = it ? ((it & 1) ? S.chg0 : S.chg1) : nullptr;
     k_dec_sync<<<blocks, 256, 0, st>>>(s, G, sorted, h1, it, S.spec_exit, S.spec_cnt,
                                        S.spec_dead, Xp, cp, Xo, K, D, co, S.nchg + it, h0,
-                                       S.entry);
+                                       S.entry, e0);
     note_launch();
   }
+  if (entry_used) cudaMemcpyAsync(entry_used, S.entry, 8, cudaMemcpyDeviceToDevice, st);
   cudaMemcpyAsync(&ctl->scratch[1], S.nchg + iters - 1, 4, cudaMemcpyDeviceToDevice, st);
 }
 
