@@ -17,11 +17,13 @@ namespace cszi {
 int launch_ctl_init(cszi_ctl *ctl, cudaStream_t st);
 int launch_range(const float *x, uint64_t n, cszi_ctl *ctl, cudaStream_t st);
 int launch_tune(const float *x, const cszi_geom *g, const cszi_params *p, cszi_ctl *ctl,
-                int32_t *vals, cudaStream_t st, bool reset_outputs = false);
+                int32_t *vals, cudaStream_t st, bool reset_outputs = false,
+                u64 *zero_hist = nullptr, int nzero = 0);
 int launch_sample_gather(const float *x, const cszi_geom *g, int32_t *vals, cudaStream_t st,
                          cszi_ctl *reset_ctl = nullptr);
 int launch_tune_from_samples(const int32_t *vals, const cszi_geom *g, const cszi_params *p,
-                             cszi_ctl *ctl, cudaStream_t st);
+                             cszi_ctl *ctl, cudaStream_t st, u64 *zero_hist = nullptr,
+                             int nzero = 0);
 uint64_t slab_anchor_count(const cszi_geom *g);
 int launch_concat_bits(uint8_t *dst, u64 dst_bit, const uint8_t *src, u64 nbits,
                        cudaStream_t st);
@@ -470,6 +472,16 @@ static std::mutex g_graph_mu;
 static std::vector<GraphEntry> g_graphs;  // most recently used last
 constexpr size_t GRAPH_CACHE = 64;  // batches of snapshots cycle through (x, payload) pairs
 
+// side stream of the current device for forked branches inside a call
+static cudaStream_t side_stream() {
+  static cudaStream_t ss[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!ss[dev]) cudaStreamCreateWithFlags(&ss[dev], cudaStreamNonBlocking);
+  return ss[dev];
+}
+
 static cudaStream_t capture_stream(int dev) {
   static cudaStream_t cs[64] = {};
   if (dev < 0 || dev >= 64) return nullptr;
@@ -569,11 +581,33 @@ static int compress_body(const float *x, const cszi_geom *g, const cszi_params *
   const u64 raw_cap = raw_capacity(g, R, caps);
   if (!range_done) {
     CK(launch_ctl_init(ctl, st));
-    CK(launch_range(x, n, ctl, st));
+    // the sample gather reads only x: it runs on a side stream beside the
+    // range scan (a fork / join in the captured graph), the decision waits
+    // for both
+    cudaStream_t side = side_stream();
+    cudaEvent_t fork = nullptr, join = nullptr;
+    if (side) {
+      cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+    }
+    if (side && fork && join) {
+      cudaEventRecord(fork, st);
+      cudaStreamWaitEvent(side, fork, 0);
+      CK(launch_sample_gather(x, g, W.samples, side));
+      cudaEventRecord(join, side);
+      CK(launch_range(x, n, ctl, st));
+      cudaStreamWaitEvent(st, join, 0);
+    } else {
+      CK(launch_range(x, n, ctl, st));
+      CK(launch_sample_gather(x, g, W.samples, st));
+    }
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+    CK(launch_tune_from_samples(W.samples, g, p, ctl, st, W.hist, (int)nbins));
+  } else {
+    // a prior range scan is kept; its output fields are reset by the sample gather
+    CK(launch_tune(x, g, p, ctl, W.samples, st, true, W.hist, (int)nbins));
   }
-  // a prior range scan is kept; its output fields are reset by the sample gather
-  CK(launch_tune(x, g, p, ctl, W.samples, st, range_done != 0));
-  cudaMemsetAsync(W.hist, 0, 8 * nbins, st);
   bool nz = false;
   CK(launch_predict(x, g, R, ctl, W.sym, W.hist, p->exact != 0, st, W.nzmap, &nz));
   uint8_t *raw = pass2 ? W.raw : payload;

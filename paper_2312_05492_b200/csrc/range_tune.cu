@@ -216,13 +216,17 @@ __global__ void __launch_bounds__(1024) k_sample_gather(const float *__restrict_
 // select_config + plan_levels from the gathered samples; the error sums are
 // accumulated in the reference's order (mesh order, per (d, v)).
 __global__ void __launch_bounds__(256) k_tune_decide(const int32_t *__restrict__ vals,
-                                                     TuneArgs A, cszi_ctl *ctl) {
+                                                     TuneArgs A, cszi_ctl *ctl, u64 *zero_hist,
+                                                     int nzero) {
   __shared__ SamplePlan sp;
   __shared__ double errs[64][3][2];
   __shared__ double err_sum[3][2];
   __shared__ int64_t cnt[3];
   const int tid = threadIdx.x;
   const int rank = A.rank, pad = A.pad_axes;
+  // the predictor's histogram bins (a memset node in the graph would cost a
+  // few us of gap on each side)
+  for (int i = tid; i < nzero; i += blockDim.x) zero_hist[i] = 0;
   if (tid == 0) sample_plan(A, sp);
   __syncthreads();
   const int P = sp.P;
@@ -381,21 +385,21 @@ int launch_sample_gather(const float *x, const cszi_geom *g, int32_t *vals, cuda
 }
 
 int launch_tune_from_samples(const int32_t *vals, const cszi_geom *g, const cszi_params *p,
-                             cszi_ctl *ctl, cudaStream_t st) {
+                             cszi_ctl *ctl, cudaStream_t st, u64 *zero_hist, int nzero) {
   TuneArgs A;
   const int rc = tune_args(g, p, A);
   if (rc != CSZI_OK) return rc;
-  k_tune_decide<<<1, 256, 0, st>>>(vals, A, ctl);
+  k_tune_decide<<<1, 256, 0, st>>>(vals, A, ctl, zero_hist, zero_hist ? nzero : 0);
   note_launch();
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
 // single device: gather (into ctl->scratch-sized device buffer) + decide
 int launch_tune(const float *x, const cszi_geom *g, const cszi_params *p, cszi_ctl *ctl,
-                int32_t *vals, cudaStream_t st, bool reset_outputs) {
+                int32_t *vals, cudaStream_t st, bool reset_outputs, u64 *zero_hist, int nzero) {
   int rc = launch_sample_gather(x, g, vals, st, reset_outputs ? ctl : nullptr);
   if (rc != CSZI_OK) return rc;
-  return launch_tune_from_samples(vals, g, p, ctl, st);
+  return launch_tune_from_samples(vals, g, p, ctl, st, zero_hist, nzero);
 }
 
 }  // namespace cszi
