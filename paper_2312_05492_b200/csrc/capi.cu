@@ -579,11 +579,13 @@ static int compress_body(const float *x, const cszi_geom *g, const cszi_params *
   const u64 nbins = 2 * (u64)R;
   const u64 na = anchors_count(g);
   const u64 raw_cap = raw_capacity(g, R, caps);
+  uint8_t *raw = pass2 ? W.raw : payload;
+  bool anchors_done = false;
   if (!range_done) {
     CK(launch_ctl_init(ctl, st));
-    // the sample gather reads only x: it runs on a side stream beside the
-    // range scan (a fork / join in the captured graph), the decision waits
-    // for both
+    // the sample gather and the anchor gather read only x: they run on a
+    // side stream beside the range scan (a fork / join in the captured
+    // graph), the decision waits for both
     cudaStream_t side = side_stream();
     cudaEvent_t fork = nullptr, join = nullptr;
     if (side) {
@@ -594,6 +596,8 @@ static int compress_body(const float *x, const cszi_geom *g, const cszi_params *
       cudaEventRecord(fork, st);
       cudaStreamWaitEvent(side, fork, 0);
       CK(launch_sample_gather(x, g, W.samples, side));
+      CK(launch_gather_anchors(x, g, reinterpret_cast<float *>(raw), side));
+      anchors_done = true;
       cudaEventRecord(join, side);
       CK(launch_range(x, n, ctl, st));
       cudaStreamWaitEvent(st, join, 0);
@@ -610,8 +614,7 @@ static int compress_body(const float *x, const cszi_geom *g, const cszi_params *
   }
   bool nz = false;
   CK(launch_predict(x, g, R, ctl, W.sym, W.hist, p->exact != 0, st, W.nzmap, &nz));
-  uint8_t *raw = pass2 ? W.raw : payload;
-  CK(launch_gather_anchors(x, g, reinterpret_cast<float *>(raw), st));
+  if (!anchors_done) CK(launch_gather_anchors(x, g, reinterpret_cast<float *>(raw), st));
   uint8_t *lengths = raw + 4 * na;  // the codebook section is the length table
   CK(launch_codebook(W.hist, (int)nbins, lengths, W.words, ctl, st, true));
   const u64 head = 4 * na + nbins;
