@@ -11,8 +11,8 @@
 // sizes scanned (look-back), then every byte writes its output independently.
 //
 // Decode = exact per-chunk transfer tables: for each entry offset e in
-// [0, 128] into a 2 KiB chunk (a literal run spills at most 128 bytes into
-// the next chunk) pointer jumping gives the exit offset and output count;
+// [0, 128] into a 256-byte chunk (a literal run spills at most 128 bytes into
+// the next chunk) one backward pass gives the exit offset and output count;
 // the chain resolver composes the tables; each chunk then walks its true
 // control chain and expands it cooperatively.
 #include "common.cuh"
