@@ -434,11 +434,14 @@ __global__ void __launch_bounds__(P2T_WPB * 32) k_p2d_tables(const uint8_t *__re
       }
     }
     while (!__all_sync(CSZI_FULL, res)) {
+      // (exit | lane pointer | resolved) in one word: two shuffles a round
       const int q = ptr;
-      const bool tr = __shfl_sync(CSZI_FULL, res, q);
+      const uint32_t pk = ((uint32_t)X << 6) | ((uint32_t)ptr << 1) | (res ? 1u : 0u);
+      const uint32_t tpk = __shfl_sync(CSZI_FULL, pk, q);
       const uint32_t ta = __shfl_sync(CSZI_FULL, acc, q);
-      const int tx = __shfl_sync(CSZI_FULL, X, q);
-      const int tp = __shfl_sync(CSZI_FULL, ptr, q);
+      const bool tr = tpk & 1u;
+      const int tx = (int)(tpk >> 6);
+      const int tp = (int)((tpk >> 1) & 31u);
       if (!res) {
         acc = ((acc & ~OVR) + (ta & ~OVR)) | ((acc | ta) & OVR);
         if (tr) {
