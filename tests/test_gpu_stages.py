@@ -146,3 +146,31 @@ def test_profile_and_gather_anchors():
         idx = O.anchor_flat_indices(shape, 8)
         assert [i for i, _ in anchors] == idx.tolist()
         assert [v for _, v in anchors] == data.ravel()[idx].tolist()
+
+
+def test_pass2_decode_chunk_boundaries():
+    """Encoded streams built control by control so literal payloads (up to
+    128 bytes) and zero-run controls straddle the decoder's 256-byte chunks
+    at every offset: the transfer tables' spill entries (0..128), a chunk
+    whose first bytes are the previous chunk's payload, streams ending inside
+    a chunk, and an overrun in the last chunk -- vs the oracle."""
+    rng = np.random.default_rng(23)
+    for trial in range(60):
+        out = bytearray()
+        target = int(rng.integers(1, 3000))
+        while len(out) < target:
+            if rng.random() < 0.5:
+                k = int(rng.integers(1, 129))
+                out.append(k - 1)
+                out += bytes(rng.integers(0, 256, k).astype(np.uint8))
+            else:
+                out.append(int(rng.integers(128, 256)))
+        enc = bytes(out)
+        assert P.pass2_decode(enc) == O.pass2_decode(enc), trial
+    # a literal header at every offset of the chunk's last 130 bytes
+    for off in range(256 - 130, 257):
+        body = bytes([0xFF]) * off + bytes([127]) + bytes(rng.integers(0, 256, 128).astype(np.uint8))
+        enc = body + bytes([0x80, 5, 1, 2, 3, 4, 5, 6])
+        assert P.pass2_decode(enc) == O.pass2_decode(enc), off
+        with pytest.raises(P.Corrupt):
+            P.pass2_decode(body[:-1])  # the literal overruns the stream
