@@ -1148,9 +1148,11 @@ DEV bool zrun_tables(const DecTables *G) { return G->counts[1] == 1 && G->first_
 __global__ void __launch_bounds__(DEC_NT) k_dec_spec(Stream s, const DecTables *G,
                                                     const uint16_t *sorted, u64 M, u64 *spec_exit,
                                                     uint32_t *spec_cnt, uint8_t *spec_dead,
-                                                    u64 jbase) {
+                                                    u64 jbase, u64 *fd_init) {
   __shared__ DecSmem T;
   __shared__ uint32_t sw[DEC_SW];
+  // the write phase's first-dead-chunk minimum starts at ~0 (no set kernel)
+  if (fd_init && blockIdx.x == 0 && threadIdx.x == 0) *fd_init = ~0ull;
   const u64 j0 = jbase + (u64)blockIdx.x * DEC_NT;
   SmemStream ss;
   stage_words(sw, s, j0, ss);
@@ -1310,8 +1312,11 @@ __global__ void __launch_bounds__(256) k_dec_sync(Stream s, const DecTables *G,
 // Phase 3 (after the generic exclusive scan of K into off): truncation
 // check.  Decodable symbols = offset + count of the first chunk whose chain
 // dies (invalid code / exhausted stream), or the total when none dies.
-__global__ void k_dec_first_dead(u64 M, const uint8_t *D, u64 *first_dead) {
+__global__ void k_dec_first_dead(u64 M, const uint8_t *D, u64 *first_dead,
+                                 const uint32_t *nchg_last, u64 *nchg_out) {
   const u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+  // chains still moving after the last sync iteration -> ctl (no copy node)
+  if (nchg_out && j == 0) *nchg_out = *nchg_last;
   if (j < M && D[j]) atomicMin(first_dead, j);
 }
 // decoded-symbol count / truncation check, run by thread 0 of block 0 of
@@ -1802,17 +1807,21 @@ static SyncScratch carve_sync(unsigned char *&p, u64 M) {
 static void huff_sync_range(const Stream &s, const DecTables *G, const uint16_t *sorted, u64 M,
                             u64 h0, u64 h1, u64 entry, u64 *X, uint32_t *K, uint8_t *D,
                             u64 *entry_used, const SyncScratch &S, cszi_ctl *ctl,
-                            cudaStream_t st, int iters = 3) {
+                            cudaStream_t st, int iters = 3, u64 *fd_init = nullptr) {
   // iters is odd: the last iteration writes X (even iterations write X,
   // odd ones the scratch copy)
   launch_zero16(S.nchg, 64, st);
   if (h1 <= h0) {
     cudaMemcpyAsync(&ctl->scratch[1], S.nchg, 4, cudaMemcpyDeviceToDevice, st);
+    if (fd_init) {
+      k_set_u64<<<1, 1, 0, st>>>(fd_init, ~0ull);
+      note_launch();
+    }
     return;
   }
   const u64 sb = (h0 > 0 && entry == ~0ull) ? h0 - 1 : h0;  // speculate h0 - 1 for the entry
   k_dec_spec<<<(unsigned)((h1 - sb + DEC_NT - 1) / DEC_NT), DEC_NT, 0, st>>>(
-      s, G, sorted, h1, S.spec_exit, S.spec_cnt, S.spec_dead, sb);
+      s, G, sorted, h1, S.spec_exit, S.spec_cnt, S.spec_dead, sb, fd_init);
   note_launch();
   // the range's entry: 0 at the stream start, else the given one, else the
   // speculative exit of chunk h0 - 1 (device-resident: read by k_dec_sync)
@@ -1831,26 +1840,41 @@ static void huff_sync_range(const Stream &s, const DecTables *G, const uint16_t 
     note_launch();
   }
   if (entry_used) cudaMemcpyAsync(entry_used, S.entry, 8, cudaMemcpyDeviceToDevice, st);
-  cudaMemcpyAsync(&ctl->scratch[1], S.nchg + iters - 1, 4, cudaMemcpyDeviceToDevice, st);
+  // (fd_init: the whole-stream decode, whose write phase copies the count)
+  if (!fd_init)
+    cudaMemcpyAsync(&ctl->scratch[1], S.nchg + iters - 1, 4, cudaMemcpyDeviceToDevice, st);
 }
 
 // Phase 3-4 over all M chunks: exclusive scan of the symbol counts,
 // truncation check, and the write of the symbol window [w0, w1).
+// first_dead of huff_write's scratch starting at p (the same carving)
+static u64 *write_first_dead(unsigned char *p, u64 M) {
+  carve(p, M * 8);
+  return reinterpret_cast<u64 *>(carve(p, 64)) + 2;
+}
+
+// fd_ready: first_dead was set by the speculative decode and the sync's
+// moving-chain count (*nchg_last) goes to ctl->scratch[1] here
 static void huff_write(const Stream &s, const DecTables *G, const uint16_t *sorted, u64 M,
                        const u64 *X, uint32_t *K, const uint8_t *D, u64 n, int R, void *out,
                        int out_kind, u64 w0, u64 w1, unsigned char *p, cszi_ctl *ctl,
-                       cudaStream_t st) {
+                       cudaStream_t st, bool fd_ready = false,
+                       const uint32_t *nchg_last = nullptr) {
   u64 *off = reinterpret_cast<u64 *>(carve(p, M * 8));
   u64 *misc = reinterpret_cast<u64 *>(carve(p, 64));
   u64 *first_dead = misc + 2;
   u64 *total = misc + 3;
   void *scan_ws = carve(p, scan_scratch_bytes(M));
-  k_set_u64<<<1, 1, 0, st>>>(first_dead, ~0ull);  // (a kernel: no memset node)
-  note_launch();
+  if (!fd_ready) {
+    k_set_u64<<<1, 1, 0, st>>>(first_dead, ~0ull);  // (a kernel: no memset node)
+    note_launch();
+  }
   const unsigned blocks = (unsigned)((M + 255) / 256);
   const unsigned dblocks = (unsigned)((M + DEC_NT - 1) / DEC_NT);
   launch_excl_scan_u32(K, M, off, total, scan_ws, st);
-  k_dec_first_dead<<<blocks, 256, 0, st>>>(M, D, first_dead);
+  k_dec_first_dead<<<blocks, 256, 0, st>>>(M, D, first_dead, nchg_last,
+                                           nchg_last ? reinterpret_cast<u64 *>(&ctl->scratch[1])
+                                                     : nullptr);
   note_launch();
   const DecCheck C{first_dead, total, ctl};
   if (out_kind == 0) {
@@ -1887,12 +1911,15 @@ int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *de
   u64 *X0 = reinterpret_cast<u64 *>(carve(p, M * 8));
   uint32_t *K = reinterpret_cast<uint32_t *>(carve(p, M * 4));
   uint8_t *D = carve(p, M);
+  const uint32_t *nchg_last = nullptr;
   if (!table_mode) {
     const SyncScratch S = carve_sync(p, M);
     // the whole stream is one range entering at bit 0; a chain still moving
     // after three iterations is reported in ctl->scratch[1] and the caller
     // reruns in table mode
-    huff_sync_range(s, G, sorted, M, 0, M, 0, X0, K, D, nullptr, S, ctl, st);
+    huff_sync_range(s, G, sorted, M, 0, M, 0, X0, K, D, nullptr, S, ctl, st, 3,
+                    write_first_dead(p, M));
+    nchg_last = S.nchg + 2;
   } else {
     if (lmax < 1 || lmax > 32) lmax = 32;
     uint8_t *tab = carve(p, M * lmax);
@@ -1909,7 +1936,8 @@ int launch_decode(const uint8_t *bytes, u64 nbytes, u64 n, int R, const void *de
     k_dec_from_tab<<<blocks, 256, 0, st>>>(M, lmax, E, ktab, dtab, X0, K, D);
     note_launch();
   }
-  huff_write(s, G, sorted, M, X0, K, D, n, R, out, out_kind, w0, w1, p, ctl, st);
+  huff_write(s, G, sorted, M, X0, K, D, n, R, out, out_kind, w0, w1, p, ctl, st,
+             nchg_last != nullptr, nchg_last);
   return cudaGetLastError() == cudaSuccess ? CSZI_OK : CSZI_E_CUDA;
 }
 
