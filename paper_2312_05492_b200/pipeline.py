@@ -212,7 +212,11 @@ def compress_device(grid: Grid, eb: float, mode: str = "rel", predictor: str = "
             grid.dims.extents, layout, mode == "rel", float(eb), R, a, variants, dim_order,
             bool(exact), worst)
         ws = _lib.WS.get(ws_bytes, "compress")
-        pay = _payload_buf(pcap)
+        # the graph writes a per-stream staging buffer (stable pointers: a
+        # fresh capacity-sized buffer per call gave the replayed graph a new
+        # argument set whenever the allocator handed out another address);
+        # the archive gets its own exact-length copy below
+        pay = _lib.WS.get(pcap, "payload")
         _lib.check(lib.cszi_compress(_lib.ptr(x), ctypes.byref(geom), ctypes.byref(params),
                                      ctypes.byref(caps), dev_pass2, 1 if range_done else 0,
                                      _lib.ptr(pay), _lib.ptr(ws), ws.numel(), ctl.ptr, st),
@@ -237,7 +241,7 @@ def compress_device(grid: Grid, eb: float, mode: str = "rel", predictor: str = "
         raise RuntimeError("compress: output capacity exceeded at worst-case sizing")
     na = count_anchors(grid.dims, layout.anchor_stride)
     sec = (4 * na, 2 * R, (int(c.bits) + 7) // 8, 8 + 12 * int(c.n_outliers))
-    payload = pay[: int(c.payload_len)]
+    payload = pay[: int(c.payload_len)].clone()  # stream-ordered before the next call's graph
     if codec_enc is not None:
         raw = payload.cpu().numpy().tobytes()
         payload = bytes(codec_enc(raw))
